@@ -1,0 +1,192 @@
+/*
+ * bsg.h -- C ABI of the B200-native integer-sorting hot path of
+ * arXiv 1708.09495 (Gerbessiotis, "Integer sorting on multicores").
+ *
+ * The reference (/root/reference/proj/include/bspsort/, header-only C++20)
+ * exposes no FFI; its "operator API" is a set of C++ free functions taking
+ * std::vector<uint32_t>.  Each entry point below replaces one of them (cited
+ * file:line), with plain pointers and sizes.  The C++ mirror of the reference
+ * signatures is include/bspsort_b200/bspsort.hpp (header-only, calls this ABI);
+ * the Python mirror is paper_1708_09495_b200/ (ctypes).
+ *
+ * Conventions
+ *  - Every function returns BSG_OK (0) or a positive status; the thread-local
+ *    message of the last failure is bsg_last_error().  BSG_EINVAL plays the
+ *    role of the reference's std::invalid_argument, BSG_EPROTO of bsp::bsp_error.
+ *  - mem_kind BSG_MEM_DEVICE: in/out are device pointers on the context's GPU;
+ *    the call only enqueues work on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and returns.  BSG_MEM_HOST: in/out are host pointers
+ *    (pinned for full PCIe speed); the call copies in, sorts, copies out and
+ *    synchronises `stream` before returning -- the reference's synchronous
+ *    by-value semantics (radix.hpp:180, netsort.hpp:157).
+ *  - in == out is allowed everywhere (in-place).
+ *  - Keys are uint32; counts and positions are 64-bit everywhere (n may
+ *    exceed 2^32 on one GPU), fixing the reference's uint32 count blocks
+ *    (radix.hpp:238-243) which wrap at 2^32 keys per worker.
+ *  - There is no CPU fallback: without a usable GPU every compute entry point
+ *    fails with BSG_ECUDA.
+ */
+#ifndef BSG_H_
+#define BSG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSG_ABI_VERSION 1
+
+enum bsg_status {
+    BSG_OK = 0,
+    BSG_EINVAL = 1, /* invalid argument (reference: std::invalid_argument) */
+    BSG_EPROTO = 2, /* protocol / consistency failure (reference: bsp::bsp_error) */
+    BSG_ECUDA = 3,  /* CUDA runtime error or no GPU */
+    BSG_ENOMEM = 4, /* device or host allocation failed */
+    BSG_ENCCL = 5   /* reserved for in-library collectives */
+};
+
+enum bsg_mem_kind { BSG_MEM_HOST = 0, BSG_MEM_DEVICE = 1 };
+
+/* core.hpp:24 enum class Algorithm { SR4, PR4, PR2, BTN, OET } (same order) */
+enum bsg_algorithm { BSG_SR4 = 0, BSG_PR4 = 1, BSG_PR2 = 2, BSG_BTN = 3, BSG_OET = 4 };
+
+/* netsort.hpp: BTN = bitonic_schedule (70-89), OET = odd_even_rounds (95-108) */
+enum bsg_network { BSG_NET_BTN = 0, BSG_NET_OET = 1 };
+
+/* bsp.hpp:86-92 RunStats, synthesised with the reference semantics. */
+typedef struct bsg_run_stats {
+    int32_t supersteps;
+    uint64_t messages_sent;
+    uint64_t messages_delivered;
+    uint64_t words_sent;
+    uint64_t words_delivered;
+} bsg_run_stats;
+
+typedef struct bsg_ctx bsg_ctx;
+
+/* ---- library / context ------------------------------------------------ */
+int bsg_abi_version(void);
+const char* bsg_last_error(void);
+/* Number of kernel launches this context has enqueued since creation. */
+uint64_t bsg_ctx_launch_count(const bsg_ctx* ctx);
+
+/* Binds a context to CUDA device `device`.  The context owns the cached
+ * device workspace (so no cudaMalloc happens on a warm path).  A context
+ * serialises its calls internally; use one per host thread for concurrency. */
+int bsg_ctx_create(int device, bsg_ctx** out);
+int bsg_ctx_destroy(bsg_ctx* ctx);
+/* Pre-sizes the workspace for sorts of up to n keys (optional). */
+int bsg_ctx_reserve(bsg_ctx* ctx, uint64_t n);
+
+/* ---- host-side helpers (no GPU needed) -------------------------------- */
+/* core.hpp:93-99 generate_uniform_keys: mt19937_64(seed), low 32 bits. */
+int bsg_generate_uniform_u32(uint32_t* out, uint64_t n, uint64_t seed);
+/* bench.hpp:77-88 derive_seed (splitmix64). */
+uint64_t bsg_derive_seed(uint64_t seed, int32_t rep);
+/* core.hpp:60-64 digit_bits + radix.hpp:143-151 checked_digit_bits:
+ * lg r for r in {2,4,16,256,65536}, else -1 (and sets the error message). */
+int bsg_checked_digit_bits(uint64_t radix);
+/* Builder-defined skewed inputs for config 3 (not in the
+ * reference): kind 0 = uniform keys & 0xFFFF, 1 = Zipf(s) over ranks
+ * 1..2^32 (key = rank-1) by rejection-inversion driven by mt19937_64(seed),
+ * 2 = all keys 0xABCD1234 (acceptance.cpp:63). */
+int bsg_generate_skewed_u32(uint32_t* out, uint64_t n, uint64_t seed, int kind, double zipf_s);
+/* netsort.hpp:70-89 / 95-108: stage-major partner[s*p+i] (-1 = idle) and
+ * keep_low[s*p+i]; *stages receives the stage count (only the first
+ * cap_stages are written). */
+int bsg_network_schedule(int network, int p, int32_t* partner, int32_t* keep_low, int cap_stages,
+                         int* stages);
+/* radix.hpp:207-229 detail::Partition */
+uint64_t bsg_partition_size_of(uint64_t n, int p, int w);
+uint64_t bsg_partition_offset_of(uint64_t n, int p, int w);
+int bsg_partition_owner_of(uint64_t n, int p, uint64_t pos);
+
+/* ---- sorts ------------------------------------------------------------ */
+/* radix.hpp:180-201 serial_radix_sort(KeyArray, radix): 32/lg r stable
+ * count-sort rounds (SR4 when r = 256).  Output is ascending. */
+int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
+                       int radix_log2, int mem_kind, void* stream);
+
+/* radix.hpp:155-176 count_sort_round(keys, round, radix): one stable pass
+ * over digit `round` (low digit first).  radix_log2 in {1,2,4,8,16}. */
+int bsg_count_sort_round_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
+                             int round, int radix_log2, int mem_kind, void* stream);
+
+/* netsort.hpp:30-51 merge_split(a, b): low = |a| smallest of a U b, high =
+ * |b| largest, both ascending; a and b must each be ascending. */
+int bsg_merge_split_u32(bsg_ctx* ctx, const uint32_t* a, uint64_t na, const uint32_t* b,
+                        uint64_t nb, uint32_t* low, uint32_t* high, int mem_kind, void* stream);
+
+/* netsort.hpp:124-199 prepare_btn/prepare_oet + run_block_network over a
+ * BATCH of independent arrays (the reference sorts one array per call;
+ * SURVEY §8(b)).  in/out hold num_arrays consecutive arrays of `len` keys.
+ * Each array is padded to p*ceil(len/p) with 0xFFFFFFFF, blocks are sorted
+ * locally, then the network's merge-split stages run.  stages_limit < 0 runs
+ * all stages and writes the stripped len keys per array; stages_limit >= 0
+ * stops early and writes the padded p*ceil(len/p) block states per array
+ * (out must then hold num_arrays*p*ceil(len/p) keys).  `stats` (optional)
+ * receives one array's RunStats. */
+int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in, uint32_t* out,
+                                  uint64_t num_arrays, uint32_t len, int p, int stages_limit,
+                                  bsg_run_stats* stats, int mem_kind, void* stream);
+
+/* radix.hpp:344-414 prepare_parallel_radix + run_parallel_radix (PR4 at
+ * r=256, PR2 at r=65536) with p logical workers resident on the context's
+ * GPU: per round a digit count per worker, the p x r count exchange, the
+ * stable local pass, slice routing and the rebuild, all as kernels.
+ * rounds_limit >= 0 stops after that many rounds (the reference's
+ * plan.rounds override) -- the concatenated per-worker blocks are then the
+ * intermediate state.  Multi-GPU (one process per GPU) runs the same steps
+ * through paper_1708_09495_b200.distributed over NCCL. */
+int bsg_parallel_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
+                                int p, int radix_log2, int rounds_limit, bsg_run_stats* stats,
+                                int mem_kind, void* stream);
+
+/* bspsort.hpp:15-25 sort_instance: validate (core.hpp:74-88) + dispatch. */
+int bsg_sort_instance_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
+                          int processors, int algorithm, uint64_t radix, int mem_kind,
+                          void* stream);
+
+/* ---- parallel-radix step kernels (one rank = one GPU) -------------------
+ * The building blocks of one PR round on one worker, exported so a host
+ * orchestrator (Python over torch.distributed / NCCL) can interleave them
+ * with the collectives.  All pointers are device pointers, all calls are
+ * asynchronous on `stream`.  Counts are uint64. */
+
+/* radix.hpp:238-243 count_digits: counts[d] = #{keys in block with digit d}. */
+int bsg_pr_count_digits(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round,
+                        int radix_log2, uint64_t* counts, void* stream);
+
+/* radix.hpp:248-290 digit_starts + the routing part of sort_and_scatter,
+ * from the gathered count matrix counts[v*r + d] (p x r, device):
+ *   send_counts[w] = #keys worker `me` sends to worker w,
+ *   recv_counts[v] = #keys worker `me` receives from worker v,
+ *   rebuild_delta[v*r + d] (int64) = where the keys of digit d received from
+ *   v land in me's rebuilt block: out_index = rebuild_delta + index within
+ *   the received (source-major) buffer.  Host-visible outputs are device
+ *   arrays; copy send/recv counts back to size the exchange. */
+int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me, int round,
+                int radix_log2, uint64_t* send_counts, uint64_t* recv_counts,
+                int64_t* rebuild_delta, void* stream);
+
+/* radix.hpp:262-290 sort_and_scatter's local stable count-sort: sorted =
+ * count_sort_round(block, round, radix).  Because global positions increase
+ * along the digit-sorted block, the slice for worker w is the contiguous
+ * range [sum(send_counts[<w]), +send_counts[w]) of `sorted` -- no per-key
+ * owner_of division. */
+int bsg_pr_local_sort(bsg_ctx* ctx, const uint32_t* block, uint32_t* sorted, uint64_t len,
+                      int round, int radix_log2, void* stream);
+
+/* radix.hpp:295-333 gather_slices: rebuilds the block from the source-major
+ * receive buffer (recv_len keys) by scattering each key to
+ * rebuild_delta[src*r + digit] + index. */
+int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len,
+                   const uint64_t* recv_counts, int p, int round, int radix_log2,
+                   const int64_t* rebuild_delta, uint32_t* block, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSG_H_ */

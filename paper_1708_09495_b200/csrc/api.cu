@@ -1,0 +1,363 @@
+// api.cu -- C ABI implementation (include/bsg.h): contexts, workspace, the
+// host<->device staging of BSG_MEM_HOST calls, argument validation with the
+// reference's error behaviour, and dispatch to the kernels.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "context.cuh"
+#include "netsort.cuh"
+#include "pr.cuh"
+#include "radix.cuh"
+
+namespace bsg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return e == cudaErrorMemoryAllocation ? BSG_ENOMEM : BSG_ECUDA;
+}
+
+} // namespace bsg
+
+using namespace bsg;
+
+int bsg_ctx::radix_ws(uint64_t n, RadixWorkspace* ws) {
+    const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
+    cudaError_t e;
+    if ((e = tmp.ensure(std::max<uint64_t>(n, 4) * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "workspace tmp");
+    if ((e = status.ensure(onesweep_status_words(std::max<uint64_t>(n, 1)) * sizeof(uint32_t))) != cudaSuccess)
+        return cuda_fail(e, "workspace status");
+    if ((e = hist.ensure(chunks * kMaxPasses * 256 * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "workspace hist");
+    if ((e = base.ensure(chunks * kMaxPasses * 256 * sizeof(uint64_t))) != cudaSuccess) return cuda_fail(e, "workspace base");
+    if ((e = plan.ensure(sizeof(PassPlan))) != cudaSuccess) return cuda_fail(e, "workspace plan");
+    ws->tmp = tmp.as<uint32_t>();
+    ws->status = status.as<uint32_t>();
+    ws->hist = hist.as<uint32_t>();
+    ws->base = base.as<uint64_t>();
+    ws->plan = plan.as<PassPlan>();
+    return BSG_OK;
+}
+
+namespace {
+
+struct CallGuard {
+    std::lock_guard<std::mutex> lock;
+    DeviceGuard dev;
+    explicit CallGuard(bsg_ctx* c) : lock(c->mu), dev(c->device) {}
+};
+
+int check_ctx(bsg_ctx* ctx) {
+    if (!ctx) return fail(BSG_EINVAL, "null context");
+    return BSG_OK;
+}
+
+// Runs `body(d_in, d_out, stream)` with device buffers.  For HOST memory the
+// keys are staged through the context's device buffers (H2D, body, D2H) and
+// the stream is synchronised before returning.
+template <class Body>
+int with_device_io(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n_in, uint64_t n_out, int mem_kind,
+                   cudaStream_t stream, Body&& body) {
+    if (mem_kind == BSG_MEM_DEVICE) return body(in, out, stream);
+    if (mem_kind != BSG_MEM_HOST) return fail(BSG_EINVAL, "mem_kind must be BSG_MEM_HOST or BSG_MEM_DEVICE");
+    cudaError_t e;
+    if ((e = ctx->stage_in.ensure(std::max<uint64_t>(n_in, 4) * 4)) != cudaSuccess) return cuda_fail(e, "host staging");
+    if ((e = ctx->stage_out.ensure(std::max<uint64_t>(n_out, 4) * 4)) != cudaSuccess) return cuda_fail(e, "host staging");
+    uint32_t* d_in = ctx->stage_in.as<uint32_t>();
+    uint32_t* d_out = ctx->stage_out.as<uint32_t>();
+    if (n_in && (e = cudaMemcpyAsync(d_in, in, n_in * 4, cudaMemcpyHostToDevice, stream)) != cudaSuccess)
+        return cuda_fail(e, "H2D copy");
+    int rc = body(d_in, d_out, stream);
+    if (rc != BSG_OK) return rc;
+    if (n_out && (e = cudaMemcpyAsync(out, d_out, n_out * 4, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+        return cuda_fail(e, "D2H copy");
+    if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "stream synchronize");
+    return BSG_OK;
+}
+
+int radix_bits_or_fail(int radix_log2) {
+    if (radix_log2 != 1 && radix_log2 != 2 && radix_log2 != 4 && radix_log2 != 8 && radix_log2 != 16) {
+        if (radix_log2 > 16 && radix_log2 <= 32 && 32 % radix_log2 == 0)
+            return fail(BSG_EINVAL, "radix 2^" + std::to_string(radix_log2) +
+                                         " needs a count array larger than memory; use r <= 65536");
+        return fail(BSG_EINVAL, "radix must be a power of two whose bit width divides 32");
+    }
+    return BSG_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int bsg_abi_version(void) { return BSG_ABI_VERSION; }
+const char* bsg_last_error(void) { return g_last_error.c_str(); }
+uint64_t bsg_ctx_launch_count(const bsg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int bsg_ctx_create(int device, bsg_ctx** out) {
+    if (!out) return fail(BSG_EINVAL, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount (no usable GPU; there is no CPU fallback)");
+    if (device < 0 || device >= count) return fail(BSG_EINVAL, "device index out of range");
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10) return fail(BSG_ECUDA, std::string("kernels are built for sm_100a; device is ") + prop.name);
+    auto* c = new (std::nothrow) bsg_ctx();
+    if (!c) return fail(BSG_ENOMEM, "context allocation");
+    c->device = device;
+    *out = c;
+    return BSG_OK;
+}
+
+int bsg_ctx_destroy(bsg_ctx* ctx) {
+    if (!ctx) return BSG_OK;
+    {
+        CallGuard g(ctx);
+        for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
+                          &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
+                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32})
+            b->release();
+    }
+    delete ctx;
+    return BSG_OK;
+}
+
+int bsg_ctx_reserve(bsg_ctx* ctx, uint64_t n) {
+    if (int rc = check_ctx(ctx)) return rc;
+    CallGuard g(ctx);
+    RadixWorkspace ws;
+    return ctx->radix_ws(n, &ws);
+}
+
+int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int radix_log2, int mem_kind,
+                       void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = radix_bits_or_fail(radix_log2)) return rc;
+    if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
+    CallGuard g(ctx);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
+        RadixWorkspace ws;
+        if (int rc = ctx->radix_ws(n, &ws)) return rc;
+        // Any digit width yields the same stable LSD result (the output of
+        // serial_radix_sort is independent of r); 8-bit passes are used for
+        // lg r <= 8.  r = 2^16 runs each 16-bit round as two stable 8-bit
+        // sub-passes (low byte then high byte of the digit), which is
+        // bit-identical to count_sort_round(., round, 65536).
+        const int l = launch_radix_sort8(d_in, d_out, n, ws, s, true);
+        if (l < 0) return cuda_fail(cudaGetLastError(), "radix sort launch");
+        ctx->launches += static_cast<uint64_t>(l);
+        return BSG_OK;
+    });
+}
+
+int bsg_count_sort_round_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int round, int radix_log2,
+                             int mem_kind, void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = radix_bits_or_fail(radix_log2)) return rc;
+    const int rounds = 32 / radix_log2;
+    if (round < 0 || round >= rounds)
+        return fail(BSG_EINVAL, "round " + std::to_string(round) + " outside [0, " + std::to_string(rounds) + ")");
+    if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
+    CallGuard g(ctx);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
+        RadixWorkspace ws;
+        if (int rc = ctx->radix_ws(n, &ws)) return rc;
+        int l = 0;
+        if (radix_log2 <= 8) {
+            l = launch_count_pass(d_in, d_out, n, radix_log2, round * radix_log2, ws, s, true);
+        } else {
+            // stable 16-bit digit pass = stable pass on its low byte, then on
+            // its high byte, ping-ponging through stage_b.
+            cudaError_t e = ctx->stage_b.ensure(std::max<uint64_t>(n, 4) * 4);
+            if (e != cudaSuccess) return cuda_fail(e, "workspace");
+            uint32_t* mid = ctx->stage_b.as<uint32_t>();
+            const int l1 = launch_count_pass(d_in, mid, n, 8, 16 * round, ws, s, true);
+            const int l2 = l1 < 0 ? -1 : launch_count_pass(mid, d_out, n, 8, 16 * round + 8, ws, s, true);
+            l = (l1 < 0 || l2 < 0) ? -1 : l1 + l2;
+        }
+        if (l < 0) return cuda_fail(cudaGetLastError(), "count-sort round launch");
+        ctx->launches += static_cast<uint64_t>(l);
+        return BSG_OK;
+    });
+}
+
+int bsg_merge_split_u32(bsg_ctx* ctx, const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* low,
+                        uint32_t* high, int mem_kind, void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if ((na && (!a || !low)) || (nb && (!b || !high))) return fail(BSG_EINVAL, "null key pointer");
+    if (na + nb >= (uint64_t{1} << 31)) return fail(BSG_EINVAL, "merge_split: |a|+|b| must be < 2^31");
+    CallGuard g(ctx);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (mem_kind == BSG_MEM_DEVICE) {
+        const int l = launch_merge_split(a, na, b, nb, low, high, st);
+        if (l < 0) return cuda_fail(cudaGetLastError(), "merge_split launch");
+        ctx->launches += static_cast<uint64_t>(l);
+        return BSG_OK;
+    }
+    if (mem_kind != BSG_MEM_HOST) return fail(BSG_EINVAL, "mem_kind must be BSG_MEM_HOST or BSG_MEM_DEVICE");
+    cudaError_t e;
+    const uint64_t tot = std::max<uint64_t>(na + nb, 4);
+    if ((e = ctx->stage_in.ensure(tot * 4)) != cudaSuccess) return cuda_fail(e, "host staging");
+    if ((e = ctx->stage_out.ensure(tot * 4)) != cudaSuccess) return cuda_fail(e, "host staging");
+    uint32_t* da = ctx->stage_in.as<uint32_t>();
+    uint32_t* db = da + na;
+    uint32_t* dl = ctx->stage_out.as<uint32_t>();
+    uint32_t* dh = dl + na;
+    if (na && (e = cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D");
+    if (nb && (e = cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D");
+    const int l = launch_merge_split(da, na, db, nb, dl, dh, st);
+    if (l < 0) return cuda_fail(cudaGetLastError(), "merge_split launch");
+    ctx->launches += static_cast<uint64_t>(l);
+    if (na && (e = cudaMemcpyAsync(low, dl, na * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e, "D2H");
+    if (nb && (e = cudaMemcpyAsync(high, dh, nb * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e, "D2H");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "stream synchronize");
+    return BSG_OK;
+}
+
+int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in, uint32_t* out, uint64_t num_arrays,
+                                  uint32_t len, int p, int stages_limit, bsg_run_stats* stats, int mem_kind,
+                                  void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    int S = 0;
+    if (int rc = bsg_network_schedule(network, p, nullptr, nullptr, 0, &S)) return rc;
+    const uint64_t L = (static_cast<uint64_t>(len) + p - 1) / p;
+    const uint64_t padded = L * static_cast<uint64_t>(p);
+    const bool full = stages_limit < 0 || stages_limit >= S;
+    const int run = full ? S : stages_limit;
+    const uint64_t out_per = full ? len : padded;
+    if (num_arrays && len && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
+    if (padded > kNetMaxPadded)
+        return fail(BSG_EINVAL, "block network: p*ceil(len/p) = " + std::to_string(padded) + " exceeds " +
+                                    std::to_string(kNetMaxPadded) + " keys per array (shared-memory resident)");
+    if (stats) {
+        std::vector<int32_t> partner(static_cast<size_t>(S) * p), keep(static_cast<size_t>(S) * p);
+        bsg_network_schedule(network, p, partner.data(), keep.data(), S, &S);
+        bsg_run_stats st{};
+        st.supersteps = 1 + run;
+        for (int s = 0; s < run; ++s)
+            for (int i = 0; i < p; ++i)
+                if (partner[static_cast<size_t>(s) * p + i] >= 0) {
+                    st.messages_sent += 1;
+                    st.words_sent += L;
+                }
+        st.messages_delivered = st.messages_sent;
+        st.words_delivered = st.words_sent;
+        *stats = st;
+    }
+    CallGuard g(ctx);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t n_in = num_arrays * len, n_out = num_arrays * out_per;
+    return with_device_io(ctx, in, out, n_in, n_out, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
+        if (num_arrays == 0 || len == 0) return BSG_OK;
+        const int l = launch_block_network(network, d_in, d_out, num_arrays, len, p, run, full, s);
+        if (l < 0) return cuda_fail(cudaGetLastError(), "block network launch");
+        ctx->launches += static_cast<uint64_t>(l);
+        return BSG_OK;
+    });
+}
+
+int bsg_parallel_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int p, int radix_log2,
+                                int rounds_limit, bsg_run_stats* stats, int mem_kind, void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (p < 1) return fail(BSG_EINVAL, "parallel radix sort: p must be >= 1");
+    if (int rc = radix_bits_or_fail(radix_log2)) return rc;
+    if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
+    const int all_rounds = 32 / radix_log2;
+    const int rounds = (rounds_limit >= 0 && rounds_limit < all_rounds) ? rounds_limit : all_rounds;
+    CallGuard g(ctx);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
+        return run_parallel_radix_local(ctx, d_in, d_out, n, p, radix_log2, rounds, stats, s);
+    });
+}
+
+int bsg_sort_instance_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int processors, int algorithm,
+                          uint64_t radix, int mem_kind, void* stream) {
+    // core.hpp:74-88 SortInstance::validate
+    if (processors < 1) return fail(BSG_EINVAL, "SortInstance: processors must be >= 1");
+    if (radix == 0 || (radix & (radix - 1)) != 0) return fail(BSG_EINVAL, "SortInstance: radix must be a power of two whose bit width divides 32");
+    int bits = 0;
+    while ((uint64_t{1} << bits) != radix) ++bits;
+    if (bits == 0 || 32 % bits != 0)
+        return fail(BSG_EINVAL, "SortInstance: radix must be a power of two whose bit width divides 32");
+    if (algorithm == BSG_SR4 && processors != 1) return fail(BSG_EINVAL, "SortInstance: sr4 is serial, requires p = 1");
+    if (algorithm == BSG_BTN && (processors & (processors - 1)) != 0)
+        return fail(BSG_EINVAL, "SortInstance: btn requires a power-of-two p");
+    if (algorithm == BSG_PR4 && radix != 256) return fail(BSG_EINVAL, "SortInstance: pr4 is radix-256 by definition");
+    if (algorithm == BSG_PR2 && radix != 65536) return fail(BSG_EINVAL, "SortInstance: pr2 is radix-65536 by definition");
+    // bspsort.hpp:15-25 dispatch
+    switch (algorithm) {
+    case BSG_SR4:
+        return bsg_radix_sort_u32(ctx, in, out, n, bits, mem_kind, stream);
+    case BSG_PR4:
+    case BSG_PR2:
+        return bsg_parallel_radix_sort_u32(ctx, in, out, n, processors, bits, -1, nullptr, mem_kind, stream);
+    case BSG_BTN:
+    case BSG_OET:
+        if (n > 0xFFFFFFFFull) return fail(BSG_EINVAL, "block network: n must fit in 32 bits");
+        return bsg_block_network_batched_u32(ctx, algorithm == BSG_BTN ? BSG_NET_BTN : BSG_NET_OET, in, out, n ? 1 : 0,
+                                             static_cast<uint32_t>(n), processors, -1, nullptr, mem_kind, stream);
+    default:
+        return fail(BSG_EINVAL, "sort_instance: unknown algorithm");
+    }
+}
+
+int bsg_pr_count_digits(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int radix_log2, uint64_t* counts,
+                        void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = radix_bits_or_fail(radix_log2)) return rc;
+    if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
+    CallGuard g(ctx);
+    const int l = launch_pr_count(ctx, block, len, round, radix_log2, counts, static_cast<cudaStream_t>(stream));
+    if (l < 0) return cuda_fail(cudaGetLastError(), "count_digits launch");
+    ctx->launches += static_cast<uint64_t>(l);
+    return BSG_OK;
+}
+
+int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me, int round, int radix_log2,
+                uint64_t* send_counts, uint64_t* recv_counts, int64_t* rebuild_delta, void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = radix_bits_or_fail(radix_log2)) return rc;
+    if (p < 1 || me < 0 || me >= p) return fail(BSG_EINVAL, "pr_plan: worker index out of range");
+    (void)round;
+    CallGuard g(ctx);
+    const int l = launch_pr_plan(counts, n, p, me, radix_log2, send_counts, recv_counts, rebuild_delta,
+                                 static_cast<cudaStream_t>(stream));
+    if (l < 0) return cuda_fail(cudaGetLastError(), "pr_plan launch");
+    ctx->launches += static_cast<uint64_t>(l);
+    return BSG_OK;
+}
+
+int bsg_pr_local_sort(bsg_ctx* ctx, const uint32_t* block, uint32_t* sorted, uint64_t len, int round, int radix_log2,
+                      void* stream) {
+    return bsg_count_sort_round_u32(ctx, block, sorted, len, round, radix_log2, BSG_MEM_DEVICE, stream);
+}
+
+int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len, const uint64_t* recv_counts, int p, int round,
+                   int radix_log2, const int64_t* rebuild_delta, uint32_t* block, void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = radix_bits_or_fail(radix_log2)) return rc;
+    if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
+    (void)recv_counts;
+    (void)p;
+    CallGuard g(ctx);
+    const int l = launch_pr_rebuild(recv, recv_len, radix_log2, round * radix_log2, rebuild_delta, block,
+                                    static_cast<cudaStream_t>(stream), recv_counts, p);
+    if (l < 0) return cuda_fail(cudaGetLastError(), "rebuild launch");
+    ctx->launches += static_cast<uint64_t>(l);
+    return BSG_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,263 @@
+// netsort.cu -- batched BTN / OET block-network sorts and merge_split for
+// sm_100a.
+//
+// Restates netsort.hpp:124-199 (prepare_blocks + run_block_network) for a
+// batch of independent arrays: one CTA owns one (or, for short arrays,
+// several) array(s) entirely in shared memory.  The p BSP workers become p
+// blocks of L = ceil(len/p) keys inside the CTA; the reference's supersteps
+// become __syncthreads() between ping-pong shared-memory buffers:
+//   superstep 0  -- local sort of every block (netsort.hpp:167): 8-key
+//                   register sorting networks, then bottom-up merge-path
+//                   merges inside each block;
+//   superstep s  -- merge_split of every (worker, partner) pair of stage s
+//                   (netsort.hpp:170-179): each thread produces 8 consecutive
+//                   outputs of the pair's merged sequence after a merge-path
+//                   binary search; the keep_low worker takes outputs [0, L),
+//                   its partner [L, 2L); idle OET edge workers copy.
+// Padding with 0xFFFFFFFF and the final strip follow netsort.hpp:131-139, 197.
+// Stage partners are computed on the fly from the closed forms of
+// bitonic_schedule (netsort.hpp:76-88) and odd_even_rounds (netsort.hpp:99-105).
+#include <algorithm>
+
+#include "common.cuh"
+#include "netsort.cuh"
+
+namespace bsg {
+
+namespace {
+
+constexpr int kNK = 8;          // outputs per thread-chunk
+constexpr int kNetThreads = 256;
+constexpr uint32_t kPad = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void cas(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// Odd-even transposition network on 8 registers (28 comparators).
+__device__ __forceinline__ void sort8(uint32_t (&v)[kNK]) {
+#pragma unroll
+    for (int r = 0; r < kNK; ++r) {
+#pragma unroll
+        for (int j = r & 1; j + 1 < kNK; j += 2) cas(v[j], v[j + 1]);
+    }
+}
+
+// Writes outputs [diag, diag+cnt) of merge(A, B) (ties taken from A first,
+// netsort.hpp:39) to dst[0..cnt).
+__device__ __forceinline__ void merge_chunk(const uint32_t* A, int na, const uint32_t* B, int nb, int diag, int cnt,
+                                            uint32_t* dst) {
+    int lo = max(0, diag - nb), hi = min(diag, na);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A[mid] <= B[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    int i = lo, j = diag - lo;
+    uint32_t av = i < na ? A[i] : 0u, bv = j < nb ? B[j] : 0u;
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) {
+        if (k < cnt) {
+            const bool take_a = i < na && (j >= nb || av <= bv);
+            if (take_a) {
+                dst[k] = av;
+                ++i;
+                av = i < na ? A[i] : 0u;
+            } else {
+                dst[k] = bv;
+                ++j;
+                bv = j < nb ? B[j] : 0u;
+            }
+        }
+    }
+}
+
+// bitonic_schedule (netsort.hpp:76-88) for stage s, worker i.
+__device__ __forceinline__ int btn_partner(int s, int i, bool& keep_low) {
+    int a = 1, base = 0;
+    while (base + a <= s) {
+        base += a;
+        ++a;
+    }
+    const int jidx = s - base;
+    const int k = 1 << a, j = 1 << (a - 1 - jidx);
+    const int q = i ^ j;
+    const bool asc = (i & k) == 0;
+    keep_low = asc ? (i < q) : (i > q);
+    return q;
+}
+
+// odd_even_rounds (netsort.hpp:99-105) for round r, worker i; -1 = idle.
+__device__ __forceinline__ int oet_partner(int r, int i, int p, bool& keep_low) {
+    const int par = r & 1;
+    if (i < par) return -1;
+    if (((i - par) & 1) == 0) {
+        if (i + 1 < p) {
+            keep_low = true;
+            return i + 1;
+        }
+        return -1;
+    }
+    keep_low = false;
+    return i - 1;
+}
+
+__global__ void __launch_bounds__(kNetThreads)
+    block_network_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t num_arrays,
+                         uint32_t len, int p, uint32_t L, int network, int run_stages, int full, int apc) {
+    extern __shared__ __align__(16) uint32_t net_smem[];
+    const uint32_t P = L * static_cast<uint32_t>(p);
+    uint32_t* bufA = net_smem;
+    uint32_t* bufB = net_smem + static_cast<uint32_t>(apc) * P;
+    const uint64_t array0 = static_cast<uint64_t>(blockIdx.x) * apc;
+    const int na = static_cast<int>(min(static_cast<uint64_t>(apc), num_arrays - array0));
+    const int tid = threadIdx.x;
+
+    // prepare_blocks: load + pad (netsort.hpp:131-139)
+    const uint32_t tot = static_cast<uint32_t>(na) * P;
+    for (uint32_t idx = tid; idx < tot; idx += kNetThreads) {
+        const uint32_t a = idx / P, e = idx - a * P;
+        bufA[idx] = e < len ? __ldg(in + (array0 + a) * len + e) : kPad;
+    }
+    __syncthreads();
+
+    const uint32_t cb = (L + kNK - 1) / kNK; // chunks per block
+    const uint32_t items = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cb;
+
+    // superstep 0: local sort of every block.  (a) 8-key register networks
+    for (uint32_t it = tid; it < items; it += kNetThreads) {
+        const uint32_t a = it / (p * cb), rem = it - a * p * cb;
+        const uint32_t w = rem / cb, c = rem - w * cb;
+        uint32_t* blk = bufA + a * P + w * L;
+        const uint32_t ob = c * kNK;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
+        uint32_t v[kNK];
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) v[k] = k < cnt ? blk[ob + k] : kPad;
+        sort8(v);
+#pragma unroll
+        for (int k = 0; k < kNK; ++k)
+            if (k < cnt) blk[ob + k] = v[k];
+    }
+    __syncthreads();
+    // (b) bottom-up merge-path merges inside each block
+    uint32_t* src = bufA;
+    uint32_t* dst = bufB;
+    for (uint32_t width = kNK; width < L; width *= 2) {
+        for (uint32_t it = tid; it < items; it += kNetThreads) {
+            const uint32_t a = it / (p * cb), rem = it - a * p * cb;
+            const uint32_t w = rem / cb, c = rem - w * cb;
+            const uint32_t bs = a * P + w * L;
+            const uint32_t ob = c * kNK;
+            const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
+            const uint32_t ps = (ob / (2 * width)) * (2 * width);
+            const uint32_t a_end = min(ps + width, L), b_end = min(ps + 2 * width, L);
+            merge_chunk(src + bs + ps, static_cast<int>(a_end - ps), src + bs + a_end, static_cast<int>(b_end - a_end),
+                        static_cast<int>(ob - ps), cnt, dst + bs + ob);
+        }
+        __syncthreads();
+        uint32_t* t = src;
+        src = dst;
+        dst = t;
+    }
+
+    // supersteps 1..S: merge_split stages
+    for (int s = 0; s < run_stages; ++s) {
+        for (uint32_t it = tid; it < items; it += kNetThreads) {
+            const uint32_t a = it / (p * cb), rem = it - a * p * cb;
+            const int i = static_cast<int>(rem / cb);
+            const uint32_t c = rem - static_cast<uint32_t>(i) * cb;
+            const uint32_t ob = c * kNK;
+            const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
+            bool keep_low = false;
+            const int q = network == 0 ? btn_partner(s, i, keep_low) : oet_partner(s, i, p, keep_low);
+            uint32_t* out_blk = dst + a * P + static_cast<uint32_t>(i) * L;
+            if (q < 0) {
+                const uint32_t* in_blk = src + a * P + static_cast<uint32_t>(i) * L;
+#pragma unroll
+                for (int k = 0; k < kNK; ++k)
+                    if (k < cnt) out_blk[ob + k] = in_blk[ob + k];
+                continue;
+            }
+            const int lo_w = min(i, q), hi_w = max(i, q);
+            const uint32_t* A = src + a * P + static_cast<uint32_t>(lo_w) * L;
+            const uint32_t* B = src + a * P + static_cast<uint32_t>(hi_w) * L;
+            const int diag = static_cast<int>((keep_low ? 0u : L) + ob);
+            merge_chunk(A, static_cast<int>(L), B, static_cast<int>(L), diag, cnt, out_blk + ob);
+        }
+        __syncthreads();
+        uint32_t* t = src;
+        src = dst;
+        dst = t;
+    }
+
+    // concatenate (+ strip the pad when the network ran to completion)
+    if (full) {
+        for (uint32_t idx = tid; idx < static_cast<uint32_t>(na) * len; idx += kNetThreads) {
+            const uint32_t a = idx / len, e = idx - a * len;
+            out[(array0 + a) * len + e] = src[a * P + e];
+        }
+    } else {
+        for (uint32_t idx = tid; idx < tot; idx += kNetThreads) out[array0 * P + idx] = src[idx];
+    }
+}
+
+constexpr int kMsThreads = 256;
+
+__global__ void __launch_bounds__(kMsThreads)
+    merge_split_kernel(const uint32_t* __restrict__ a, uint32_t na, const uint32_t* __restrict__ b, uint32_t nb,
+                       uint32_t* __restrict__ low, uint32_t* __restrict__ high) {
+    const uint32_t total = na + nb;
+    const uint32_t chunks = (total + kNK - 1) / kNK;
+    for (uint32_t c = blockIdx.x * kMsThreads + threadIdx.x; c < chunks; c += gridDim.x * kMsThreads) {
+        const uint32_t o = c * kNK;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), total - o));
+        uint32_t v[kNK];
+        merge_chunk(a, static_cast<int>(na), b, static_cast<int>(nb), static_cast<int>(o), cnt, v);
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) {
+            if (k < cnt) {
+                const uint32_t pos = o + k;
+                if (pos < na) low[pos] = v[k];
+                else high[pos - na] = v[k];
+            }
+        }
+    }
+}
+
+} // namespace
+
+int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p,
+                         int run_stages, bool full, cudaStream_t stream) {
+    const uint32_t L = (len + static_cast<uint32_t>(p) - 1) / static_cast<uint32_t>(p);
+    const uint32_t P = L * static_cast<uint32_t>(p);
+    if (P == 0 || P > kNetMaxPadded) return -1;
+    const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
+    const size_t smem = 2ull * apc * P * sizeof(uint32_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(block_network_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(2 * kNetMaxPadded * sizeof(uint32_t)));
+        attr = true;
+    }
+    const uint64_t grid = (num_arrays + apc - 1) / apc;
+    if (grid > 0x7FFFFFFFull) return -1;
+    block_network_kernel<<<static_cast<unsigned>(grid), kNetThreads, smem, stream>>>(in, out, num_arrays, len, p, L,
+                                                                                   network, run_stages, full ? 1 : 0, apc);
+    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_merge_split(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* low, uint32_t* high,
+                       cudaStream_t stream) {
+    const uint64_t total = na + nb;
+    if (total == 0) return 0;
+    const uint64_t chunks = (total + kNK - 1) / kNK;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((chunks + kMsThreads - 1) / kMsThreads, 148 * 16));
+    merge_split_kernel<<<grid, kMsThreads, 0, stream>>>(a, static_cast<uint32_t>(na), b, static_cast<uint32_t>(nb), low,
+                                                       high);
+    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+} // namespace bsg

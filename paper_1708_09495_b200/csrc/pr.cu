@@ -1,0 +1,359 @@
+// pr.cu -- parallel LSD radix sort (PR4 at r = 2^8, PR2 at r = 2^16).
+//
+// Restates one BSP round of run_parallel_radix (radix.hpp:371-414) per
+// worker as device steps, so no per-key owner_of() division and no per-slice
+// vector copies are needed:
+//   count   -- count_digits (radix.hpp:238-243): digit histogram of the block.
+//   plan    -- digit_starts + the routing of sort_and_scatter
+//              (radix.hpp:248-290): from the p x r count matrix compute, per
+//              worker, how many keys go to / come from each worker and, for the
+//              rebuild, where the keys of (source v, digit d) land.  Because
+//              global positions increase along a digit-sorted block, every
+//              slice is a contiguous range, found from counts alone.
+//   local   -- the stable local pass of sort_and_scatter (count_sort_round).
+//   rebuild -- gather_slices (radix.hpp:295-333): walking (digit, source) in
+//              order is a stable digit scatter of the source-major receive
+//              buffer, block[delta[v][d] + j] = recv[j].
+// In-process (p logical workers on one GPU) the exchange is fused into the
+// rebuild: it reads each source's slice straight from that source's sorted
+// block.  Across GPUs, paper_1708_09495_b200/distributed.py interleaves the
+// same steps with NCCL all-gather / all-to-all-v.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "context.cuh"
+#include "pr.cuh"
+#include "radix.cuh"
+
+namespace bsg {
+
+namespace {
+
+constexpr int kPlanThreads = 256;
+
+__device__ __forceinline__ uint64_t part_size(uint64_t n, int p, int w) {
+    return n / static_cast<uint64_t>(p) + (static_cast<uint64_t>(w) < n % static_cast<uint64_t>(p) ? 1 : 0);
+}
+__device__ __forceinline__ uint64_t part_offset(uint64_t n, int p, int w) {
+    const uint64_t uw = static_cast<uint64_t>(w), big = n % static_cast<uint64_t>(p);
+    return uw * (n / static_cast<uint64_t>(p)) + (uw < big ? uw : big);
+}
+__device__ __forceinline__ int part_owner(uint64_t n, int p, uint64_t pos) {
+    const uint64_t small = n / static_cast<uint64_t>(p), bigc = n % static_cast<uint64_t>(p);
+    const uint64_t big = small + 1, split = bigc * big;
+    if (pos < split) return static_cast<int>(pos / big);
+    return static_cast<int>(bigc + (pos - split) / small);
+}
+__device__ __forceinline__ uint64_t overlap(uint64_t a0, uint64_t a1, uint64_t b0, uint64_t b1) {
+    const uint64_t lo = a0 > b0 ? a0 : b0, hi = a1 < b1 ? a1 : b1;
+    return hi > lo ? hi - lo : 0;
+}
+
+// Block-wide exclusive scan of one uint64 per thread; returns the block total.
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t& excl, uint64_t* s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t incl = warp_inclusive_scan(v);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t pre = 0, total = 0;
+    for (int w = 0; w < kPlanThreads / 32; ++w) {
+        if (w < warp) pre += s_warp[w];
+        total += s_warp[w];
+    }
+    excl = pre + incl - v;
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    pr_plan1_kernel(const uint64_t* __restrict__ counts, uint64_t n, int p, int me, int radix,
+                    uint64_t* __restrict__ send_counts, uint64_t* __restrict__ recv_counts,
+                    int64_t* __restrict__ delta, uint64_t* __restrict__ split) {
+    extern __shared__ uint64_t s_send[]; // p entries
+    __shared__ uint64_t s_warp[kPlanThreads / 32];
+    __shared__ uint64_t s_red[2][kPlanThreads / 32];
+    const int v = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (v == me)
+        for (int w = tid; w < p; w += kPlanThreads) s_send[w] = 0;
+    __syncthreads();
+    const uint64_t lo_me = part_offset(n, p, me), hi_me = lo_me + part_size(n, p, me);
+    uint64_t run_start = 0, run_local = 0, acc_recv = 0, acc_split = 0;
+    for (int d0 = 0; d0 < radix; d0 += kPlanThreads) {
+        const int d = d0 + tid;
+        uint64_t col = 0, before = 0, cv = 0;
+        if (d < radix) {
+            for (int u = 0; u < p; ++u) {
+                const uint64_t c = counts[static_cast<uint64_t>(u) * radix + d];
+                col += c;
+                if (u < v) before += c;
+                if (u == v) cv = c;
+            }
+        }
+        uint64_t ex_col, ex_cv;
+        const uint64_t tot_col = block_excl_scan(col, ex_col, s_warp);
+        const uint64_t tot_cv = block_excl_scan(cv, ex_cv, s_warp);
+        if (d < radix) {
+            const uint64_t np = run_start + ex_col + before; // next_pos[d] of worker v
+            const uint64_t ls = run_local + ex_cv;           // local start of digit d in v's sorted block
+            acc_recv += overlap(np, np + cv, lo_me, hi_me);
+            acc_split += overlap(np, np + cv, 0, lo_me);
+            delta[static_cast<uint64_t>(v) * radix + d] = static_cast<int64_t>(np) - static_cast<int64_t>(ls);
+            if (v == me && cv) {
+                const int w0 = part_owner(n, p, np), w1 = part_owner(n, p, np + cv - 1);
+                for (int w = w0; w <= w1; ++w) {
+                    const uint64_t lo = part_offset(n, p, w);
+                    const uint64_t o = overlap(np, np + cv, lo, lo + part_size(n, p, w));
+                    if (o) atomicAdd(reinterpret_cast<unsigned long long*>(&s_send[w]), static_cast<unsigned long long>(o));
+                }
+            }
+        }
+        run_start += tot_col;
+        run_local += tot_cv;
+    }
+    // block reductions of acc_recv / acc_split
+    const uint64_t r1 = warp_sum(acc_recv), r2 = warp_sum(acc_split);
+    if ((tid & 31) == 0) {
+        s_red[0][tid >> 5] = r1;
+        s_red[1][tid >> 5] = r2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t a = 0, b = 0;
+        for (int w = 0; w < kPlanThreads / 32; ++w) {
+            a += s_red[0][w];
+            b += s_red[1][w];
+        }
+        recv_counts[v] = a;
+        split[v] = b;
+    }
+    if (v == me)
+        for (int w = tid; w < p; w += kPlanThreads) send_counts[w] = s_send[w];
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    pr_plan2_kernel(uint64_t n, int p, int me, int radix, const uint64_t* __restrict__ recv_counts,
+                    const uint64_t* __restrict__ split, int64_t* __restrict__ delta) {
+    const int v = blockIdx.x;
+    uint64_t recv_off = 0;
+    for (int u = 0; u < v; ++u) recv_off += recv_counts[u];
+    const int64_t adj = static_cast<int64_t>(split[v]) - static_cast<int64_t>(recv_off) -
+                        static_cast<int64_t>(part_offset(n, p, me));
+    for (int d = threadIdx.x; d < radix; d += kPlanThreads) delta[static_cast<uint64_t>(v) * radix + d] += adj;
+}
+
+constexpr int kRebuildThreads = 256;
+constexpr int kMaxP = 1024;
+
+__global__ void __launch_bounds__(kRebuildThreads)
+    pr_rebuild_kernel(const uint32_t* __restrict__ recv, uint64_t recv_len, int p,
+                      const uint64_t* __restrict__ recv_counts, const uint32_t* const* __restrict__ src_ptrs,
+                      uint32_t mask, int shift, int radix, const int64_t* __restrict__ delta,
+                      uint32_t* __restrict__ block) {
+    __shared__ uint64_t s_off[kMaxP + 1];
+    if (threadIdx.x == 0) {
+        uint64_t run = 0;
+        for (int v = 0; v < p; ++v) {
+            s_off[v] = run;
+            run += recv_counts[v];
+        }
+        s_off[p] = run;
+    }
+    __syncthreads();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kRebuildThreads;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * kRebuildThreads + threadIdx.x; j < recv_len; j += stride) {
+        int lo = 0, hi = p - 1; // largest v with s_off[v] <= j
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_off[mid] <= j) lo = mid;
+            else hi = mid - 1;
+        }
+        const int v = lo;
+        const uint32_t key = src_ptrs ? src_ptrs[v][j - s_off[v]] : recv[j];
+        const uint32_t d = (key >> shift) & mask;
+        block[static_cast<uint64_t>(delta[static_cast<uint64_t>(v) * radix + d] + static_cast<int64_t>(j))] = key;
+    }
+}
+
+__global__ void pr_src_ptrs_kernel(const uint32_t* sorted, uint64_t n, int p, const uint64_t* __restrict__ split,
+                                   const uint32_t** out_ptrs) {
+    for (int v = threadIdx.x; v < p; v += blockDim.x) out_ptrs[v] = sorted + part_offset(n, p, v) + split[v];
+}
+
+// 16-bit digit histogram: 65536 16-bit counters packed in 128 KiB of shared
+// memory; a counter that reaches 2^15 carries 2^15 to the global uint64 bin.
+constexpr int kHist16Threads = 1024;
+
+__global__ void __launch_bounds__(kHist16Threads)
+    hist16_kernel(const uint32_t* __restrict__ in, uint64_t n, int shift, unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t h16[]; // 32768 words
+    for (int i = threadIdx.x; i < 32768; i += kHist16Threads) h16[i] = 0;
+    __syncthreads();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kHist16Threads;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kHist16Threads + threadIdx.x; i < n; i += stride) {
+        const uint32_t d = (__ldg(in + i) >> shift) & 0xFFFFu;
+        const uint32_t sh = (d & 1u) * 16u;
+        const uint32_t old = atomicAdd(&h16[d >> 1], 1u << sh);
+        if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {
+            atomicSub(&h16[d >> 1], 0x8000u << sh);
+            atomicAdd(&counts[d], 0x8000ull);
+        }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 65536; d += kHist16Threads) {
+        const uint32_t c = (h16[d >> 1] >> ((d & 1) * 16)) & 0xFFFFu;
+        if (c) atomicAdd(&counts[d], static_cast<unsigned long long>(c));
+    }
+}
+
+} // namespace
+
+int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int bits, uint64_t* counts,
+                    cudaStream_t stream) {
+    const int radix = 1 << bits;
+    if (bits == 16) {
+        if (cudaMemsetAsync(counts, 0, radix * sizeof(uint64_t), stream) != cudaSuccess) return -1;
+        if (len == 0) return 0;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(hist16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+            attr = true;
+        }
+        const uint64_t want = (len + kHist16Threads * 16 - 1) / (kHist16Threads * 16);
+        const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200)));
+        hist16_kernel<<<grid, kHist16Threads, 32768 * 4, stream>>>(block, len, 16 * round,
+                                                                   reinterpret_cast<unsigned long long*>(counts));
+        return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    }
+    const uint64_t chunks = len ? (len + kChunkKeys - 1) / kChunkKeys : 1;
+    if (ctx->cnt32.ensure(chunks * 256 * sizeof(uint32_t)) != cudaSuccess) return -1;
+    if (len == 0) {
+        if (cudaMemsetAsync(counts, 0, radix * sizeof(uint64_t), stream) != cudaSuccess) return -1;
+        return 0;
+    }
+    return launch_digit_counts(block, len, bits, round * bits, counts, ctx->cnt32.as<uint32_t>(), stream);
+}
+
+int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, uint64_t* send_counts,
+                   uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* split) {
+    if (!split || p > kMaxP) return -1;
+    const int radix = 1 << bits;
+    pr_plan1_kernel<<<p, kPlanThreads, sizeof(uint64_t) * p, stream>>>(counts, n, p, me, radix, send_counts,
+                                                                        recv_counts, rebuild_delta, split);
+    pr_plan2_kernel<<<p, kPlanThreads, 0, stream>>>(n, p, me, radix, recv_counts, split, rebuild_delta);
+    return cudaGetLastError() == cudaSuccess ? 2 : -1;
+}
+
+int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shift, const int64_t* rebuild_delta,
+                      uint32_t* block, cudaStream_t stream, const uint64_t* recv_counts, int p) {
+    if (p > kMaxP) return -1;
+    if (recv_len == 0) return 0;
+    const uint64_t want = (recv_len + kRebuildThreads * 8 - 1) / (kRebuildThreads * 8);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
+    pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(recv, recv_len, p, recv_counts, nullptr, (1u << bits) - 1u,
+                                                           shift, 1 << bits, rebuild_delta, block);
+    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int p, int bits, int rounds,
+                             bsg_run_stats* stats, cudaStream_t stream) {
+    if (p > kMaxP) return fail(BSG_EINVAL, "parallel radix sort: p must be <= 1024 on one GPU");
+    const int radix = 1 << bits;
+    const uint64_t pp = static_cast<uint64_t>(p) * p;
+    cudaError_t e;
+    if ((e = ctx->pr_block.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if ((e = ctx->pr_sorted.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if ((e = ctx->pr_counts.ensure(static_cast<uint64_t>(p) * radix * 8)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if ((e = ctx->pr_delta.ensure(static_cast<uint64_t>(p) * radix * 8)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if ((e = ctx->pr_misc.ensure(pp * 8 * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if (bits == 16 && (e = ctx->stage_b.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    RadixWorkspace ws;
+    if (int rc = ctx->radix_ws(std::max<uint64_t>(n / p + 1, 1), &ws)) return rc;
+
+    uint32_t* A = ctx->pr_block.as<uint32_t>();
+    uint32_t* S = ctx->pr_sorted.as<uint32_t>();
+    uint64_t* counts = ctx->pr_counts.as<uint64_t>();
+    int64_t* delta = ctx->pr_delta.as<int64_t>();
+    uint64_t* send = ctx->pr_misc.as<uint64_t>();
+    uint64_t* recv = send + pp;
+    uint64_t* split = recv + pp;
+    const uint32_t** srcp = reinterpret_cast<const uint32_t**>(split + pp);
+
+    if (n && (e = cudaMemcpyAsync(A, in, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
+        return cuda_fail(e, "pr copy in");
+    bsg_run_stats st{};
+    std::vector<uint64_t> h_send(pp);
+    uint64_t launches = 0;
+    auto add = [&](int l) -> bool {
+        if (l < 0) return false;
+        launches += static_cast<uint64_t>(l);
+        return true;
+    };
+    for (int round = 0; round < rounds && n; ++round) {
+        const int shift = round * bits;
+        for (int w = 0; w < p; ++w) {
+            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
+            if (!add(launch_pr_count(ctx, A + off, sz, round, bits, counts + static_cast<uint64_t>(w) * radix, stream)))
+                return cuda_fail(cudaGetLastError(), "pr count");
+        }
+        for (int w = 0; w < p; ++w) {
+            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
+            if (sz == 0) continue;
+            if (bits <= 8) {
+                if (!add(launch_count_pass(A + off, S + off, sz, bits, shift, ws, stream, true)))
+                    return cuda_fail(cudaGetLastError(), "pr local pass");
+            } else {
+                uint32_t* mid = ctx->stage_b.as<uint32_t>();
+                if (!add(launch_count_pass(A + off, mid, sz, 8, shift, ws, stream, true)) ||
+                    !add(launch_count_pass(mid, S + off, sz, 8, shift + 8, ws, stream, true)))
+                    return cuda_fail(cudaGetLastError(), "pr local pass");
+            }
+        }
+        for (int me = 0; me < p; ++me) {
+            const uint64_t off = bsg_partition_offset_of(n, p, me), sz = bsg_partition_size_of(n, p, me);
+            if (!add(launch_pr_plan(counts, n, p, me, bits, send + static_cast<uint64_t>(me) * p,
+                                    recv + static_cast<uint64_t>(me) * p, delta, stream,
+                                    split + static_cast<uint64_t>(me) * p)))
+                return cuda_fail(cudaGetLastError(), "pr plan");
+            pr_src_ptrs_kernel<<<1, 256, 0, stream>>>(S, n, p, split + static_cast<uint64_t>(me) * p,
+                                                       srcp + static_cast<uint64_t>(me) * p);
+            ++launches;
+            if (sz) {
+                const uint64_t want = (sz + kRebuildThreads * 8 - 1) / (kRebuildThreads * 8);
+                const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
+                pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(
+                    nullptr, sz, p, recv + static_cast<uint64_t>(me) * p, srcp + static_cast<uint64_t>(me) * p,
+                    static_cast<uint32_t>(radix - 1), shift, radix, delta, A + off);
+                ++launches;
+            }
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr rebuild");
+        }
+        if (stats) {
+            if ((e = cudaMemcpyAsync(h_send.data(), send, pp * 8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess ||
+                (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+                return cuda_fail(e, "pr stats");
+            uint64_t nz = 0;
+            for (uint64_t i = 0; i < pp; ++i) nz += h_send[i] ? 1 : 0;
+            st.messages_sent += pp + nz;
+            st.words_sent += pp * static_cast<uint64_t>(radix) + n;
+        }
+    }
+    if (stats) {
+        if (n == 0) {
+            // empty input: the count exchange still happens every round
+            st.messages_sent = static_cast<uint64_t>(rounds) * pp;
+            st.words_sent = static_cast<uint64_t>(rounds) * pp * radix;
+        }
+        st.supersteps = 2 * rounds + 1;
+        st.messages_delivered = st.messages_sent;
+        st.words_delivered = st.words_sent;
+        *stats = st;
+    }
+    if (n && (e = cudaMemcpyAsync(out, A, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
+        return cuda_fail(e, "pr copy out");
+    ctx->launches += launches;
+    return BSG_OK;
+}
+
+} // namespace bsg

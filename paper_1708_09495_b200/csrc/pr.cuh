@@ -1,0 +1,32 @@
+// pr.cuh -- parallel radix sort (PR4 / PR2) step kernels and the in-process
+// p-logical-worker orchestration (pr.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/bsg.h"
+
+struct bsg_ctx;
+
+namespace bsg {
+
+// count_digits (radix.hpp:238-243) into uint64 counts[radix].
+int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int bits, uint64_t* counts,
+                    cudaStream_t stream);
+
+// Routing plan of worker `me` from the p x r count matrix (radix.hpp:248-290).
+// split (optional, p entries): index in each source's sorted block where the
+// slice for `me` begins.
+int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, uint64_t* send_counts,
+                   uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* split = nullptr);
+
+// gather_slices (radix.hpp:295-333) as a stable scatter of the source-major
+// receive buffer: block[delta[src][digit] + j] = recv[j].
+int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shift, const int64_t* rebuild_delta,
+                      uint32_t* block, cudaStream_t stream, const uint64_t* recv_counts, int p);
+
+// PR with p logical workers on the context's GPU.
+int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int p, int bits, int rounds,
+                             bsg_run_stats* stats, cudaStream_t stream);
+
+} // namespace bsg

@@ -1,0 +1,520 @@
+// radix.cu -- stable LSD radix sort of uint32 keys for sm_100a.
+//
+// Restates the count-sort round of radix.hpp:155-176 (histogram, exclusive
+// scan, stable forward scatter) and serial_radix_sort (radix.hpp:180-201) as
+// three kernels:
+//   K1 hist_kernel      -- one read of the keys, per-CTA shared-memory
+//                          histograms of every digit with per-thread run-length
+//                          aggregation (skewed inputs hit far fewer atomics),
+//                          flushed to per-chunk global bins.
+//   K2 scan_plan_kernel -- exclusive digit scans -> per-chunk output bases, and
+//                          a device-resident PassPlan that skips identity
+//                          passes (one digit value holds all n keys) and picks
+//                          the ping-pong buffers so the result lands in `out`
+//                          with no host round trip.
+//   K3 onesweep_kernel  -- one stable pass: TMA bulk load of an 8192-key tile
+//                          into shared memory, warp-striped match-any ranking
+//                          (original order inside a warp = item-major,
+//                          lane-minor, so ranks are stable), per-warp digit
+//                          counts -> early publication of the tile aggregate,
+//                          decoupled look-back across tiles per digit, then the
+//                          tile is staged in digit order in shared memory and
+//                          written out in digit runs (coalesced).
+// All counts/positions are 64-bit at the chunk level (a chunk is <= 2^29
+// keys so the 30-bit look-back payload never overflows).
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "radix.cuh"
+
+namespace bsg {
+
+namespace {
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1;
+constexpr int kHistThreads = 256;
+constexpr int kScanThreads = 256;
+
+// ---------------------------------------------------------------------------
+// K1: digit histograms.  NDIG digits of BITS bits starting at first_shift.
+// ---------------------------------------------------------------------------
+template <int BITS, int NDIG>
+__global__ void __launch_bounds__(kHistThreads)
+    hist_kernel(const uint32_t* __restrict__ in, uint64_t n, int first_shift,
+                uint32_t* __restrict__ hist) {
+    constexpr int RADIX = 1 << BITS;
+    constexpr uint32_t MASK = RADIX - 1;
+    __shared__ uint32_t sh[NDIG * RADIX];
+    for (int i = threadIdx.x; i < NDIG * RADIX; i += kHistThreads) sh[i] = 0;
+    __syncthreads();
+
+    const uint64_t mis = (reinterpret_cast<uintptr_t>(in) >> 2) & 3;
+    uint64_t head = mis ? 4 - mis : 0;
+    if (head > n) head = n;
+    const uint4* body = reinterpret_cast<const uint4*>(in + head);
+    const uint64_t groups = ((n - head) / 4) / 2; // 8-key groups
+
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kHistThreads;
+    for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * kHistThreads + threadIdx.x; g < groups;
+         g += stride) {
+        const uint4 a = ldg_stream_v4(body + 2 * g);
+        const uint4 b = ldg_stream_v4(body + 2 * g + 1);
+        const uint32_t k[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < NDIG; ++j) {
+            const int s = first_shift + j * BITS;
+            uint32_t cur = (k[0] >> s) & MASK, cnt = 1;
+#pragma unroll
+            for (int t = 1; t < 8; ++t) {
+                const uint32_t d = (k[t] >> s) & MASK;
+                if (d == cur) {
+                    ++cnt;
+                } else {
+                    atomicAdd(&sh[j * RADIX + cur], cnt);
+                    cur = d;
+                    cnt = 1;
+                }
+            }
+            atomicAdd(&sh[j * RADIX + cur], cnt);
+        }
+    }
+    if (blockIdx.x == 0) {
+        auto count_one = [&](uint32_t key) {
+#pragma unroll
+            for (int j = 0; j < NDIG; ++j)
+                atomicAdd(&sh[j * RADIX + ((key >> (first_shift + j * BITS)) & MASK)], 1u);
+        };
+        for (uint64_t i = threadIdx.x; i < head; i += kHistThreads) count_one(in[i]);
+        for (uint64_t i = head + groups * 8 + threadIdx.x; i < n; i += kHistThreads) count_one(in[i]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NDIG * RADIX; i += kHistThreads)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// ---------------------------------------------------------------------------
+// K2: digit scans + pass plan.  hist/base layout [chunk][pass][radix].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kScanThreads)
+    scan_plan_kernel(const uint32_t* __restrict__ hist, int chunks, int passes, int radix,
+                     uint64_t n, uint64_t* __restrict__ base, PassPlan* __restrict__ plan,
+                     const uint32_t* in, uint32_t* out, uint32_t* tmp, int allow_skip) {
+    __shared__ uint64_t s_warp[kScanThreads / 32];
+    __shared__ int s_active[kMaxPasses];
+    const int d = threadIdx.x;
+    const int lane = d & 31, warp = d >> 5;
+    for (int p = 0; p < passes; ++p) {
+        uint64_t total = 0;
+        if (d < radix)
+            for (int c = 0; c < chunks; ++c) total += hist[(static_cast<uint64_t>(c) * passes + p) * radix + d];
+        const int ident = __syncthreads_or(d < radix && total == n);
+        const uint64_t incl = warp_inclusive_scan(total);
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        uint64_t excl = incl - total;
+        for (int w = 0; w < warp; ++w) excl += s_warp[w];
+        __syncthreads();
+        if (d < radix) {
+            uint64_t run = excl;
+            for (int c = 0; c < chunks; ++c) {
+                const uint64_t idx = (static_cast<uint64_t>(c) * passes + p) * radix + d;
+                base[idx] = run;
+                run += hist[idx];
+            }
+        }
+        if (d == 0) s_active[p] = (n > 0) && !(allow_skip && ident);
+    }
+    __syncthreads();
+    if (d != 0) return;
+    int m = 0;
+    for (int p = 0; p < passes; ++p) m += s_active[p];
+    PassPlan pl;
+    for (int p = 0; p < kMaxPasses; ++p) {
+        pl.src[p] = nullptr;
+        pl.dst[p] = nullptr;
+        pl.active[p] = p < passes ? s_active[p] : 0;
+    }
+    pl.executed = m;
+    if (m == 0) {
+        pl.final_buf = in;
+        pl.need_copy = (in != out) && n > 0;
+    } else {
+        const bool forward = (in == out) && (m % 2 == 1);
+        const uint32_t* cur = in;
+        int j = 0;
+        for (int p = 0; p < passes; ++p) {
+            if (!s_active[p]) continue;
+            uint32_t* dst;
+            if (forward) dst = (j % 2 == 0) ? tmp : out;
+            else dst = ((m - 1 - j) % 2 == 0) ? out : tmp;
+            pl.src[p] = cur;
+            pl.dst[p] = dst;
+            cur = dst;
+            ++j;
+        }
+        pl.final_buf = cur;
+        pl.need_copy = cur != out;
+    }
+    *plan = pl;
+}
+
+__global__ void final_copy_kernel(const PassPlan* __restrict__ plan, uint32_t* out, uint64_t n) {
+    if (!plan->need_copy) return;
+    const uint32_t* src = plan->final_buf;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (vec) {
+        const uint64_t nv = n / 4;
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* o4 = reinterpret_cast<uint4*>(out);
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride)
+            o4[i] = ldg_stream_v4(s4 + i);
+        for (uint64_t i = nv * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+            out[i] = src[i];
+    } else {
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+            out[i] = src[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: one-sweep stable pass (ranking + decoupled look-back + staged scatter).
+// ---------------------------------------------------------------------------
+template <int BITS, int THREADS, int ITEMS>
+struct OnesweepSmem {
+    static constexpr int RADIX = 1 << BITS;
+    static constexpr int WARPS = THREADS / 32;
+    static constexpr int TILE = THREADS * ITEMS;
+    static constexpr size_t keys_off = 0;                                        // TILE u32
+    static constexpr size_t wcnt_off = keys_off + sizeof(uint32_t) * TILE;       // WARPS*RADIX u32
+    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX u64
+    static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
+    static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
+    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // tile id etc
+    static constexpr size_t bar_off = misc_off + 16;                              // mbarrier (8B aligned)
+    static constexpr size_t bytes = bar_off + 16;
+};
+
+template <int BITS, int THREADS, int ITEMS, bool USE_TMA>
+__global__ void __launch_bounds__(THREADS, 2)
+    onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
+                    int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+                    uint32_t* __restrict__ tile_counter) {
+    using L = OnesweepSmem<BITS, THREADS, ITEMS>;
+    constexpr int RADIX = L::RADIX;
+    constexpr int WARPS = L::WARPS;
+    constexpr int TILE = L::TILE;
+    constexpr uint32_t MASK = RADIX - 1;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* s_keys = reinterpret_cast<uint32_t*>(smem + L::keys_off);
+    uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + L::wcnt_off);
+    uint64_t* s_delta = reinterpret_cast<uint64_t*>(smem + L::delta_off);
+    uint32_t* s_excl = reinterpret_cast<uint32_t*>(smem + L::excl_off);
+    uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
+    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L::misc_off);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+
+    if (!plan->active[pass]) return;
+    const uint32_t* __restrict__ src = plan->src[pass] + chunk_off;
+    uint32_t* __restrict__ dst = plan->dst[pass];
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+
+    if (tid == 0) {
+        s_misc[0] = atomicAdd(tile_counter, 1u);
+        if constexpr (USE_TMA) {
+            mbar_init(s_bar, 1);
+            fence_mbar_init();
+        }
+    }
+    for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_misc[0];
+    const uint32_t tile_start = tile * TILE;
+    const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - tile_start);
+
+    // ---- load the tile ---------------------------------------------------
+    uint32_t keys[ITEMS];
+    const uint32_t wbase = warp * (32 * ITEMS);
+    if constexpr (USE_TMA) {
+        const uint32_t vec_keys = valid & ~3u;
+        if (tid == 0) {
+            if (vec_keys) {
+                mbar_arrive_expect_tx(s_bar, vec_keys * 4);
+                tma_bulk_g2s(s_keys, src + tile_start, vec_keys * 4, s_bar);
+            } else {
+                mbar_arrive_expect_tx(s_bar, 0);
+            }
+        }
+        mbar_wait_parity(s_bar, 0);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t idx = wbase + i * 32 + lane;
+            keys[i] = idx < vec_keys ? s_keys[idx] : (idx < valid ? src[tile_start + idx] : 0u);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t idx = wbase + i * 32 + lane;
+            keys[i] = idx < valid ? __ldg(src + tile_start + idx) : 0u;
+        }
+    }
+
+    // ---- warp-local stable ranks + per-warp digit counts ------------------
+    uint32_t ranks[ITEMS];
+    uint32_t* wc = s_wcnt + warp * RADIX;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint32_t idx = wbase + i * 32 + lane;
+        const bool ok = idx < valid;
+        const uint32_t d = ok ? (keys[i] >> shift) & MASK : static_cast<uint32_t>(RADIX);
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = 31 - __clz(peers);
+        uint32_t before = 0;
+        if (lane == leader && ok) {
+            before = wc[d];
+            wc[d] = before + __popc(peers);
+        }
+        before = __shfl_sync(0xffffffffu, before, leader);
+        ranks[i] = before + __popc(peers & lt);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // ---- per-digit: warp prefix, tile count, publish aggregate -----------
+    uint32_t tile_cnt = 0;
+    if (tid < RADIX) {
+#pragma unroll 4
+        for (int w = 0; w < WARPS; ++w) {
+            const uint32_t c = s_wcnt[w * RADIX + tid];
+            s_wcnt[w * RADIX + tid] = tile_cnt;
+            tile_cnt += c;
+        }
+        st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
+                       (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
+    }
+    // block exclusive scan of tile_cnt over the RADIX digits
+    constexpr int SCAN_WARPS = (RADIX + 31) / 32;
+    uint32_t incl = 0;
+    if (warp < SCAN_WARPS) {
+        incl = warp_inclusive_scan(tile_cnt);
+        if (lane == 31) s_scan[warp] = incl;
+    }
+    __syncthreads();
+    if (tid < RADIX) {
+        uint32_t excl = incl - tile_cnt;
+        for (int w = 0; w < warp; ++w) excl += s_scan[w];
+        s_excl[tid] = excl;
+#pragma unroll 4
+        for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
+    }
+    __syncthreads();
+
+    // ---- stage the tile in digit order in shared memory ------------------
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint32_t idx = wbase + i * 32 + lane;
+        if (idx < valid) {
+            const uint32_t d = (keys[i] >> shift) & MASK;
+            s_keys[wc[d] + ranks[i]] = keys[i];
+        }
+    }
+
+    // ---- decoupled look-back per digit ----------------------------------
+    if (tid < RADIX) {
+        uint32_t prefix = 0;
+        if (tile > 0) {
+            int64_t t = static_cast<int64_t>(tile) - 1;
+            while (true) {
+                const uint32_t s = ld_relaxed_gpu(&status[static_cast<uint64_t>(t) * RADIX + tid]);
+                if ((s & ~kValMask) == 0) continue;
+                prefix += s & kValMask;
+                if (s & kFlagInc) break;
+                --t;
+            }
+            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+        }
+        s_delta[tid] = digit_base[tid] + prefix - s_excl[tid];
+    }
+    __syncthreads();
+
+    // ---- write digit runs -------------------------------------------------
+    for (uint32_t i = tid; i < valid; i += THREADS) {
+        const uint32_t k = s_keys[i];
+        dst[s_delta[(k >> shift) & MASK] + i] = k;
+    }
+}
+
+template <int BITS>
+int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
+                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+    using L = OnesweepSmem<BITS, kOnesweepThreads, kOnesweepItems>;
+    constexpr int RADIX = 1 << BITS;
+    auto kern_tma = onesweep_kernel<BITS, kOnesweepThreads, kOnesweepItems, true>;
+    auto kern_ldg = onesweep_kernel<BITS, kOnesweepThreads, kOnesweepItems, false>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
+        cudaFuncSetAttribute(kern_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
+        attr_set = true;
+    }
+    const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
+    // status layout per chunk: [counter (32 words)] [tiles * RADIX]
+    const uint64_t words_per_chunk = 32 + ((kChunkKeys + L::TILE - 1) / L::TILE) * RADIX;
+    int launches = 0;
+    for (uint64_t c = 0; c < chunks; ++c) {
+        const uint64_t off = c * kChunkKeys;
+        const uint32_t len = static_cast<uint32_t>(std::min<uint64_t>(kChunkKeys, n - off));
+        const uint32_t tiles = (len + L::TILE - 1) / L::TILE;
+        uint32_t* st = status + c * words_per_chunk;
+        const uint64_t* base = base_for_pass + c * static_cast<uint64_t>(passes_stride) * RADIX;
+        if (use_tma)
+            kern_tma<<<tiles, kOnesweepThreads, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st);
+        else
+            kern_ldg<<<tiles, kOnesweepThreads, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st);
+        ++launches;
+    }
+    return launches;
+}
+
+template <int BITS>
+uint64_t status_words_for(uint64_t n) {
+    constexpr int RADIX = 1 << BITS;
+    const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
+    const uint64_t per_chunk = 32 + ((kChunkKeys + kOnesweepTile - 1) / kOnesweepTile) * RADIX;
+    if (chunks <= 1) return 32 + ((n + kOnesweepTile - 1) / kOnesweepTile) * RADIX;
+    return chunks * per_chunk;
+}
+
+inline int grid_for_stream(uint64_t items_per_thread_groups) {
+    const uint64_t want = (items_per_thread_groups + kHistThreads - 1) / kHistThreads;
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
+}
+
+} // namespace
+
+uint64_t onesweep_status_words(uint64_t n) { return status_words_for<8>(n); }
+
+int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws,
+                       cudaStream_t stream, bool allow_tma) {
+    constexpr int PASSES = 4;
+    constexpr int RADIX = 256;
+    const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
+    int launches = 0;
+    if (cudaMemsetAsync(ws.hist, 0, chunks * PASSES * RADIX * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    for (uint64_t c = 0; c < chunks && n; ++c) {
+        const uint64_t off = c * kChunkKeys;
+        const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
+        hist_kernel<8, PASSES><<<grid_for_stream(len / 8), kHistThreads, 0, stream>>>(in + off, len, 0,
+                                                                                        ws.hist + c * PASSES * RADIX);
+        ++launches;
+    }
+    scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), PASSES, RADIX, n, ws.base,
+                                                     ws.plan, in, out, ws.tmp, 1);
+    ++launches;
+    const bool tma = allow_tma && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
+                                    reinterpret_cast<uintptr_t>(ws.tmp)) & 15) == 0;
+    const uint64_t sw = status_words_for<8>(n);
+    for (int p = 0; p < PASSES && n; ++p) {
+        if (cudaMemsetAsync(ws.status, 0, sw * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+        launches += launch_onesweep_pass<8>(ws.plan, p, n, 8 * p, ws.base + p * RADIX, PASSES, ws.status, stream, tma);
+    }
+    final_copy_kernel<<<kSmCountB200 * 4, 256, 0, stream>>>(ws.plan, out, n);
+    ++launches;
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    return launches;
+}
+
+int launch_count_pass(const uint32_t* in, uint32_t* out, uint64_t n, int bits, int shift,
+                      const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma) {
+    const int radix = 1 << bits;
+    const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
+    int launches = 0;
+    if (cudaMemsetAsync(ws.hist, 0, chunks * radix * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    for (uint64_t c = 0; c < chunks && n; ++c) {
+        const uint64_t off = c * kChunkKeys;
+        const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
+        uint32_t* h = ws.hist + c * radix;
+        const int grid = grid_for_stream(len / 8);
+        switch (bits) {
+        case 1: hist_kernel<1, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 2: hist_kernel<2, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 4: hist_kernel<4, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 8: hist_kernel<8, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        default: return -1;
+        }
+        ++launches;
+    }
+    // The reference always performs the pass (no identity skip), but an
+    // identity pass is a copy either way; skipping keeps the result identical.
+    scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), 1, radix, n, ws.base, ws.plan,
+                                                     in, out, ws.tmp, 1);
+    ++launches;
+    const bool tma = allow_tma && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
+                                    reinterpret_cast<uintptr_t>(ws.tmp)) & 15) == 0;
+    if (n) {
+        uint64_t sw = 0;
+        switch (bits) {
+        case 1: sw = status_words_for<1>(n); break;
+        case 2: sw = status_words_for<2>(n); break;
+        case 4: sw = status_words_for<4>(n); break;
+        default: sw = status_words_for<8>(n); break;
+        }
+        if (cudaMemsetAsync(ws.status, 0, sw * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+        switch (bits) {
+        case 1: launches += launch_onesweep_pass<1>(ws.plan, 0, n, shift, ws.base, 1, ws.status, stream, tma); break;
+        case 2: launches += launch_onesweep_pass<2>(ws.plan, 0, n, shift, ws.base, 1, ws.status, stream, tma); break;
+        case 4: launches += launch_onesweep_pass<4>(ws.plan, 0, n, shift, ws.base, 1, ws.status, stream, tma); break;
+        default: launches += launch_onesweep_pass<8>(ws.plan, 0, n, shift, ws.base, 1, ws.status, stream, tma); break;
+        }
+    }
+    final_copy_kernel<<<kSmCountB200 * 4, 256, 0, stream>>>(ws.plan, out, n);
+    ++launches;
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    return launches;
+}
+
+namespace {
+__global__ void widen_counts_kernel(const uint32_t* __restrict__ c32, uint64_t* __restrict__ c64, int radix,
+                                    int chunks) {
+    for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < radix; d += gridDim.x * blockDim.x) {
+        uint64_t s = 0;
+        for (int c = 0; c < chunks; ++c) s += c32[static_cast<uint64_t>(c) * radix + d];
+        c64[d] = s;
+    }
+}
+} // namespace
+
+int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uint64_t* counts, uint32_t* scratch32,
+                        cudaStream_t stream) {
+    const int radix = 1 << bits;
+    const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
+    int launches = 0;
+    if (cudaMemsetAsync(scratch32, 0, chunks * radix * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    for (uint64_t c = 0; c < chunks && n; ++c) {
+        const uint64_t off = c * kChunkKeys;
+        const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
+        uint32_t* h = scratch32 + c * radix;
+        const int grid = grid_for_stream(len / 8);
+        switch (bits) {
+        case 1: hist_kernel<1, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 2: hist_kernel<2, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 4: hist_kernel<4, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 8: hist_kernel<8, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        default: return -1;
+        }
+        ++launches;
+    }
+    widen_counts_kernel<<<(radix + 255) / 256, 256, 0, stream>>>(scratch32, counts, radix, static_cast<int>(chunks));
+    ++launches;
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    return launches;
+}
+
+} // namespace bsg

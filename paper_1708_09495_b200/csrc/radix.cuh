@@ -1,0 +1,54 @@
+// radix.cuh -- host-side launchers for the LSD radix kernels (radix.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bsg {
+
+constexpr int kMaxPasses = 8;
+
+// Device-resident plan of one sort: which digit passes execute and where each
+// reads and writes.  Built on the device from the histograms (identity passes,
+// where one digit value holds all n keys, are skipped without a host sync).
+struct PassPlan {
+    const uint32_t* src[kMaxPasses];
+    uint32_t* dst[kMaxPasses];
+    int32_t active[kMaxPasses];
+    int32_t executed;          // number of active passes
+    int32_t need_copy;         // result is not in `out` yet
+    const uint32_t* final_buf; // buffer holding the result after the last pass
+};
+
+// Tile geometry of the one-sweep pass.
+constexpr int kOnesweepThreads = 512;
+constexpr int kOnesweepItems = 16;
+constexpr int kOnesweepTile = kOnesweepThreads * kOnesweepItems; // 8192 keys
+// Keys per look-back chunk: status words hold a 30-bit count.
+constexpr uint64_t kChunkKeys = uint64_t{1} << 29;
+
+struct RadixWorkspace {
+    uint32_t* tmp = nullptr;     // ping-pong buffer, >= n keys
+    uint32_t* status = nullptr;  // look-back status words + tile counters
+    uint32_t* hist = nullptr;    // [chunks][passes][256]
+    uint64_t* base = nullptr;    // [chunks][passes][256]
+    PassPlan* plan = nullptr;
+};
+
+// Bytes of look-back status needed for one pass over min(n, kChunkKeys) keys.
+uint64_t onesweep_status_words(uint64_t n);
+
+// Full LSD sort of n keys with 8-bit passes over bits [0, 8*passes).
+// Returns the number of kernel launches enqueued, or -1 on launch error.
+int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws,
+                       cudaStream_t stream, bool allow_tma);
+
+// One stable count-sort pass over the `bits`-wide digit at bit `shift`
+// (bits in {1,2,4,8}).  Returns launches enqueued or -1.
+int launch_count_pass(const uint32_t* in, uint32_t* out, uint64_t n, int bits, int shift,
+                      const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma);
+
+// Digit histogram of one `bits`-wide digit into 64-bit counts (PR count_digits).
+int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uint64_t* counts,
+                        uint32_t* scratch32, cudaStream_t stream);
+
+} // namespace bsg

@@ -1,0 +1,141 @@
+"""GPU parity of the count-sort round and the serial LSD sort against the
+oracle (radix_test.cpp / acceptance.cpp criteria 1-2 restated)."""
+import numpy as np
+import pytest
+
+from conftest import stable_digit_sort
+
+pytestmark = pytest.mark.gpu
+
+
+def test_count_sort_round_kats(cuda, bsg):
+    # radix_test.cpp:137-151
+    assert bsg.radix.count_sort_round(np.array([], np.uint32), 0, 256).size == 0
+    assert bsg.radix.count_sort_round(np.array([], np.uint32), 3, 256).size == 0
+    out = bsg.radix.count_sort_round(np.array([0x0103, 0x0201, 0x0102], np.uint32), 0, 256)
+    assert out.tolist() == [0x0201, 0x0102, 0x0103]
+    inp = np.array([0x0101, 0x0001], np.uint32)
+    assert bsg.radix.count_sort_round(inp, 0, 256).tolist() == inp.tolist()
+
+
+def test_count_sort_round_vs_stable_oracle(cuda, bsg, orc):
+    # radix_test.cpp:153-166 (40 random arrays, seed 2024, len < 300)
+    draws = orc.mt64_draws(40 * 400, 2024)
+    pos = 0
+    for _ in range(40):
+        n = int(draws[pos] % 300); pos += 1
+        keys = (draws[pos:pos + n] & 0xFFFFFFFF).astype(np.uint32); pos += n
+        for radix in (256, 65536):
+            rounds = 32 // (radix.bit_length() - 1)
+            rnd = int(draws[pos] % rounds); pos += 1
+            got = bsg.radix.count_sort_round(keys, rnd, radix)
+            np.testing.assert_array_equal(got, stable_digit_sort(keys, rnd, radix))
+            np.testing.assert_array_equal(got, orc.count_sort_round(keys, rnd, radix))
+
+
+@pytest.mark.parametrize("radix", [2, 4, 16, 256, 65536])
+@pytest.mark.parametrize("n", [1, 2, 3, 10, 1000, 8191, 8192, 8193, 100003])
+def test_count_sort_round_every_round(cuda, bsg, orc, radix, n):
+    keys = orc.generate_uniform_keys(n, 1000 + n)
+    rounds = 32 // (radix.bit_length() - 1)
+    for rnd in sorted({0, rounds // 2, rounds - 1}):
+        np.testing.assert_array_equal(bsg.radix.count_sort_round(keys, rnd, radix),
+                                      orc.count_sort_round(keys, rnd, radix))
+
+
+@pytest.mark.parametrize("seed", [7, 99])
+def test_index_tagged_stability(cuda, bsg, orc, seed):
+    # radix_test.cpp:67-83 / acceptance.cpp:124-141
+    n = 10000
+    draws = orc.mt64_draws(n, seed)
+    tagged = (((draws % (1 << 18)).astype(np.uint64) << np.uint64(14)) | np.arange(n, dtype=np.uint64)).astype(np.uint32)
+    out = bsg.radix.count_sort_round(tagged, 3, 256)
+    d = out >> 24
+    assert np.all(d[:-1] <= d[1:])
+    same = d[:-1] == d[1:]
+    assert np.all((out[:-1] & 0x3FFF)[same] < (out[1:] & 0x3FFF)[same])
+    np.testing.assert_array_equal(out, orc.count_sort_round(tagged, 3, 256))
+
+
+def adversarial(kind, n):
+    # acceptance.cpp:60-72
+    if kind == 0:
+        return np.full(n, 0xABCD1234, np.uint32)
+    if kind == 1:
+        return (np.arange(n, dtype=np.uint64) * 3).astype(np.uint32)
+    return ((n - np.arange(n, dtype=np.uint64)) * 3).astype(np.uint32)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 10, 1000, 100000, 1000000])
+def test_serial_radix_sort_grid(cuda, bsg, orc, n):
+    # acceptance.cpp:85-120 criterion 1 (SR4 column) + both radixes
+    inputs = [orc.generate_uniform_keys(n, s) for s in (11, 22, 33)] + [adversarial(k, n) for k in range(3)]
+    for keys in inputs:
+        expect = np.sort(keys)
+        for radix in (256, 65536, 2):
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, radix), expect)
+
+
+def test_serial_equals_composed_rounds(cuda, bsg, orc):
+    # radix_test.cpp:93-104
+    keys = orc.generate_uniform_keys(5000, 11)
+    for radix, rounds in ((256, 4), (65536, 2)):
+        comp = keys
+        for r in range(rounds):
+            comp = bsg.radix.count_sort_round(comp, r, radix)
+        np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, radix), comp)
+        np.testing.assert_array_equal(comp, orc.serial_radix_sort(keys, radix))
+
+
+def test_device_tensors_and_inplace(cuda, bsg, orc):
+    torch = cuda
+    keys = orc.generate_uniform_keys(1 << 20, 5)
+    t = torch.from_numpy(keys.view(np.int32)).cuda().view(torch.uint32)
+    out = bsg.radix.serial_radix_sort(t, 256)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), np.sort(keys))
+    # in place through the C ABI
+    ctx = bsg._lib.context(0)
+    rc = bsg._lib.lib().bsg_radix_sort_u32(ctx.handle, t.data_ptr(), t.data_ptr(), t.numel(), 8, 1,
+                                           torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(t.cpu().numpy(), np.sort(keys))
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_skewed_inputs(cuda, bsg, orc, kind):
+    keys = bsg.generate_skewed_keys(1 << 22, 3, kind)
+    expect = np.sort(keys)
+    for radix in (256, 65536):
+        np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, radix), expect)
+    for rnd in range(4):
+        np.testing.assert_array_equal(bsg.radix.count_sort_round(keys, rnd, 256), orc.count_sort_round(keys, rnd, 256))
+
+
+def test_rejects_bad_arguments(cuda, bsg):
+    # radix_test.cpp:189-195
+    with pytest.raises(ValueError):
+        bsg.radix.count_sort_round(np.array([1], np.uint32), 4, 256)
+    with pytest.raises(ValueError):
+        bsg.radix.count_sort_round(np.array([1], np.uint32), -1, 256)
+    with pytest.raises(ValueError):
+        bsg.radix.count_sort_round(np.array([1], np.uint32), 0, 100)
+    with pytest.raises(ValueError):
+        bsg.radix.count_sort_round(np.array([1], np.uint32), 0, 1 << 32)
+
+
+def test_full_size_2_28_properties(cuda, bsg):
+    # config 2 at full size: sortedness + permutation (checksums) on device
+    torch = cuda
+    n = 1 << 28
+    keys = bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0))
+    t = torch.from_numpy(keys.view(np.int32)).cuda()
+    out = bsg.radix.serial_radix_sort(t.view(torch.uint32), 256).view(torch.int32)
+    o64 = out.to(torch.int64) & 0xFFFFFFFF
+    assert bool((o64[1:] >= o64[:-1]).all())
+    i64 = t.to(torch.int64) & 0xFFFFFFFF
+    assert int(o64.sum()) == int(i64.sum())
+    assert int((o64 * o64 % 1000003).sum()) == int((i64 * i64 % 1000003).sum())
+    ref_sorted = torch.sort(i64).values
+    assert bool(torch.equal(ref_sorted, o64))
