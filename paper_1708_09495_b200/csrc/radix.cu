@@ -24,6 +24,8 @@
 // keys so the 30-bit look-back payload never overflows).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "radix.cuh"
@@ -183,35 +185,51 @@ __global__ void final_copy_kernel(const PassPlan* __restrict__ plan, uint32_t* o
 // ---------------------------------------------------------------------------
 // K3: one-sweep stable pass (ranking + decoupled look-back + staged scatter).
 // ---------------------------------------------------------------------------
-template <int BITS, int THREADS, int ITEMS>
+template <int BITS>
+__device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
+    if constexpr (BITS == 8) {
+        return __byte_perm(k, 0u, 0x4440u | static_cast<uint32_t>(shift >> 3)); // one PRMT
+    } else {
+        return (k >> shift) & ((1u << BITS) - 1u);
+    }
+}
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
 struct OnesweepSmem {
     static constexpr int RADIX = 1 << BITS;
     static constexpr int WARPS = THREADS / 32;
     static constexpr int TILE = THREADS * ITEMS;
-    static constexpr size_t keys_off = 0;                                        // TILE u32
-    static constexpr size_t wcnt_off = keys_off + sizeof(uint32_t) * TILE;       // WARPS*RADIX u32
-    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX u64
+    using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
+    static constexpr size_t in_off = 0;                                          // TILE u32 (TMA target)
+    static constexpr size_t out_off = in_off + sizeof(uint32_t) * TILE;          // TILE u32 (digit-ordered)
+    static constexpr size_t wcnt_off = out_off + sizeof(uint32_t) * TILE;        // WARPS*RADIX u32
+    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX Off
     static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
     static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
-    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // tile id etc
-    static constexpr size_t bar_off = misc_off + 16;                              // mbarrier (8B aligned)
+    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // tile id
+    static constexpr size_t bar_off = misc_off + 16;                              // mbarrier
     static constexpr size_t bytes = bar_off + 16;
 };
 
-template <int BITS, int THREADS, int ITEMS, bool USE_TMA>
-__global__ void __launch_bounds__(THREADS, 2)
+// dbg: 0 = normal; bit0 = skip look-back waits (timing only, wrong output);
+//      bit1 = unstable atomic ranks instead of match-any (timing only).
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
+__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
                     int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
-                    uint32_t* __restrict__ tile_counter) {
-    using L = OnesweepSmem<BITS, THREADS, ITEMS>;
+                    uint32_t* __restrict__ tile_counter, int use_tma, int dbg) {
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
+    using Off = typename L::Off;
     constexpr int RADIX = L::RADIX;
     constexpr int WARPS = L::WARPS;
     constexpr int TILE = L::TILE;
-    constexpr uint32_t MASK = RADIX - 1;
+    static_assert(ITEMS % 2 == 0, "ranks are packed in pairs");
+    static_assert(RADIX <= THREADS, "one thread per digit");
     extern __shared__ __align__(128) uint8_t smem[];
-    uint32_t* s_keys = reinterpret_cast<uint32_t*>(smem + L::keys_off);
+    uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
+    uint32_t* s_out = reinterpret_cast<uint32_t*>(smem + L::out_off);
     uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + L::wcnt_off);
-    uint64_t* s_delta = reinterpret_cast<uint64_t*>(smem + L::delta_off);
+    Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
     uint32_t* s_excl = reinterpret_cast<uint32_t*>(smem + L::excl_off);
     uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
     uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L::misc_off);
@@ -227,7 +245,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 
     if (tid == 0) {
         s_misc[0] = atomicAdd(tile_counter, 1u);
-        if constexpr (USE_TMA) {
+        if (use_tma) {
             mbar_init(s_bar, 1);
             fence_mbar_init();
         }
@@ -237,60 +255,59 @@ __global__ void __launch_bounds__(THREADS, 2)
     const uint32_t tile = s_misc[0];
     const uint32_t tile_start = tile * TILE;
     const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - tile_start);
+    const bool full = valid == TILE;
 
-    // ---- load the tile ---------------------------------------------------
-    uint32_t keys[ITEMS];
-    const uint32_t wbase = warp * (32 * ITEMS);
-    if constexpr (USE_TMA) {
+    // ---- tile -> shared memory (one TMA bulk copy) ------------------------
+    if (use_tma) {
         const uint32_t vec_keys = valid & ~3u;
         if (tid == 0) {
-            if (vec_keys) {
-                mbar_arrive_expect_tx(s_bar, vec_keys * 4);
-                tma_bulk_g2s(s_keys, src + tile_start, vec_keys * 4, s_bar);
-            } else {
-                mbar_arrive_expect_tx(s_bar, 0);
-            }
+            mbar_arrive_expect_tx(s_bar, vec_keys * 4);
+            if (vec_keys) tma_bulk_g2s(s_in, src + tile_start, vec_keys * 4, s_bar);
         }
+        for (uint32_t i = vec_keys + tid; i < valid; i += THREADS) s_in[i] = src[tile_start + i];
         mbar_wait_parity(s_bar, 0);
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const uint32_t idx = wbase + i * 32 + lane;
-            keys[i] = idx < vec_keys ? s_keys[idx] : (idx < valid ? src[tile_start + idx] : 0u);
-        }
+        __syncthreads();
     } else {
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const uint32_t idx = wbase + i * 32 + lane;
-            keys[i] = idx < valid ? __ldg(src + tile_start + idx) : 0u;
-        }
+        for (uint32_t i = tid; i < valid; i += THREADS) s_in[i] = __ldg(src + tile_start + i);
+        __syncthreads();
     }
 
     // ---- warp-local stable ranks + per-warp digit counts ------------------
-    uint32_t ranks[ITEMS];
+    // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS) of the tile, item i of lane
+    // l is key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
+    const uint32_t wbase = warp * (32 * ITEMS);
+    const uint32_t* w_in = s_in + wbase;
     uint32_t* wc = s_wcnt + warp * RADIX;
     const uint32_t lt = lanemask_lt();
+    uint32_t packed[ITEMS / 2];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const uint32_t idx = wbase + i * 32 + lane;
-        const bool ok = idx < valid;
-        const uint32_t d = ok ? (keys[i] >> shift) & MASK : static_cast<uint32_t>(RADIX);
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const int leader = 31 - __clz(peers);
-        uint32_t before = 0;
-        if (lane == leader && ok) {
-            before = wc[d];
-            wc[d] = before + __popc(peers);
+        const bool ok = full || idx < valid;
+        const uint32_t d = ok ? digit_of_key<BITS>(w_in[i * 32 + lane], shift) : static_cast<uint32_t>(RADIX);
+        uint32_t r;
+        if (dbg & 2) {
+            r = ok ? atomicAdd(&wc[d], 1u) : 0u;
+        } else {
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const int leader = __ffs(peers) - 1;
+            uint32_t before = 0;
+            if (lane == leader && ok) {
+                before = wc[d];
+                wc[d] = before + __popc(peers);
+            }
+            r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers & lt);
+            __syncwarp();
         }
-        before = __shfl_sync(0xffffffffu, before, leader);
-        ranks[i] = before + __popc(peers & lt);
-        __syncwarp();
+        if (i & 1) packed[i >> 1] |= r << 16;
+        else packed[i >> 1] = r;
     }
     __syncthreads();
 
     // ---- per-digit: warp prefix, tile count, publish aggregate -----------
     uint32_t tile_cnt = 0;
     if (tid < RADIX) {
-#pragma unroll 4
+#pragma unroll
         for (int w = 0; w < WARPS; ++w) {
             const uint32_t c = s_wcnt[w * RADIX + tid];
             s_wcnt[w * RADIX + tid] = tile_cnt;
@@ -299,7 +316,6 @@ __global__ void __launch_bounds__(THREADS, 2)
         st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
                        (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
     }
-    // block exclusive scan of tile_cnt over the RADIX digits
     constexpr int SCAN_WARPS = (RADIX + 31) / 32;
     uint32_t incl = 0;
     if (warp < SCAN_WARPS) {
@@ -309,86 +325,153 @@ __global__ void __launch_bounds__(THREADS, 2)
     __syncthreads();
     if (tid < RADIX) {
         uint32_t excl = incl - tile_cnt;
-        for (int w = 0; w < warp; ++w) excl += s_scan[w];
+#pragma unroll
+        for (int w = 0; w < SCAN_WARPS; ++w)
+            if (w < warp) excl += s_scan[w];
         s_excl[tid] = excl;
-#pragma unroll 4
+#pragma unroll
         for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
     }
     __syncthreads();
 
-    // ---- stage the tile in digit order in shared memory ------------------
+    // ---- stage the tile in digit order ------------------------------------
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const uint32_t idx = wbase + i * 32 + lane;
-        if (idx < valid) {
-            const uint32_t d = (keys[i] >> shift) & MASK;
-            s_keys[wc[d] + ranks[i]] = keys[i];
+        if (full || idx < valid) {
+            const uint32_t k = w_in[i * 32 + lane];
+            const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+            s_out[wc[digit_of_key<BITS>(k, shift)] + r] = k;
         }
     }
 
-    // ---- decoupled look-back per digit ----------------------------------
+    // ---- decoupled look-back, 4 predecessors per round trip -------------
     if (tid < RADIX) {
         uint32_t prefix = 0;
-        if (tile > 0) {
+        if (tile > 0 && !(dbg & 1)) {
             int64_t t = static_cast<int64_t>(tile) - 1;
             while (true) {
-                const uint32_t s = ld_relaxed_gpu(&status[static_cast<uint64_t>(t) * RADIX + tid]);
-                if ((s & ~kValMask) == 0) continue;
-                prefix += s & kValMask;
-                if (s & kFlagInc) break;
-                --t;
+                uint32_t s[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    s[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid]) : kFlagInc;
+                int used = 0;
+                bool done = false;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (done || used < j) break;
+                    if ((s[j] & ~kValMask) == 0) break;
+                    prefix += s[j] & kValMask;
+                    ++used;
+                    if (s[j] & kFlagInc) done = true;
+                }
+                if (done) break;
+                t -= used;
             }
-            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
         }
-        s_delta[tid] = digit_base[tid] + prefix - s_excl[tid];
+        if (tile > 0)
+            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+        s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
     }
     __syncthreads();
 
-    // ---- write digit runs -------------------------------------------------
-    for (uint32_t i = tid; i < valid; i += THREADS) {
-        const uint32_t k = s_keys[i];
-        dst[s_delta[(k >> shift) & MASK] + i] = k;
+    // ---- write digit runs (coalesced within each run) --------------------
+    if (full) {
+#pragma unroll 4
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t i = j * THREADS + tid;
+            const uint32_t k = s_out[i];
+            dst[static_cast<Off>(s_delta[digit_of_key<BITS>(k, shift)] + i)] = k;
+        }
+    } else {
+        for (uint32_t i = tid; i < valid; i += THREADS) {
+            const uint32_t k = s_out[i];
+            dst[static_cast<Off>(s_delta[digit_of_key<BITS>(k, shift)] + i)] = k;
+        }
     }
 }
 
-template <int BITS>
-int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
-                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
-    using L = OnesweepSmem<BITS, kOnesweepThreads, kOnesweepItems>;
+constexpr int kMinTile = 4096;
+
+inline int onesweep_cfg() {
+    static int cfg = [] {
+        const char* e = getenv("BSG_OS_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    return cfg;
+}
+inline int onesweep_dbg() {
+    static int d = [] {
+        const char* e = getenv("BSG_OS_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    return d;
+}
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
+int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
+                        int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
-    auto kern_tma = onesweep_kernel<BITS, kOnesweepThreads, kOnesweepItems, true>;
-    auto kern_ldg = onesweep_kernel<BITS, kOnesweepThreads, kOnesweepItems, false>;
+    auto kern = onesweep_kernel<BITS, THREADS, ITEMS, WIDE>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(kern_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
-        cudaFuncSetAttribute(kern_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
         attr_set = true;
     }
     const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
     // status layout per chunk: [counter (32 words)] [tiles * RADIX]
-    const uint64_t words_per_chunk = 32 + ((kChunkKeys + L::TILE - 1) / L::TILE) * RADIX;
+    const uint64_t words_per_chunk = 32 + ((kChunkKeys + kMinTile - 1) / kMinTile) * RADIX;
     int launches = 0;
+    const int dbg = onesweep_dbg();
     for (uint64_t c = 0; c < chunks; ++c) {
         const uint64_t off = c * kChunkKeys;
         const uint32_t len = static_cast<uint32_t>(std::min<uint64_t>(kChunkKeys, n - off));
         const uint32_t tiles = (len + L::TILE - 1) / L::TILE;
         uint32_t* st = status + c * words_per_chunk;
         const uint64_t* base = base_for_pass + c * static_cast<uint64_t>(passes_stride) * RADIX;
-        if (use_tma)
-            kern_tma<<<tiles, kOnesweepThreads, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st);
-        else
-            kern_ldg<<<tiles, kOnesweepThreads, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st);
+        kern<<<tiles, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0,
+                                                   dbg);
         ++launches;
     }
     return launches;
 }
 
 template <int BITS>
+int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
+                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+    const bool wide = n > 0xFFFFFFFFull;
+    if (wide)
+        return launch_onesweep_cfg<BITS, 512, 16, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                        stream, use_tma);
+    if constexpr (BITS != 8)
+        return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    switch (onesweep_cfg()) {
+    case 1:
+        return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    case 2:
+        return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                          stream, use_tma);
+    case 3:
+        return launch_onesweep_cfg<BITS, 512, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    case 4:
+        return launch_onesweep_cfg<BITS, 256, 32, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    default:
+        return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    }
+}
+
+template <int BITS>
 uint64_t status_words_for(uint64_t n) {
     constexpr int RADIX = 1 << BITS;
     const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
-    const uint64_t per_chunk = 32 + ((kChunkKeys + kOnesweepTile - 1) / kOnesweepTile) * RADIX;
-    if (chunks <= 1) return 32 + ((n + kOnesweepTile - 1) / kOnesweepTile) * RADIX;
+    const uint64_t per_chunk = 32 + ((kChunkKeys + kMinTile - 1) / kMinTile) * RADIX;
+    if (chunks <= 1) return 32 + ((n + kMinTile - 1) / kMinTile) * RADIX;
     return chunks * per_chunk;
 }
 
