@@ -83,7 +83,7 @@ SIGNATURES = {
 }
 
 _lib: Optional[ctypes.CDLL] = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 def lib() -> ctypes.CDLL:

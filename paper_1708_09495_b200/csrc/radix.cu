@@ -184,6 +184,8 @@ __global__ void final_copy_kernel(const PassPlan* __restrict__ plan, uint32_t* o
 
 // ---------------------------------------------------------------------------
 // K3: one-sweep stable pass (ranking + decoupled look-back + staged scatter).
+// Persistent CTAs: while tile k is ranked/scattered, the TMA engine already
+// streams tile k+1 into the other shared-memory buffer.
 // ---------------------------------------------------------------------------
 template <int BITS>
 __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
@@ -194,26 +196,38 @@ __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
     }
 }
 
+// Lanes of the warp holding the same digit (bit-serial ballot multisplit).
+template <int BITS>
+__device__ __forceinline__ uint32_t peers_ballot(uint32_t d) {
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < BITS + 1; ++b) { // BITS+1: the sentinel bin RADIX has bit BITS set
+        const bool bit = (d >> b) & 1u;
+        const uint32_t v = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? v : ~v;
+    }
+    return peers;
+}
+
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 struct OnesweepSmem {
     static constexpr int RADIX = 1 << BITS;
     static constexpr int WARPS = THREADS / 32;
     static constexpr int TILE = THREADS * ITEMS;
     using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
-    static constexpr size_t in_off = 0;                                          // TILE u32 (TMA target)
-    static constexpr size_t out_off = in_off + sizeof(uint32_t) * TILE;          // TILE u32 (digit-ordered)
-    static constexpr size_t wcnt_off = out_off + sizeof(uint32_t) * TILE;        // WARPS*RADIX u32
+    static constexpr size_t in_off = 0;                                          // 2 x TILE u32
+    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // WARPS*RADIX u32
     static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX Off
     static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
     static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
-    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // tile id
-    static constexpr size_t bar_off = misc_off + 16;                              // mbarrier
+    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // 2 tile ids
+    static constexpr size_t bar_off = misc_off + 16;                              // 2 mbarriers
     static constexpr size_t bytes = bar_off + 16;
 };
 
-// dbg: 0 = normal; bit0 = skip look-back waits (timing only, wrong output);
-//      bit1 = unstable atomic ranks instead of match-any (timing only).
-template <int BITS, int THREADS, int ITEMS, bool WIDE>
+// dbg bits (timing experiments only; output is wrong when set):
+//   1 = skip look-back waits, 2 = unstable atomic ranks instead of match/ballot.
+template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
                     int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
@@ -227,166 +241,184 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     static_assert(RADIX <= THREADS, "one thread per digit");
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
-    uint32_t* s_out = reinterpret_cast<uint32_t*>(smem + L::out_off);
     uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + L::wcnt_off);
     Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
     uint32_t* s_excl = reinterpret_cast<uint32_t*>(smem + L::excl_off);
     uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
-    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L::misc_off);
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
 
     if (!plan->active[pass]) return;
     const uint32_t* __restrict__ src = plan->src[pass] + chunk_off;
     uint32_t* __restrict__ dst = plan->dst[pass];
+    const uint32_t ntiles = (chunk_n + TILE - 1) / TILE;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
 
+    // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
+    auto issue = [&](uint32_t tile, int b) {
+        if (tile >= ntiles) return;
+        const uint32_t start = tile * TILE;
+        const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - start);
+        const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_bar[b], vec * 4);
+        if (vec) tma_bulk_g2s(s_in + b * TILE, src + start, vec * 4, &s_bar[b]);
+    };
+
     if (tid == 0) {
-        s_misc[0] = atomicAdd(tile_counter, 1u);
-        if (use_tma) {
-            mbar_init(s_bar, 1);
-            fence_mbar_init();
-        }
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+        const uint32_t t0 = atomicAdd(tile_counter, 1u);
+        s_tile[0] = t0;
+        issue(t0, 0);
     }
     for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
-    __syncthreads();
-    const uint32_t tile = s_misc[0];
-    const uint32_t tile_start = tile * TILE;
-    const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - tile_start);
-    const bool full = valid == TILE;
 
-    // ---- tile -> shared memory (one TMA bulk copy) ------------------------
-    if (use_tma) {
-        const uint32_t vec_keys = valid & ~3u;
-        if (tid == 0) {
-            mbar_arrive_expect_tx(s_bar, vec_keys * 4);
-            if (vec_keys) tma_bulk_g2s(s_in, src + tile_start, vec_keys * 4, s_bar);
-        }
-        for (uint32_t i = vec_keys + tid; i < valid; i += THREADS) s_in[i] = src[tile_start + i];
-        mbar_wait_parity(s_bar, 0);
-        __syncthreads();
-    } else {
-        for (uint32_t i = tid; i < valid; i += THREADS) s_in[i] = __ldg(src + tile_start + i);
-        __syncthreads();
-    }
-
-    // ---- warp-local stable ranks + per-warp digit counts ------------------
-    // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS) of the tile, item i of lane
-    // l is key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
-    const uint32_t wbase = warp * (32 * ITEMS);
-    const uint32_t* w_in = s_in + wbase;
-    uint32_t* wc = s_wcnt + warp * RADIX;
     const uint32_t lt = lanemask_lt();
-    uint32_t packed[ITEMS / 2];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const uint32_t idx = wbase + i * 32 + lane;
-        const bool ok = full || idx < valid;
-        const uint32_t d = ok ? digit_of_key<BITS>(w_in[i * 32 + lane], shift) : static_cast<uint32_t>(RADIX);
-        uint32_t r;
-        if (dbg & 2) {
-            r = ok ? atomicAdd(&wc[d], 1u) : 0u;
-        } else {
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const int leader = __ffs(peers) - 1;
-            uint32_t before = 0;
-            if (lane == leader && ok) {
-                before = wc[d];
-                wc[d] = before + __popc(peers);
-            }
-            r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers & lt);
-            __syncwarp();
+    for (uint32_t k = 0;; ++k) {
+        const int cur = k & 1;
+        __syncthreads(); // s_tile[cur] visible; previous tile's buffer/counters free
+        const uint32_t tile = s_tile[cur];
+        if (tile >= ntiles) break;
+        if (tid == 0) {
+            const uint32_t nxt = atomicAdd(tile_counter, 1u);
+            s_tile[cur ^ 1] = nxt;
+            issue(nxt, cur ^ 1);
         }
-        if (i & 1) packed[i >> 1] |= r << 16;
-        else packed[i >> 1] = r;
-    }
-    __syncthreads();
+        const uint32_t tile_start = tile * TILE;
+        const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - tile_start);
+        const bool full = valid == TILE;
+        uint32_t* buf = s_in + cur * TILE;
+        // non-TMA body / unaligned tail straight from global
+        const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
+        mbar_wait_parity(&s_bar[cur], (k >> 1) & 1);
 
-    // ---- per-digit: warp prefix, tile count, publish aggregate -----------
-    uint32_t tile_cnt = 0;
-    if (tid < RADIX) {
+        // ---- warp-local stable ranks + per-warp digit counts --------------
+        // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS); item i of lane l is
+        // key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
+        const uint32_t wbase = warp * (32 * ITEMS);
+        uint32_t* wc = s_wcnt + warp * RADIX;
+        uint32_t keys[ITEMS];
+        uint32_t packed[ITEMS / 2];
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) {
-            const uint32_t c = s_wcnt[w * RADIX + tid];
-            s_wcnt[w * RADIX + tid] = tile_cnt;
-            tile_cnt += c;
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t idx = wbase + i * 32 + lane;
+            const bool ok = full || idx < valid;
+            keys[i] = ok ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
         }
-        st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
-                       (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
-    }
-    constexpr int SCAN_WARPS = (RADIX + 31) / 32;
-    uint32_t incl = 0;
-    if (warp < SCAN_WARPS) {
-        incl = warp_inclusive_scan(tile_cnt);
-        if (lane == 31) s_scan[warp] = incl;
-    }
-    __syncthreads();
-    if (tid < RADIX) {
-        uint32_t excl = incl - tile_cnt;
 #pragma unroll
-        for (int w = 0; w < SCAN_WARPS; ++w)
-            if (w < warp) excl += s_scan[w];
-        s_excl[tid] = excl;
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
-    }
-    __syncthreads();
-
-    // ---- stage the tile in digit order ------------------------------------
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const uint32_t idx = wbase + i * 32 + lane;
-        if (full || idx < valid) {
-            const uint32_t k = w_in[i * 32 + lane];
-            const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
-            s_out[wc[digit_of_key<BITS>(k, shift)] + r] = k;
-        }
-    }
-
-    // ---- decoupled look-back, 4 predecessors per round trip -------------
-    if (tid < RADIX) {
-        uint32_t prefix = 0;
-        if (tile > 0 && !(dbg & 1)) {
-            int64_t t = static_cast<int64_t>(tile) - 1;
-            while (true) {
-                uint32_t s[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    s[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid]) : kFlagInc;
-                int used = 0;
-                bool done = false;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (done || used < j) break;
-                    if ((s[j] & ~kValMask) == 0) break;
-                    prefix += s[j] & kValMask;
-                    ++used;
-                    if (s[j] & kFlagInc) done = true;
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t idx = wbase + i * 32 + lane;
+            const bool ok = full || idx < valid;
+            const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : static_cast<uint32_t>(RADIX);
+            uint32_t r;
+            if (dbg & 2) {
+                r = ok ? atomicAdd(&wc[d], 1u) : 0u;
+            } else {
+                const uint32_t peers = RANK == 0 ? __match_any_sync(0xffffffffu, d) : peers_ballot<BITS>(d);
+                const int leader = __ffs(peers) - 1;
+                uint32_t before = 0;
+                if (lane == leader && ok) {
+                    before = wc[d];
+                    wc[d] = before + __popc(peers);
                 }
-                if (done) break;
-                t -= used;
+                r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers & lt);
+                __syncwarp();
+            }
+            if (i & 1) packed[i >> 1] |= r << 16;
+            else packed[i >> 1] = r;
+        }
+        __syncthreads();
+
+        // ---- per-digit: warp prefix, tile count, publish aggregate ---------
+        uint32_t tile_cnt = 0;
+        if (tid < RADIX) {
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) {
+                const uint32_t c = s_wcnt[w * RADIX + tid];
+                s_wcnt[w * RADIX + tid] = tile_cnt;
+                tile_cnt += c;
+            }
+            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
+                           (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
+        }
+        constexpr int SCAN_WARPS = (RADIX + 31) / 32;
+        uint32_t incl = 0;
+        if (warp < SCAN_WARPS) {
+            incl = warp_inclusive_scan(tile_cnt);
+            if (lane == 31) s_scan[warp] = incl;
+        }
+        __syncthreads();
+        if (tid < RADIX) {
+            uint32_t excl = incl - tile_cnt;
+#pragma unroll
+            for (int w = 0; w < SCAN_WARPS; ++w)
+                if (w < warp) excl += s_scan[w];
+            s_excl[tid] = excl;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
+        }
+        __syncthreads();
+
+        // ---- stage the tile in digit order (in place: keys are in registers)
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t idx = wbase + i * 32 + lane;
+            if (full || idx < valid) {
+                const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+                buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
         }
-        if (tile > 0)
-            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
-        s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
-    }
-    __syncthreads();
 
-    // ---- write digit runs (coalesced within each run) --------------------
-    if (full) {
-#pragma unroll 4
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint32_t i = j * THREADS + tid;
-            const uint32_t k = s_out[i];
-            dst[static_cast<Off>(s_delta[digit_of_key<BITS>(k, shift)] + i)] = k;
+        // ---- decoupled look-back, 4 predecessors per round trip -----------
+        if (tid < RADIX) {
+            uint32_t prefix = 0;
+            if (tile > 0 && !(dbg & 1)) {
+                int64_t t = static_cast<int64_t>(tile) - 1;
+                while (true) {
+                    uint32_t s[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        s[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                            : kFlagInc;
+                    int used = 0;
+                    bool done = false;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (done || used < j) break;
+                        if ((s[j] & ~kValMask) == 0) break;
+                        prefix += s[j] & kValMask;
+                        ++used;
+                        if (s[j] & kFlagInc) done = true;
+                    }
+                    if (done) break;
+                    t -= used;
+                }
+            }
+            if (tile > 0)
+                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
         }
-    } else {
-        for (uint32_t i = tid; i < valid; i += THREADS) {
-            const uint32_t k = s_out[i];
-            dst[static_cast<Off>(s_delta[digit_of_key<BITS>(k, shift)] + i)] = k;
+        __syncthreads();
+
+        // ---- write digit runs (coalesced within each run); reset counters --
+        for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
+        if (full) {
+#pragma unroll 4
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t i = j * THREADS + tid;
+                const uint32_t key = buf[i];
+                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
+            }
+        } else {
+            for (uint32_t i = tid; i < valid; i += THREADS) {
+                const uint32_t key = buf[i];
+                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
+            }
         }
     }
 }
@@ -408,16 +440,31 @@ inline int onesweep_dbg() {
     return d;
 }
 
-template <int BITS, int THREADS, int ITEMS, bool WIDE>
-int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
-                        int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+inline int onesweep_rank_mode() {
+    static int r = [] {
+        const char* e = getenv("BSG_OS_RANK");
+        return e ? atoi(e) : 0;
+    }();
+    return r;
+}
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
+int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
+                          int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
-    auto kern = onesweep_kernel<BITS, THREADS, ITEMS, WIDE>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    auto kern = onesweep_kernel<BITS, THREADS, ITEMS, WIDE, RANK>;
+    static int per_sm = 0;
+    if (per_sm == 0) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
-        attr_set = true;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, L::bytes);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int sms = kSmCountB200;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
     // status layout per chunk: [counter (32 words)] [tiles * RADIX]
@@ -428,13 +475,23 @@ int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, c
         const uint64_t off = c * kChunkKeys;
         const uint32_t len = static_cast<uint32_t>(std::min<uint64_t>(kChunkKeys, n - off));
         const uint32_t tiles = (len + L::TILE - 1) / L::TILE;
+        const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
         uint32_t* st = status + c * words_per_chunk;
         const uint64_t* base = base_for_pass + c * static_cast<uint64_t>(passes_stride) * RADIX;
-        kern<<<tiles, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0,
-                                                   dbg);
+        kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0, dbg);
         ++launches;
     }
     return launches;
+}
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
+int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
+                        int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+    if (onesweep_rank_mode() == 1)
+        return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 1>(plan, pass, n, shift, base_for_pass,
+                                                                    passes_stride, status, stream, use_tma);
+    return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 0>(plan, pass, n, shift, base_for_pass, passes_stride,
+                                                                status, stream, use_tma);
 }
 
 template <int BITS>
@@ -455,10 +512,7 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                           stream, use_tma);
     case 3:
-        return launch_onesweep_cfg<BITS, 512, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                         stream, use_tma);
-    case 4:
-        return launch_onesweep_cfg<BITS, 256, 32, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+        return launch_onesweep_cfg<BITS, 384, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     default:
         return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
