@@ -304,34 +304,47 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         uint32_t* wc = s_wcnt + warp * RADIX;
         uint32_t keys[ITEMS];
         uint32_t packed[ITEMS / 2];
+        auto rank_items = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+            uint32_t peers[ITEMS];
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const uint32_t idx = wbase + i * 32 + lane;
-            const bool ok = full || idx < valid;
-            keys[i] = ok ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
-        }
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t idx = wbase + i * 32 + lane;
+                if (FULL) {
+                    keys[i] = buf[idx];
+                } else {
+                    keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
+                }
+            }
+            // all match-any / ballot masks first: independent, latencies overlap
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const uint32_t idx = wbase + i * 32 + lane;
-            const bool ok = full || idx < valid;
-            const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : static_cast<uint32_t>(RADIX);
-            uint32_t r;
-            if (dbg & 2) {
-                r = ok ? atomicAdd(&wc[d], 1u) : 0u;
-            } else {
-                const uint32_t peers = RANK == 0 ? __match_any_sync(0xffffffffu, d) : peers_ballot<BITS>(d);
-                const int leader = __ffs(peers) - 1;
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t idx = wbase + i * 32 + lane;
+                const bool ok = FULL || idx < valid;
+                const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : static_cast<uint32_t>(RADIX);
+                if (dbg & 2) peers[i] = 1u << lane;
+                else peers[i] = RANK == 0 ? __match_any_sync(0xffffffffu, d) : peers_ballot<BITS>(d);
+            }
+            // then the per-warp running counts, item by item (input order)
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t idx = wbase + i * 32 + lane;
+                const bool ok = FULL || idx < valid;
+                const uint32_t d = digit_of_key<BITS>(keys[i], shift);
+                const int leader = __ffs(peers[i]) - 1;
                 uint32_t before = 0;
                 if (lane == leader && ok) {
                     before = wc[d];
-                    wc[d] = before + __popc(peers);
+                    wc[d] = before + __popc(peers[i]);
                 }
-                r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers & lt);
+                const uint32_t r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers[i] & lt);
                 __syncwarp();
+                if (i & 1) packed[i >> 1] |= r << 16;
+                else packed[i >> 1] = r;
             }
-            if (i & 1) packed[i >> 1] |= r << 16;
-            else packed[i >> 1] = r;
-        }
+        };
+        if (full) rank_items(std::true_type{});
+        else rank_items(std::false_type{});
         __syncthreads();
 
         // ---- per-digit: warp prefix, tile count, publish aggregate ---------
@@ -361,6 +374,34 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             s_excl[tid] = excl;
 #pragma unroll
             for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
+
+            // ---- decoupled look-back, 4 predecessors per round trip -------
+            uint32_t prefix = 0;
+            if (tile > 0 && !(dbg & 1)) {
+                int64_t t = static_cast<int64_t>(tile) - 1;
+                while (true) {
+                    uint32_t sv[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                             : kFlagInc;
+                    int used = 0;
+                    bool done = false;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (done || used < j) break;
+                        if ((sv[j] & ~kValMask) == 0) break;
+                        prefix += sv[j] & kValMask;
+                        ++used;
+                        if (sv[j] & kFlagInc) done = true;
+                    }
+                    if (done) break;
+                    t -= used;
+                }
+            }
+            if (tile > 0)
+                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - excl);
         }
         __syncthreads();
 
@@ -372,36 +413,6 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
                 buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
-        }
-
-        // ---- decoupled look-back, 4 predecessors per round trip -----------
-        if (tid < RADIX) {
-            uint32_t prefix = 0;
-            if (tile > 0 && !(dbg & 1)) {
-                int64_t t = static_cast<int64_t>(tile) - 1;
-                while (true) {
-                    uint32_t s[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        s[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
-                                            : kFlagInc;
-                    int used = 0;
-                    bool done = false;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (done || used < j) break;
-                        if ((s[j] & ~kValMask) == 0) break;
-                        prefix += s[j] & kValMask;
-                        ++used;
-                        if (s[j] & kFlagInc) done = true;
-                    }
-                    if (done) break;
-                    t -= used;
-                }
-            }
-            if (tile > 0)
-                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
-            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
         }
         __syncthreads();
 
