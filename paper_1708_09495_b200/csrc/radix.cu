@@ -375,33 +375,6 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 #pragma unroll
             for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
 
-            // ---- decoupled look-back, 4 predecessors per round trip -------
-            uint32_t prefix = 0;
-            if (tile > 0 && !(dbg & 1)) {
-                int64_t t = static_cast<int64_t>(tile) - 1;
-                while (true) {
-                    uint32_t sv[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
-                                             : kFlagInc;
-                    int used = 0;
-                    bool done = false;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (done || used < j) break;
-                        if ((sv[j] & ~kValMask) == 0) break;
-                        prefix += sv[j] & kValMask;
-                        ++used;
-                        if (sv[j] & kFlagInc) done = true;
-                    }
-                    if (done) break;
-                    t -= used;
-                }
-            }
-            if (tile > 0)
-                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
-            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - excl);
         }
         __syncthreads();
 
@@ -413,6 +386,43 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
                 buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
+        }
+
+        // ---- decoupled look-back: LB_WIN predecessors per round trip ------
+        // (each warp's load covers 32 consecutive digits of one predecessor:
+        // one coalesced 128-byte request per predecessor per warp)
+        if (tid < RADIX) {
+            constexpr int LB_WIN = 32;
+            uint32_t prefix = 0;
+            if (tile > 0 && !(dbg & 1)) {
+                int64_t t = static_cast<int64_t>(tile) - 1;
+                while (true) {
+                    uint32_t sv[LB_WIN];
+#pragma unroll
+                    for (int j = 0; j < LB_WIN; ++j)
+                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                             : kFlagInc;
+                    int used = 0;
+                    bool done = false, stop = false;
+#pragma unroll
+                    for (int j = 0; j < LB_WIN; ++j) {
+                        if (!stop) {
+                            if ((sv[j] & ~kValMask) == 0) {
+                                stop = true;
+                            } else {
+                                prefix += sv[j] & kValMask;
+                                ++used;
+                                if (sv[j] & kFlagInc) done = stop = true;
+                            }
+                        }
+                    }
+                    if (done) break;
+                    t -= used;
+                }
+            }
+            if (tile > 0)
+                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
         }
         __syncthreads();
 
