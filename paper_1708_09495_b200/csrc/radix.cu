@@ -196,15 +196,21 @@ __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
     }
 }
 
-// Lanes of the warp holding the same digit (bit-serial ballot multisplit).
-template <int BITS>
+// Lanes of the warp holding the same digit (bit-serial ballot multisplit):
+// per bit one predicate test, one VOTE, a predicated invert and an AND.
+template <int NBITS>
 __device__ __forceinline__ uint32_t peers_ballot(uint32_t d) {
     uint32_t peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < BITS + 1; ++b) { // BITS+1: the sentinel bin RADIX has bit BITS set
-        const bool bit = (d >> b) & 1u;
-        const uint32_t v = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? v : ~v;
+    for (int b = 0; b < NBITS; ++b) {
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, v;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 v, p, 0xffffffff;\n\t"
+            "@!p not.b32 v, v;\n\t"
+            "and.b32 %0, %0, v;\n\t}"
+            : "+r"(peers)
+            : "r"(d), "r"(1u << b));
     }
     return peers;
 }
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const bool ok = FULL || idx < valid;
                 const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : static_cast<uint32_t>(RADIX);
                 if (dbg & 2) peers[i] = 1u << lane;
-                else peers[i] = RANK == 0 ? __match_any_sync(0xffffffffu, d) : peers_ballot<BITS>(d);
+                else peers[i] = RANK == 1 ? __match_any_sync(0xffffffffu, d) : peers_ballot<FULL ? BITS : BITS + 1>(d);
             }
             // then the per-warp running counts, item by item (input order)
 #pragma unroll
@@ -508,6 +514,7 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+    // RANK 0 = ballot multisplit (default), 1 = match-any
     if (onesweep_rank_mode() == 1)
         return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 1>(plan, pass, n, shift, base_for_pass,
                                                                     passes_stride, status, stream, use_tma);
