@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- sorted uint32 keys per second on B200 (arXiv 1708.09495 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 (default): config 2 of BASELINE.json -- single-GPU LSD radix sort (SR4:
+radix 2^8, 4 stable count-sort rounds) of n = 2^28 uint32 keys drawn by the
+reference generator (generate_uniform_keys, core.hpp:93-99, seed
+derive_seed(1, 0), bench.hpp:86-88), device-resident; a step is one full sort.
+N > 1 (torchrun, one rank per GPU): the paper's PR4 parallel radix sort over
+NCCL, weak scaling with 2^28 keys per GPU (block-distributed; rank w's block
+is generate_uniform_keys(2^28, derive_seed(1, w))).
+
+--impl reference: the reference's own CPU implementation (its unmodified
+headers compiled into oracle/_ref/libbspref.so, else the oracle port) on
+this box's host cores: PR4 with p = all host threads, timed like
+bench::detail::run_once, on a bounded sample of the workload per step.
+Prints one JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "uint32 keys sorted/sec"
+UNIT = "keys/s"
+N_PER_GPU = 1 << 28
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(kernel: str, n: int):
+    """dram__bytes_read+write per launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        e = tr.get(kernel)
+        if e and int(e.get("n", -1)) == n:
+            return float(e["dram_bytes_per_launch"]), e.get("source")
+    except Exception:
+        pass
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline_sample(n_sample: int = 1 << 24, reps: int = 3):
+    """The reference's serial_radix_sort(., 256) on one host core (SR4, the
+    paper's baseline row) on a bounded sample, timed like run_once."""
+    from oracle.pyoracle import Oracle, maybe_reference
+    import paper_1708_09495_b200 as bsg
+
+    keys = bsg.generate_uniform_keys(n_sample, bsg.derive_seed(1, 0))
+    ref = maybe_reference()
+    impl, kind = (ref, "reference") if ref is not None else (Oracle(), "port")
+    ts = []
+    for _ in range(reps):
+        t, out = impl.time_serial_radix_sort(keys, 256)
+        ts.append(t)
+    assert np.array_equal(out, np.sort(keys))
+    t = statistics.median(ts)
+    return {"value": n_sample / t, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"serial_radix_sort(.,256) (SR4) of {n_sample} uniform keys on 1 host core, median of {reps}, "
+                      f"timed like bench.hpp run_once; host {os.cpu_count()} threads"}
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: PR4 with p = all host threads on a bounded sample."""
+    if rank != 0:
+        return
+    from oracle.pyoracle import Oracle, maybe_reference
+    import paper_1708_09495_b200 as bsg
+
+    n = args.ref_n
+    keys = bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0))
+    ref = maybe_reference()
+    p = os.cpu_count() or 1
+    if ref is not None:
+        kind = "reference"
+        step = lambda: ref.time_parallel_radix(keys, p, 256)  # noqa: E731
+        what = f"run_parallel_radix PR4 (r=256) with p={p} worker threads"
+    else:  # the oracle port is single-threaded
+        kind, p = "port", 1
+        orc = Oracle()
+        step = lambda: orc.time_serial_radix_sort(keys, 256)  # noqa: E731
+        what = "oracle port serial_radix_sort(.,256), 1 thread"
+    for _ in range(args.warmup):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t, out = step()
+        ts.append(t)
+    assert np.array_equal(out, np.sort(keys))
+    t = sum(ts) / len(ts)
+    value = n / t
+    sample = (f"{what} on {n} uniform keys per step (a bounded sample of the {N_PER_GPU * world}-key workload), "
+              f"mean of {args.steps} steps, timed like bench.hpp run_once")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": _config(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": p, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config(world: int):
+    if world == 1:
+        return {"workload": "config 2: single-GPU LSD radix sort (SR4: radix 2^8, 4 stable count-sort rounds) of "
+                            "n=2^28 uint32 keys, generate_uniform_keys(n, derive_seed(1,0))",
+                "n": N_PER_GPU, "radix": 256, "rounds": 4, "parallelism": "single GPU",
+                "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush needed"}
+    return {"workload": f"config 5 (weak-scaled): PR4 parallel radix sort over {world} GPUs, 2^28 uint32 keys per GPU "
+                        f"(n={N_PER_GPU * world}), per round digit count + NCCL all-gather of counts + NCCL "
+                        f"all-to-all-v of keys + rebuild",
+            "n": N_PER_GPU * world, "n_per_gpu": N_PER_GPU, "radix": 256, "rounds": 4, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2; no flush needed"}
+
+
+def run_single(args):
+    import torch
+    import paper_1708_09495_b200 as bsg
+    from paper_1708_09495_b200 import _lib
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n = args.n
+    keys = bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0))
+    d_in = torch.from_numpy(keys.view(np.int32)).to(dev)
+    d_out = torch.empty_like(d_in)
+    ctx = _lib.context(0)
+    ctx.reserve(n)
+    L = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step():
+        _lib.check(L.bsg_radix_sort_u32(ctx.handle, d_in.data_ptr(), d_out.data_ptr(), n, 8, _lib.MEM_DEVICE, sh))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.launches - l0
+    # correctness of what was timed (untimed)
+    ref_sorted = torch.sort(d_in.to(torch.int64) & 0xFFFFFFFF).values
+    ok = bool(torch.equal(d_out.to(torch.int64) & 0xFFFFFFFF, ref_sorted))
+    del ref_sorted
+
+    # dominant kernel, timed live on the launching stream
+    ctx.set_timing(True)
+    for _ in range(3):
+        step()
+    os_ms, os_cnt = ctx.kernel_time(_lib.K_ONESWEEP)
+    h_ms, h_cnt = ctx.kernel_time(_lib.K_HIST)
+    ctx.set_timing(False)
+    per_launch_s = os_ms / max(os_cnt, 1) / 1e3
+    alg_bytes = 8.0 * n  # one read + one write of every key per pass
+    achieved = alg_bytes / per_launch_s / 1e9
+    peak, peak_src = _peaks()
+    traffic, tsrc = _traffic("onesweep_pass", n)
+
+    # end to end through the public C ABI with pinned host buffers
+    h_in = torch.from_numpy(keys.view(np.int32)).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+
+    def e2e_step():
+        _lib.check(L.bsg_radix_sort_u32(ctx.handle, h_in.data_ptr(), h_out.data_ptr(), n, 8, _lib.MEM_HOST, sh))
+
+    e2e_step()
+    ke = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(ke):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / ke
+    ok_e2e = bool(np.array_equal(h_out.numpy().view(np.uint32)[:: max(1, n // 4096)],
+                                 d_out.cpu().numpy().view(np.uint32)[:: max(1, n // 4096)]))
+
+    line = {
+        "metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic (reference generator, seeded)", "config": _config(1),
+        "e2e": {"value": n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+                "ms_per_step": e2e_ms, "path": "bsg_radix_sort_u32(BSG_MEM_HOST) from pinned host memory"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "onesweep_kernel (one stable 8-bit pass)",
+                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": per_launch_s * 1e3,
+                     "peak_source": peak_src, "frac_of_8TBps_nominal": achieved / 8000.0,
+                     "traffic_source": tsrc},
+        "kernels_ms_per_sort": {"onesweep": os_ms / 3, "hist": h_ms / 3},
+        "clocks": clk.summary(),
+        "verified": ok and ok_e2e,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line), flush=True)
+
+
+def run_multi(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    import paper_1708_09495_b200 as bsg
+    from paper_1708_09495_b200 import _lib, distributed as D
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    n_local = args.n
+    n_total = n_local * world
+    keys = bsg.generate_uniform_keys(n_local, bsg.derive_seed(1, rank))
+    d_in = torch.from_numpy(keys.view(np.int32)).to(dev)
+    ctx = _lib.context(local_rank)
+
+    def step(events=None):
+        return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events)
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    l0 = ctx.launches
+    ev = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            out = step(ev)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    a2a_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms, a2a_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, a2a_max = t.tolist()
+    launches = ctx.launches - l0
+    # verification (untimed): local sortedness, boundaries, global checksum
+    o64 = out.to(torch.int64) & 0xFFFFFFFF
+    local_ok = bool((o64[1:] >= o64[:-1]).all()) if o64.numel() > 1 else True
+    ends = torch.tensor([o64[0].item(), o64[-1].item()], dtype=torch.int64, device=dev)
+    allends = [torch.empty_like(ends) for _ in range(world)]
+    dist.all_gather(allends, ends)
+    bounds_ok = all(allends[w][1].item() <= allends[w + 1][0].item() for w in range(world - 1))
+    cs = torch.tensor([(d_in.to(torch.int64) & 0xFFFFFFFF).sum().item(), o64.sum().item(), int(local_ok)],
+                      dtype=torch.float64, device=dev)
+    dist.all_reduce(cs)
+    ok = bounds_ok and cs[0].item() == cs[1].item() and int(cs[2].item()) == world
+
+    # e2e: each rank's block from pinned host memory, sort, result back
+    h_in = torch.from_numpy(keys.view(np.int32)).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+
+    def e2e_step():
+        blk = h_in.to(dev, non_blocking=True)
+        res = D.parallel_radix_sort(blk, n_total, radix=256)
+        h_out.copy_(res, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ke = max(1, min(args.steps, 3))
+    e0.record()
+    for _ in range(ke):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / ke], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = te.item()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n_total / (ms_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference generator, seeded per rank)",
+            "config": _config(world),
+            "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_total,
+                    "d2h_bytes_per_step": 4 * n_total, "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "nvlink_all_to_all_ms_per_step": a2a_max, "nvlink_share_of_step": a2a_max / ms_max,
+            "clocks": clk.summary(), "verified": ok,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
+    ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world == 1:
+        run_single(args)
+    else:
+        run_multi(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

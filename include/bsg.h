@@ -79,6 +79,20 @@ int bsg_ctx_destroy(bsg_ctx* ctx);
 /* Pre-sizes the workspace for sorts of up to n keys (optional). */
 int bsg_ctx_reserve(bsg_ctx* ctx, uint64_t n);
 
+/* Kernel-level timing on the launching stream (CUDA events around every
+ * launch of the given class while enabled).  Classes: */
+enum bsg_kernel_class {
+    BSG_K_ONESWEEP = 0, /* one stable digit pass (radix.cu K3) */
+    BSG_K_HIST = 1,     /* digit histograms (radix.cu K1) */
+    BSG_K_NETWORK = 2,  /* batched BTN/OET block network (netsort.cu) */
+    BSG_K_PR = 3,       /* parallel-radix plan/rebuild kernels (pr.cu) */
+    BSG_K_CLASSES = 4
+};
+int bsg_ctx_set_timing(bsg_ctx* ctx, int enable);
+/* Synchronises the recorded events and returns the summed duration (ms) and
+ * launch count of one class since timing was (re-)enabled. */
+int bsg_ctx_get_timing(bsg_ctx* ctx, int kernel_class, double* total_ms, uint64_t* launches);
+
 /* ---- host-side helpers (no GPU needed) -------------------------------- */
 /* core.hpp:93-99 generate_uniform_keys: mt19937_64(seed), low 32 bits. */
 int bsg_generate_uniform_u32(uint32_t* out, uint64_t n, uint64_t seed);
@@ -177,6 +191,12 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
  * owner_of division. */
 int bsg_pr_local_sort(bsg_ctx* ctx, const uint32_t* block, uint32_t* sorted, uint64_t len,
                       int round, int radix_log2, void* stream);
+
+/* Host (CPU) restatement of bsg_pr_plan over a host count matrix -- the
+ * same routing arithmetic, for hosts that plan on the CPU and for
+ * cross-checking the device planner.  No GPU needed. */
+int bsg_pr_plan_host(const uint64_t* counts, uint64_t n, int p, int me, int radix_log2,
+                     uint64_t* send_counts, uint64_t* recv_counts, int64_t* rebuild_delta);
 
 /* radix.hpp:295-333 gather_slices: rebuilds the block from the source-major
  * receive buffer (recv_len keys) by scattering each key to

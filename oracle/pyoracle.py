@@ -134,6 +134,18 @@ class Oracle:
         full = stages_limit < 0 or stages_limit >= S
         return (out[:k.size] if full else out[:L * p]), st.as_dict()
 
+    def time_serial_radix_sort(self, keys, radix: int):
+        import time
+
+        k = _u32(keys)
+        out = np.empty_like(k)
+        t0 = time.perf_counter()
+        rc = self.h.orc_serial_radix_sort(_p(k), k.size, radix, _p(out))
+        t = time.perf_counter() - t0
+        if rc:
+            raise RuntimeError("oracle serial_radix_sort failed")
+        return t, out
+
     def partition(self, n: int, p: int):
         return ([int(self.h.orc_part_offset_of(n, p, w)) for w in range(p)],
                 [int(self.h.orc_part_size_of(n, p, w)) for w in range(p)])
@@ -156,6 +168,12 @@ class Reference:
         h.ref_merge_split.argtypes = [vp, u64, vp, u64, vp, vp]
         h.ref_schedule.argtypes = [i, i, vp, vp, i, ctypes.POINTER(i)]
         h.ref_sort_instance.argtypes = [vp, u64, i, i, u64, vp]
+        h.ref_time_serial_radix_sort.argtypes = [vp, u64, u64, vp]
+        h.ref_time_serial_radix_sort.restype = ctypes.c_double
+        h.ref_time_parallel_radix.argtypes = [vp, u64, i, u64, vp]
+        h.ref_time_parallel_radix.restype = ctypes.c_double
+        h.ref_time_block_network.argtypes = [i, vp, u64, u64, i, vp]
+        h.ref_time_block_network.restype = ctypes.c_double
 
     def generate_uniform_keys(self, n: int, seed: int) -> np.ndarray:
         out = np.empty(n, dtype=np.uint32)
@@ -215,6 +233,32 @@ class Reference:
         if rc:
             raise ValueError("bad p")
         return partner[:S.value * p].reshape(S.value, p), keep[:S.value * p].reshape(S.value, p)
+
+    def time_serial_radix_sort(self, keys, radix: int):
+        """bench.hpp run_once timing of serial_radix_sort: (seconds, output)."""
+        k = _u32(keys)
+        out = np.empty_like(k)
+        t = self.h.ref_time_serial_radix_sort(_p(k), k.size, radix, _p(out))
+        if t < 0:
+            raise RuntimeError("reference serial_radix_sort failed")
+        return t, out
+
+    def time_parallel_radix(self, keys, p: int, radix: int):
+        """bench.hpp run_once timing of run_parallel_radix (threaded executor)."""
+        k = _u32(keys)
+        out = np.empty_like(k)
+        t = self.h.ref_time_parallel_radix(_p(k), k.size, p, radix, _p(out))
+        if t < 0:
+            raise RuntimeError("reference parallel radix failed")
+        return t, out
+
+    def time_block_network(self, network: int, arrays, p: int):
+        a = _u32(arrays)
+        out = np.empty_like(a)
+        t = self.h.ref_time_block_network(network, _p(a), a.shape[0], a.shape[1], p, _p(out))
+        if t < 0:
+            raise RuntimeError("reference block network failed")
+        return t, out
 
     def sort_instance(self, keys, processors: int, algorithm: int, radix: int) -> np.ndarray:
         k = _u32(keys)

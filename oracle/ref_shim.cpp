@@ -10,6 +10,7 @@
 // Only core/bsp/radix/netsort are included: bench.hpp and bspsort.hpp pull in
 // costmodel.hpp, which needs Boost.Multiprecision (absent), so the 5-way
 // dispatch of bspsort.hpp:15-25 is restated in ref_sort_instance below.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -132,6 +133,60 @@ int ref_schedule(int network, int p, int* partner, int* keep_low, int cap_stages
                 keep_low[s * p + i] = st[s][i].keep_low ? 1 : 0;
             }
     });
+}
+
+// Timed entry points mirroring bench::detail::run_once (bench.hpp:114-141):
+// the input copy / prepare stay outside the timer, only the sort is timed
+// (steady_clock, bench.hpp:92-97).  Return seconds, or a negative value on
+// error.
+double ref_time_serial_radix_sort(const std::uint32_t* in, std::uint64_t n, std::uint64_t radix,
+                                  std::uint32_t* out) {
+    try {
+        KeyArray work(in, in + n);
+        const auto t0 = std::chrono::steady_clock::now();
+        KeyArray r = radix::serial_radix_sort(std::move(work), radix);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::memcpy(out, r.data(), n * sizeof(std::uint32_t));
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (...) {
+        return -1.0;
+    }
+}
+
+double ref_time_parallel_radix(const std::uint32_t* in, std::uint64_t n, int p, std::uint64_t radix,
+                               std::uint32_t* out) {
+    try {
+        KeyArray keys(in, in + n);
+        auto prep = radix::prepare_parallel_radix(keys, p, radix);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto res = radix::run_parallel_radix(std::move(prep));
+        const auto t1 = std::chrono::steady_clock::now();
+        std::memcpy(out, res.output.data(), n * sizeof(std::uint32_t));
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (...) {
+        return -1.0;
+    }
+}
+
+double ref_time_block_network(int network, const std::uint32_t* in, std::uint64_t num_arrays, std::uint64_t len,
+                              int p, std::uint32_t* out) {
+    // The reference has no batched API: one run_block_network per array with
+    // the sequential executor, timed over the whole batch.
+    try {
+        double total = 0;
+        for (std::uint64_t a = 0; a < num_arrays; ++a) {
+            KeyArray keys(in + a * len, in + (a + 1) * len);
+            auto prep = network == 0 ? netsort::prepare_btn(keys, p) : netsort::prepare_oet(keys, p);
+            const auto t0 = std::chrono::steady_clock::now();
+            auto res = netsort::run_block_network(std::move(prep), true);
+            const auto t1 = std::chrono::steady_clock::now();
+            total += std::chrono::duration<double>(t1 - t0).count();
+            std::memcpy(out + a * len, res.output.data(), len * sizeof(std::uint32_t));
+        }
+        return total;
+    } catch (...) {
+        return -1.0;
+    }
 }
 
 // The 5-way dispatch of bspsort.hpp:15-25 (that header needs Boost).

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("BSG_LIB", os.path.join(_HERE, "libbsg.so"))
 BSG_OK, BSG_EINVAL, BSG_EPROTO, BSG_ECUDA, BSG_ENOMEM, BSG_ENCCL = range(6)
 MEM_HOST, MEM_DEVICE = 0, 1
 NET_BTN, NET_OET = 0, 1
+K_ONESWEEP, K_HIST, K_NETWORK, K_PR = range(4)
 
 
 class LibraryNotBuilt(RuntimeError):
@@ -60,6 +61,8 @@ SIGNATURES = {
     "bsg_ctx_create": (_i, [_i, ctypes.POINTER(_vp)]),
     "bsg_ctx_destroy": (_i, [_vp]),
     "bsg_ctx_reserve": (_i, [_vp, _u64]),
+    "bsg_ctx_set_timing": (_i, [_vp, _i]),
+    "bsg_ctx_get_timing": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "bsg_generate_uniform_u32": (_i, [_u32p, _u64, _u64]),
     "bsg_derive_seed": (ctypes.c_uint64, [_u64, ctypes.c_int32]),
     "bsg_checked_digit_bits": (_i, [_u64]),
@@ -79,6 +82,7 @@ SIGNATURES = {
     "bsg_pr_count_digits": (_i, [_vp, _u32p, _u64, _i, _i, _vp, _vp]),
     "bsg_pr_plan": (_i, [_vp, _vp, _u64, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "bsg_pr_local_sort": (_i, [_vp, _u32p, _u32p, _u64, _i, _i, _vp]),
+    "bsg_pr_plan_host": (_i, [_vp, _u64, _i, _i, _i, _vp, _vp, _vp]),
     "bsg_pr_rebuild": (_i, [_vp, _u32p, _u64, _vp, _i, _i, _i, _vp, _u32p, _vp]),
 }
 
@@ -137,6 +141,17 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().bsg_ctx_launch_count(self.handle))
+
+    def set_timing(self, enable: bool) -> None:
+        """Per-launch CUDA-event timing of kernel classes (K_ONESWEEP, ...)."""
+        check(lib().bsg_ctx_set_timing(self.handle, int(enable)), "bsg_ctx_set_timing")
+
+    def kernel_time(self, kernel_class: int):
+        """(total ms, launches) of one kernel class since timing was enabled."""
+        ms, cnt = ctypes.c_double(0), ctypes.c_uint64(0)
+        check(lib().bsg_ctx_get_timing(self.handle, kernel_class, ctypes.byref(ms), ctypes.byref(cnt)),
+              "bsg_ctx_get_timing")
+        return ms.value, cnt.value
 
     def reserve(self, n: int) -> None:
         check(lib().bsg_ctx_reserve(self.handle, n), "bsg_ctx_reserve")

@@ -14,6 +14,7 @@
 namespace bsg {
 
 static thread_local std::string g_last_error;
+thread_local KTimer* tl_timer = nullptr;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int status, const std::string& msg) {
@@ -51,7 +52,8 @@ namespace {
 struct CallGuard {
     std::lock_guard<std::mutex> lock;
     DeviceGuard dev;
-    explicit CallGuard(bsg_ctx* c) : lock(c->mu), dev(c->device) {}
+    explicit CallGuard(bsg_ctx* c) : lock(c->mu), dev(c->device) { tl_timer = &c->timer; }
+    ~CallGuard() { tl_timer = nullptr; }
 };
 
 int check_ctx(bsg_ctx* ctx) {
@@ -129,6 +131,34 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
             b->release();
     }
     delete ctx;
+    return BSG_OK;
+}
+
+int bsg_ctx_set_timing(bsg_ctx* ctx, int enable) {
+    if (int rc = check_ctx(ctx)) return rc;
+    CallGuard g(ctx);
+    ctx->timer.reset();
+    ctx->timer.enabled = enable != 0;
+    return BSG_OK;
+}
+
+int bsg_ctx_get_timing(bsg_ctx* ctx, int kernel_class, double* total_ms, uint64_t* launches) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (kernel_class < 0 || kernel_class >= BSG_K_CLASSES) return fail(BSG_EINVAL, "unknown kernel class");
+    CallGuard g(ctx);
+    double ms = 0;
+    uint64_t cnt = 0;
+    for (auto& r : ctx->timer.recs) {
+        if (r.cls != kernel_class) continue;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "timing event");
+        float f = 0;
+        cudaEventElapsedTime(&f, r.a, r.b);
+        ms += f;
+        ++cnt;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = cnt;
     return BSG_OK;
 }
 
@@ -333,8 +363,10 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
     if (p < 1 || me < 0 || me >= p) return fail(BSG_EINVAL, "pr_plan: worker index out of range");
     (void)round;
     CallGuard g(ctx);
+    cudaError_t e = ctx->pr_recv.ensure(static_cast<uint64_t>(p) * sizeof(uint64_t));
+    if (e != cudaSuccess) return cuda_fail(e, "pr_plan scratch");
     const int l = launch_pr_plan(counts, n, p, me, radix_log2, send_counts, recv_counts, rebuild_delta,
-                                 static_cast<cudaStream_t>(stream));
+                                 static_cast<cudaStream_t>(stream), ctx->pr_recv.as<uint64_t>());
     if (l < 0) return cuda_fail(cudaGetLastError(), "pr_plan launch");
     ctx->launches += static_cast<uint64_t>(l);
     return BSG_OK;

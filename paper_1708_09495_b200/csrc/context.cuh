@@ -11,6 +11,7 @@
 
 #include "../../include/bsg.h"
 #include "radix.cuh"
+#include "timer.cuh"
 
 namespace bsg {
 
@@ -46,6 +47,7 @@ struct bsg_ctx {
     int device = 0;
     std::mutex mu;
     uint64_t launches = 0;
+    bsg::KTimer timer;
     // radix workspace
     bsg::DevBuf tmp, status, hist, base, plan;
     // host-path staging and PR / network scratch

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "netsort.cuh"
+#include "timer.cuh"
 
 namespace bsg {
 
@@ -244,6 +245,7 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     }
     const uint64_t grid = (num_arrays + apc - 1) / apc;
     if (grid > 0x7FFFFFFFull) return -1;
+    TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
     block_network_kernel<<<static_cast<unsigned>(grid), kNetThreads, smem, stream>>>(in, out, num_arrays, len, p, L,
                                                                                    network, run_stages, full ? 1 : 0, apc);
     return cudaGetLastError() == cudaSuccess ? 1 : -1;

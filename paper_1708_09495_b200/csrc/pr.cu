@@ -25,6 +25,7 @@
 #include "context.cuh"
 #include "pr.cuh"
 #include "radix.cuh"
+#include "timer.cuh"
 
 namespace bsg {
 
@@ -239,6 +240,7 @@ int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, 
                    uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* split) {
     if (!split || p > kMaxP) return -1;
     const int radix = 1 << bits;
+    TimedScope ts(3 /*BSG_K_PR*/, stream);
     pr_plan1_kernel<<<p, kPlanThreads, sizeof(uint64_t) * p, stream>>>(counts, n, p, me, radix, send_counts,
                                                                         recv_counts, rebuild_delta, split);
     pr_plan2_kernel<<<p, kPlanThreads, 0, stream>>>(n, p, me, radix, recv_counts, split, rebuild_delta);
@@ -251,6 +253,7 @@ int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shi
     if (recv_len == 0) return 0;
     const uint64_t want = (recv_len + kRebuildThreads * 8 - 1) / (kRebuildThreads * 8);
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
+    TimedScope ts(3 /*BSG_K_PR*/, stream);
     pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(recv, recv_len, p, recv_counts, nullptr, (1u << bits) - 1u,
                                                            shift, 1 << bits, rebuild_delta, block);
     return cudaGetLastError() == cudaSuccess ? 1 : -1;
@@ -357,3 +360,54 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
 }
 
 } // namespace bsg
+
+// Host restatement of the routing plan (same arithmetic as pr_plan1/2).
+extern "C" int bsg_pr_plan_host(const uint64_t* counts, uint64_t n, int p, int me, int radix_log2,
+                                uint64_t* send_counts, uint64_t* recv_counts, int64_t* rebuild_delta) {
+    using namespace bsg;
+    if (p < 1 || me < 0 || me >= p) return fail(BSG_EINVAL, "pr_plan_host: worker index out of range");
+    if (radix_log2 != 1 && radix_log2 != 2 && radix_log2 != 4 && radix_log2 != 8 && radix_log2 != 16)
+        return fail(BSG_EINVAL, "radix must be a power of two whose bit width divides 32");
+    if (!counts || !send_counts || !recv_counts || !rebuild_delta) return fail(BSG_EINVAL, "null pointer");
+    const uint64_t r = uint64_t{1} << radix_log2;
+    auto ov = [](uint64_t a0, uint64_t a1, uint64_t b0, uint64_t b1) -> uint64_t {
+        const uint64_t lo = a0 > b0 ? a0 : b0, hi = a1 < b1 ? a1 : b1;
+        return hi > lo ? hi - lo : 0;
+    };
+    std::vector<uint64_t> starts(r), before(r, 0), split(p);
+    uint64_t run = 0;
+    for (uint64_t d = 0; d < r; ++d) {
+        starts[d] = run;
+        for (int u = 0; u < p; ++u) run += counts[static_cast<uint64_t>(u) * r + d];
+    }
+    const uint64_t lo_me = bsg_partition_offset_of(n, p, me), hi_me = lo_me + bsg_partition_size_of(n, p, me);
+    for (int w = 0; w < p; ++w) send_counts[w] = 0;
+    for (int v = 0; v < p; ++v) {
+        uint64_t local = 0, acc_recv = 0, acc_split = 0;
+        for (uint64_t d = 0; d < r; ++d) {
+            const uint64_t cv = counts[static_cast<uint64_t>(v) * r + d];
+            const uint64_t np = starts[d] + before[d];
+            acc_recv += ov(np, np + cv, lo_me, hi_me);
+            acc_split += ov(np, np + cv, 0, lo_me);
+            rebuild_delta[static_cast<uint64_t>(v) * r + d] = static_cast<int64_t>(np) - static_cast<int64_t>(local);
+            if (v == me && cv) {
+                const int w0 = bsg_partition_owner_of(n, p, np), w1 = bsg_partition_owner_of(n, p, np + cv - 1);
+                for (int w = w0; w <= w1; ++w) {
+                    const uint64_t lo = bsg_partition_offset_of(n, p, w);
+                    send_counts[w] += ov(np, np + cv, lo, lo + bsg_partition_size_of(n, p, w));
+                }
+            }
+            local += cv;
+        }
+        recv_counts[v] = acc_recv;
+        split[v] = acc_split;
+        for (uint64_t d = 0; d < r; ++d) before[d] += counts[static_cast<uint64_t>(v) * r + d];
+    }
+    uint64_t recv_off = 0;
+    for (int v = 0; v < p; ++v) {
+        const int64_t adj = static_cast<int64_t>(split[v]) - static_cast<int64_t>(recv_off) - static_cast<int64_t>(lo_me);
+        for (uint64_t d = 0; d < r; ++d) rebuild_delta[static_cast<uint64_t>(v) * r + d] += adj;
+        recv_off += recv_counts[v];
+    }
+    return BSG_OK;
+}

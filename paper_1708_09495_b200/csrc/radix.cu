@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "radix.cuh"
+#include "timer.cuh"
 
 namespace bsg {
 
@@ -505,6 +506,7 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
         const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
         uint32_t* st = status + c * words_per_chunk;
         const uint64_t* base = base_for_pass + c * static_cast<uint64_t>(passes_stride) * RADIX;
+        TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
         kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0, dbg);
         ++launches;
     }
@@ -527,24 +529,18 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
                          int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
     const bool wide = n > 0xFFFFFFFFull;
     if (wide)
-        return launch_onesweep_cfg<BITS, 512, 16, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+        return launch_onesweep_cfg<BITS, 1024, 16, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                         stream, use_tma);
     if constexpr (BITS != 8)
-        return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+        return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     switch (onesweep_cfg()) {
     case 1:
-        return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                         stream, use_tma);
-    case 2:
-        return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                          stream, use_tma);
-    case 3:
-        return launch_onesweep_cfg<BITS, 384, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                         stream, use_tma);
-    default:
         return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
+    default: // 1024 threads x 16 keys: 16384-key tiles, one CTA per SM
+        return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                          stream, use_tma);
     }
 }
 
@@ -576,6 +572,7 @@ int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const Radi
     for (uint64_t c = 0; c < chunks && n; ++c) {
         const uint64_t off = c * kChunkKeys;
         const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
+        TimedScope ts(1 /*BSG_K_HIST*/, stream);
         hist_kernel<8, PASSES><<<grid_for_stream(len / 8), kHistThreads, 0, stream>>>(in + off, len, 0,
                                                                                         ws.hist + c * PASSES * RADIX);
         ++launches;

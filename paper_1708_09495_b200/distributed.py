@@ -1,0 +1,121 @@
+"""Multi-GPU parallel radix sort (PR4 at r = 2^8, PR2 at r = 2^16): one
+process per GPU, the reference's BSP supersteps re-expressed over NCCL.
+
+Reference: run_parallel_radix (radix.hpp:371-414).  Per round, on every rank:
+
+  superstep 2k     count_digits(block) (radix.hpp:238-243)          -> kernel
+                   send the r counts to every worker (radix.hpp:386-388)
+                                                  -> NCCL all_gather (p x r)
+  superstep 2k+1   sort_and_scatter (radix.hpp:262-290): local stable pass
+                   -> kernel; the routing plan from the count matrix
+                   -> kernel; contiguous slices to their owners
+                                                  -> NCCL all_to_all_v
+  superstep 2k+2   gather_slices (radix.hpp:295-333) -> rebuild kernel
+
+The block a rank holds after round k is bit-identical to worker `rank`'s
+block in run_parallel_radix with plan.rounds = k.  The only host round trip
+per round is the 2p split sizes NCCL's all-to-all-v needs on the host.
+
+The step operations are injectable (``ops``) so the host orchestration can
+be exercised on CPU under gloo in tests; the product default is
+:class:`CudaStepOps`, which fails loudly without libbsg.so / a GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .radix import checked_digit_bits
+
+
+def partition_size_of(n: int, p: int, w: int) -> int:
+    return int(_lib.lib().bsg_partition_size_of(n, p, w))
+
+
+def partition_offset_of(n: int, p: int, w: int) -> int:
+    return int(_lib.lib().bsg_partition_offset_of(n, p, w))
+
+
+class CudaStepOps:
+    """The per-worker PR steps as sm_100a kernels (C ABI, device memory)."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.ctx = _lib.context(device.index or 0)
+        self.L = _lib.lib()
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def keys(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=torch.int32, device=self.device)
+
+    def count(self, block: torch.Tensor, rnd: int, bits: int) -> torch.Tensor:
+        counts = torch.empty(1 << bits, dtype=torch.int64, device=self.device)
+        _lib.check(self.L.bsg_pr_count_digits(self.ctx.handle, block.data_ptr(), block.numel(), rnd, bits,
+                                              counts.data_ptr(), self._stream()), "pr count_digits")
+        return counts
+
+    def local_sort(self, block: torch.Tensor, rnd: int, bits: int) -> torch.Tensor:
+        out = torch.empty_like(block)
+        _lib.check(self.L.bsg_pr_local_sort(self.ctx.handle, block.data_ptr(), out.data_ptr(), block.numel(), rnd,
+                                            bits, self._stream()), "pr local sort")
+        return out
+
+    def plan(self, counts_all: torch.Tensor, n: int, p: int, me: int, rnd: int, bits: int):
+        sr = torch.empty(2 * p, dtype=torch.int64, device=self.device)
+        delta = torch.empty(p << bits, dtype=torch.int64, device=self.device)
+        _lib.check(self.L.bsg_pr_plan(self.ctx.handle, counts_all.data_ptr(), n, p, me, rnd, bits, sr.data_ptr(),
+                                      sr[p:].data_ptr(), delta.data_ptr(), self._stream()), "pr plan")
+        host = sr.cpu().tolist()  # the one host round trip per round: split sizes
+        return host[:p], host[p:], sr[p:], delta
+
+    def rebuild(self, recv: torch.Tensor, recv_counts_dev: torch.Tensor, p: int, rnd: int, bits: int,
+                delta: torch.Tensor, out_len: int) -> torch.Tensor:
+        block = torch.empty(out_len, dtype=torch.int32, device=self.device)
+        _lib.check(self.L.bsg_pr_rebuild(self.ctx.handle, recv.data_ptr(), recv.numel(), recv_counts_dev.data_ptr(),
+                                         p, rnd, bits, delta.data_ptr(), block.data_ptr(), self._stream()),
+                   "pr rebuild")
+        return block
+
+
+def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rounds: Optional[int] = None,
+                        group=None, ops=None, a2a_events: Optional[list] = None) -> torch.Tensor:
+    """Sorts the globally block-distributed array (rank w holds the keys at
+    Partition(n_total, p).offset_of(w) .. +size_of(w), radix.hpp:207-229).
+    Returns this rank's block of the sorted array (int32 bit patterns of the
+    uint32 keys).  `rounds` < 32/lg r stops early (plan.rounds override).
+    If `a2a_events` is a list, CUDA event pairs around each all-to-all are
+    appended to it (NVLink share of the step)."""
+    bits = checked_digit_bits(radix)
+    p = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    if block.dtype == torch.uint32:
+        block = block.view(torch.int32)
+    if block.numel() != partition_size_of(n_total, p, me):
+        raise ValueError(f"rank {me} holds {block.numel()} keys; Partition({n_total}, {p}) expects "
+                         f"{partition_size_of(n_total, p, me)}")
+    if ops is None:
+        ops = CudaStepOps(block.device)
+    all_rounds = 32 // bits
+    rounds = all_rounds if rounds is None else max(0, min(int(rounds), all_rounds))
+    for rnd in range(rounds):
+        counts = ops.count(block, rnd, bits)
+        counts_all = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
+        dist.all_gather_into_tensor(counts_all, counts, group=group)
+        sorted_ = ops.local_sort(block, rnd, bits)
+        send, recv, recv_dev, delta = ops.plan(counts_all, n_total, p, me, rnd, bits)
+        recv_buf = ops.keys(sum(recv))
+        if a2a_events is not None and block.is_cuda:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        dist.all_to_all_single(recv_buf, sorted_, output_split_sizes=recv, input_split_sizes=send, group=group)
+        if a2a_events is not None and block.is_cuda:
+            e1.record()
+            a2a_events.append((e0, e1))
+        block = ops.rebuild(recv_buf, recv_dev, p, rnd, bits, delta, partition_size_of(n_total, p, me))
+    return block

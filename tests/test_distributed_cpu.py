@@ -1,0 +1,117 @@
+"""CPU: the multi-process PR orchestration (paper_1708_09495_b200.distributed)
+under gloo with world_size 2 and 3.  The per-worker steps are host stand-ins
+(oracle count/sort, the product's host planner bsg_pr_plan_host, a numpy
+rebuild) so the collective sequence, split sizes and buffer handling of the
+product orchestration are exercised without a GPU.  Every rank's block after
+k rounds must equal worker `rank`'s block of the reference's
+run_parallel_radix with plan.rounds = k."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class HostOps:
+    def __init__(self):
+        from oracle.pyoracle import Oracle
+        import paper_1708_09495_b200 as bsg
+
+        self.orc = Oracle()
+        self.L = bsg._lib.lib()
+
+    def keys(self, n):
+        return torch.empty(n, dtype=torch.int32)
+
+    def count(self, block, rnd, bits):
+        k = block.numpy().view(np.uint32)
+        d = (k.astype(np.uint64) >> np.uint64(rnd * bits)) & np.uint64((1 << bits) - 1)
+        return torch.from_numpy(np.bincount(d.astype(np.int64), minlength=1 << bits).astype(np.int64))
+
+    def local_sort(self, block, rnd, bits):
+        out = self.orc.count_sort_round(block.numpy().view(np.uint32), rnd, 1 << bits)
+        return torch.from_numpy(out.view(np.int32).copy())
+
+    def plan(self, counts_all, n, p, me, rnd, bits):
+        c = np.ascontiguousarray(counts_all.numpy().astype(np.uint64))
+        send = np.zeros(p, np.uint64)
+        recv = np.zeros(p, np.uint64)
+        delta = np.zeros(p << bits, np.int64)
+        rc = self.L.bsg_pr_plan_host(c.ctypes.data, n, p, me, bits, send.ctypes.data, recv.ctypes.data,
+                                     delta.ctypes.data)
+        assert rc == 0
+        return [int(x) for x in send], [int(x) for x in recv], recv, delta
+
+    def rebuild(self, recv, recv_counts, p, rnd, bits, delta, out_len):
+        k = recv.numpy().view(np.uint32)
+        src = np.repeat(np.arange(p), recv_counts.astype(np.int64))
+        d = ((k.astype(np.uint64) >> np.uint64(rnd * bits)) & np.uint64((1 << bits) - 1)).astype(np.int64)
+        pos = delta[src * (1 << bits) + d] + np.arange(k.size)
+        out = np.empty(out_len, np.uint32)
+        out[pos] = k
+        assert np.array_equal(np.sort(pos), np.arange(out_len))
+        return torch.from_numpy(out.view(np.int32))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cases, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1708_09495_b200 import distributed as D
+
+        ops = HostOps()
+        res = []
+        for keys, radix, rounds in cases:
+            n = keys.size
+            off = D.partition_offset_of(n, world, rank)
+            sz = D.partition_size_of(n, world, rank)
+            blk = torch.from_numpy(keys[off:off + sz].view(np.int32).copy())
+            out = D.parallel_radix_sort(blk, n, radix=radix, rounds=rounds, ops=ops)
+            res.append(out.numpy().view(np.uint32).copy())
+        q.put((rank, res, None))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_pr_matches_reference_rounds(world, orc):
+    keys_u = orc.generate_uniform_keys(4001, 17)
+    keys_d = orc.generate_uniform_keys(3000, 5) % 31
+    cases = []
+    for keys in (keys_u, keys_d):
+        for radix in (256, 65536):
+            for rounds in sorted({0, 1, 32 // (radix.bit_length() - 1)}):
+                cases.append((keys, radix, rounds))
+    cases.append((np.array([5, 1, 4], np.uint32), 256, 4))  # fewer keys than... p=3 edge
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(world):
+        rank, res, err = q.get(timeout=300)
+        assert err is None, err
+        out[rank] = res
+    for pr in procs:
+        pr.join(timeout=60)
+    for ci, (keys, radix, rounds) in enumerate(cases):
+        exp, _ = orc.parallel_radix(keys, world, radix, rounds)
+        got = np.concatenate([out[r][ci] for r in range(world)])
+        np.testing.assert_array_equal(got, exp, err_msg=f"case {ci} radix={radix} rounds={rounds}")

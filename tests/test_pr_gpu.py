@@ -59,3 +59,52 @@ def test_superstep_counts(cuda, bsg, orc):
     keys = orc.generate_uniform_keys(5000, 21)
     assert pr(bsg, keys, 4, 256).stats["supersteps"] == 9
     assert pr(bsg, keys, 4, 65536).stats["supersteps"] == 5
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+def test_device_plan_equals_host_plan(cuda, bsg, orc, bits, p):
+    torch = cuda
+    rng = np.random.default_rng(bits * 100 + p)
+    r = 1 << bits
+    counts = rng.integers(0, 50, size=p * r).astype(np.uint64)
+    counts[rng.integers(0, p * r, size=5)] = 0
+    n = int(counts.sum())
+    L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    dc = torch.from_numpy(counts.view(np.int64)).cuda()
+    for me in range(p):
+        sr = torch.empty(2 * p, dtype=torch.int64, device="cuda")
+        delta = torch.empty(p * r, dtype=torch.int64, device="cuda")
+        assert L.bsg_pr_plan(ctx.handle, dc.data_ptr(), n, p, me, 0, bits, sr.data_ptr(), sr[p:].data_ptr(),
+                             delta.data_ptr(), torch.cuda.current_stream().cuda_stream) == 0
+        hs, hr, hd = np.zeros(p, np.uint64), np.zeros(p, np.uint64), np.zeros(p * r, np.int64)
+        assert L.bsg_pr_plan_host(counts.ctypes.data, n, p, me, bits, hs.ctypes.data, hr.ctypes.data,
+                                  hd.ctypes.data) == 0
+        torch.cuda.synchronize()
+        assert sr[:p].cpu().numpy().astype(np.uint64).tolist() == hs.tolist()
+        assert sr[p:].cpu().numpy().astype(np.uint64).tolist() == hr.tolist()
+        np.testing.assert_array_equal(delta.cpu().numpy(), hd)
+
+
+def test_distributed_nccl_world1(cuda, bsg, orc):
+    """The NCCL orchestration with one rank on the GPU (all-gather and
+    all-to-all-v degenerate to copies) equals the serial sort, per round."""
+    torch = cuda
+    import os
+    import torch.distributed as dist
+    from paper_1708_09495_b200 import distributed as D
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        keys = orc.generate_uniform_keys(100003, 9)
+        for radix in (256, 65536):
+            for rounds in (1, None):
+                blk = torch.from_numpy(keys.view(np.int32)).cuda()
+                out = D.parallel_radix_sort(blk, keys.size, radix=radix, rounds=rounds)
+                exp, _ = orc.parallel_radix(keys, 1, radix, -1 if rounds is None else rounds)
+                np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), exp)
+    finally:
+        dist.destroy_process_group()
