@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
                 if (FULL) {
-                    keys[i] = buf[idx];
+                    keys[i] = idx < vec ? buf[idx] : __ldg(src + tile_start + idx);
                 } else {
                     keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
                 }

@@ -139,3 +139,24 @@ def test_full_size_2_28_properties(cuda, bsg):
     assert int((o64 * o64 % 1000003).sum()) == int((i64 * i64 % 1000003).sum())
     ref_sorted = torch.sort(i64).values
     assert bool(torch.equal(ref_sorted, o64))
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3, 5])
+def test_unaligned_device_pointers(cuda, bsg, orc, offset):
+    """Misaligned sub-array pointers take the non-TMA load path."""
+    torch = cuda
+    n = 3 * 16384 + 777
+    keys = orc.generate_uniform_keys(n + offset, 99)
+    t = torch.from_numpy(keys.view(np.int32)).cuda()
+    sub = t[offset:]
+    out = torch.empty(n + offset, dtype=torch.int32, device="cuda")[offset:]
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    for rnd in range(4):
+        assert L.bsg_count_sort_round_u32(ctx.handle, sub.data_ptr(), out.data_ptr(), n, rnd, 8, 1, st) == 0
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), orc.count_sort_round(keys[offset:], rnd, 256))
+    assert L.bsg_radix_sort_u32(ctx.handle, sub.data_ptr(), out.data_ptr(), n, 8, 1, st) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys[offset:]))
