@@ -341,8 +341,12 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const int leader = __ffs(peers[i]) - 1;
                 uint32_t before = 0;
                 if (lane == leader && ok) {
-                    before = wc[d];
-                    wc[d] = before + __popc(peers[i]);
+                    if (dbg & 4) {
+                        before = atomicAdd(&wc[d], static_cast<uint32_t>(__popc(peers[i])));
+                    } else {
+                        before = wc[d];
+                        wc[d] = before + __popc(peers[i]);
+                    }
                 }
                 const uint32_t r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers[i] & lt);
                 __syncwarp();
