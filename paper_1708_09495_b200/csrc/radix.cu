@@ -330,7 +330,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const bool ok = FULL || idx < valid;
                 const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : static_cast<uint32_t>(RADIX);
                 if (dbg & 2) peers[i] = 1u << lane;
-                else peers[i] = RANK == 1 ? __match_any_sync(0xffffffffu, d) : peers_ballot<FULL ? BITS : BITS + 1>(d);
+                else if (RANK == 1 || (RANK == 2 && (i & 3) == 0) || (RANK == 3 && (i & 1) == 0))
+                    peers[i] = __match_any_sync(0xffffffffu, d);
+                else
+                    peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d);
             }
             // then the per-warp running counts, item by item (input order)
 #pragma unroll
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const uint32_t idx = wbase + i * 32 + lane;
                 const bool ok = FULL || idx < valid;
                 const uint32_t d = digit_of_key<BITS>(keys[i], shift);
-                const int leader = __ffs(peers[i]) - 1;
+                const int leader = 31 - __clz(peers[i]); // highest peer lane: one FLO
                 uint32_t before = 0;
                 if (lane == leader && ok) {
                     if (dbg & 4) {
@@ -520,10 +523,22 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
-    // RANK 0 = ballot multisplit (default), 1 = match-any
-    if (onesweep_rank_mode() == 1)
-        return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 1>(plan, pass, n, shift, base_for_pass,
-                                                                    passes_stride, status, stream, use_tma);
+    // RANK 0 = ballot multisplit (default), 1 = match-any, 2/3 = match-any on 1/4 / 1/2 of the items
+    if constexpr (BITS == 8) {
+        switch (onesweep_rank_mode()) {
+        case 1:
+            return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 1>(plan, pass, n, shift, base_for_pass,
+                                                                        passes_stride, status, stream, use_tma);
+        case 2:
+            return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 2>(plan, pass, n, shift, base_for_pass,
+                                                                        passes_stride, status, stream, use_tma);
+        case 3:
+            return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 3>(plan, pass, n, shift, base_for_pass,
+                                                                        passes_stride, status, stream, use_tma);
+        default:
+            break;
+        }
+    }
     return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 0>(plan, pass, n, shift, base_for_pass, passes_stride,
                                                                 status, stream, use_tma);
 }
