@@ -38,64 +38,81 @@ namespace {
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
-constexpr int kHistThreads = 256;
 constexpr int kScanThreads = 256;
 
 // ---------------------------------------------------------------------------
 // K1: digit histograms.  NDIG digits of BITS bits starting at first_shift.
+// Every lane owns a private copy of every counter (counter c of lane l lives
+// at word c*32 + l, i.e. in bank l), so a warp's 32 shared-memory atomics
+// never conflict -- for uniform and for all-equal keys alike.  One persistent
+// CTA per SM streams 128-bit loads; copies are reduced once at the end.
 // ---------------------------------------------------------------------------
+constexpr int kHist2Threads = 1024;
+
 template <int BITS, int NDIG>
-__global__ void __launch_bounds__(kHistThreads)
-    hist_kernel(const uint32_t* __restrict__ in, uint64_t n, int first_shift,
-                uint32_t* __restrict__ hist) {
+__global__ void __launch_bounds__(kHist2Threads)
+    hist_kernel(const uint32_t* __restrict__ in, uint64_t n, int first_shift, uint32_t* __restrict__ hist) {
     constexpr int RADIX = 1 << BITS;
     constexpr uint32_t MASK = RADIX - 1;
-    __shared__ uint32_t sh[NDIG * RADIX];
-    for (int i = threadIdx.x; i < NDIG * RADIX; i += kHistThreads) sh[i] = 0;
+    constexpr int COUNTERS = NDIG * RADIX;
+    extern __shared__ uint32_t sh[]; // COUNTERS * 32
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < COUNTERS * 32; i += kHist2Threads) sh[i] = 0;
     __syncthreads();
-
+    uint32_t* mine = sh + lane;
+    auto count_key = [&](uint32_t key) {
+#pragma unroll
+        for (int j = 0; j < NDIG; ++j) {
+            const uint32_t d = (key >> (first_shift + j * BITS)) & MASK;
+            atomicAdd(mine + (j * RADIX + d) * 32, 1u);
+        }
+    };
     const uint64_t mis = (reinterpret_cast<uintptr_t>(in) >> 2) & 3;
     uint64_t head = mis ? 4 - mis : 0;
     if (head > n) head = n;
     const uint4* body = reinterpret_cast<const uint4*>(in + head);
-    const uint64_t groups = ((n - head) / 4) / 2; // 8-key groups
-
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kHistThreads;
-    for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * kHistThreads + threadIdx.x; g < groups;
-         g += stride) {
-        const uint4 a = ldg_stream_v4(body + 2 * g);
-        const uint4 b = ldg_stream_v4(body + 2 * g + 1);
-        const uint32_t k[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int j = 0; j < NDIG; ++j) {
-            const int s = first_shift + j * BITS;
-            uint32_t cur = (k[0] >> s) & MASK, cnt = 1;
-#pragma unroll
-            for (int t = 1; t < 8; ++t) {
-                const uint32_t d = (k[t] >> s) & MASK;
-                if (d == cur) {
-                    ++cnt;
-                } else {
-                    atomicAdd(&sh[j * RADIX + cur], cnt);
-                    cur = d;
-                    cnt = 1;
-                }
-            }
-            atomicAdd(&sh[j * RADIX + cur], cnt);
-        }
+    const uint64_t nvec = (n - head) / 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kHist2Threads;
+    uint64_t v = static_cast<uint64_t>(blockIdx.x) * kHist2Threads + threadIdx.x;
+    for (; v + stride < nvec; v += 2 * stride) { // two independent 16-byte loads in flight
+        const uint4 a = ldg_stream_v4(body + v);
+        const uint4 b = ldg_stream_v4(body + v + stride);
+        count_key(a.x); count_key(a.y); count_key(a.z); count_key(a.w);
+        count_key(b.x); count_key(b.y); count_key(b.z); count_key(b.w);
+    }
+    for (; v < nvec; v += stride) {
+        const uint4 a = ldg_stream_v4(body + v);
+        count_key(a.x); count_key(a.y); count_key(a.z); count_key(a.w);
     }
     if (blockIdx.x == 0) {
-        auto count_one = [&](uint32_t key) {
-#pragma unroll
-            for (int j = 0; j < NDIG; ++j)
-                atomicAdd(&sh[j * RADIX + ((key >> (first_shift + j * BITS)) & MASK)], 1u);
-        };
-        for (uint64_t i = threadIdx.x; i < head; i += kHistThreads) count_one(in[i]);
-        for (uint64_t i = head + groups * 8 + threadIdx.x; i < n; i += kHistThreads) count_one(in[i]);
+        for (uint64_t i = threadIdx.x; i < head; i += kHist2Threads) count_key(in[i]);
+        for (uint64_t i = head + nvec * 4 + threadIdx.x; i < n; i += kHist2Threads) count_key(in[i]);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < NDIG * RADIX; i += kHistThreads)
-        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+    for (int c = threadIdx.x; c < COUNTERS; c += kHist2Threads) {
+        uint32_t s = 0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) s += sh[c * 32 + ((l + c) & 31)]; // rotate: conflict-free
+        if (s) atomicAdd(&hist[c], s);
+    }
+}
+
+template <int BITS, int NDIG>
+void launch_hist(const uint32_t* in, uint64_t n, int first_shift, uint32_t* hist, cudaStream_t stream) {
+    constexpr size_t smem = sizeof(uint32_t) * NDIG * (1 << BITS) * 32;
+    static int per_sm = 0;
+    auto kern = hist_kernel<BITS, NDIG>;
+    if (per_sm == 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHist2Threads, smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int sms = kSmCountB200, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (n / 4 + kHist2Threads - 1) / kHist2Threads;
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, sms * per_sm)));
+    kern<<<grid, kHist2Threads, smem, stream>>>(in, n, first_shift, hist);
 }
 
 // ---------------------------------------------------------------------------
@@ -572,10 +589,6 @@ uint64_t status_words_for(uint64_t n) {
     return chunks * per_chunk;
 }
 
-inline int grid_for_stream(uint64_t items_per_thread_groups) {
-    const uint64_t want = (items_per_thread_groups + kHistThreads - 1) / kHistThreads;
-    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
-}
 
 } // namespace
 
@@ -592,8 +605,7 @@ int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const Radi
         const uint64_t off = c * kChunkKeys;
         const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
         TimedScope ts(1 /*BSG_K_HIST*/, stream);
-        hist_kernel<8, PASSES><<<grid_for_stream(len / 8), kHistThreads, 0, stream>>>(in + off, len, 0,
-                                                                                        ws.hist + c * PASSES * RADIX);
+        launch_hist<8, PASSES>(in + off, len, 0, ws.hist + c * PASSES * RADIX, stream);
         ++launches;
     }
     scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), PASSES, RADIX, n, ws.base,
@@ -622,12 +634,11 @@ int launch_count_pass(const uint32_t* in, uint32_t* out, uint64_t n, int bits, i
         const uint64_t off = c * kChunkKeys;
         const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
         uint32_t* h = ws.hist + c * radix;
-        const int grid = grid_for_stream(len / 8);
         switch (bits) {
-        case 1: hist_kernel<1, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
-        case 2: hist_kernel<2, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
-        case 4: hist_kernel<4, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
-        case 8: hist_kernel<8, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 1: launch_hist<1, 1>(in + off, len, shift, h, stream); break;
+        case 2: launch_hist<2, 1>(in + off, len, shift, h, stream); break;
+        case 4: launch_hist<4, 1>(in + off, len, shift, h, stream); break;
+        case 8: launch_hist<8, 1>(in + off, len, shift, h, stream); break;
         default: return -1;
         }
         ++launches;
@@ -682,12 +693,11 @@ int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uin
         const uint64_t off = c * kChunkKeys;
         const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
         uint32_t* h = scratch32 + c * radix;
-        const int grid = grid_for_stream(len / 8);
         switch (bits) {
-        case 1: hist_kernel<1, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
-        case 2: hist_kernel<2, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
-        case 4: hist_kernel<4, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
-        case 8: hist_kernel<8, 1><<<grid, kHistThreads, 0, stream>>>(in + off, len, shift, h); break;
+        case 1: launch_hist<1, 1>(in + off, len, shift, h, stream); break;
+        case 2: launch_hist<2, 1>(in + off, len, shift, h, stream); break;
+        case 4: launch_hist<4, 1>(in + off, len, shift, h, stream); break;
+        case 8: launch_hist<8, 1>(in + off, len, shift, h, stream); break;
         default: return -1;
         }
         ++launches;
