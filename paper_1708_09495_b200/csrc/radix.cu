@@ -218,18 +218,23 @@ __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
 // per bit one predicate test, one VOTE, a predicated invert and an AND.
 template <int NBITS>
 __device__ __forceinline__ uint32_t peers_ballot(uint32_t d) {
-    uint32_t peers = 0xffffffffu;
+    uint32_t m[NBITS];
 #pragma unroll
     for (int b = 0; b < NBITS; ++b) {
-        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, v;\n\t"
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
             "and.b32 t, %1, %2;\n\t"
             "setp.ne.u32 p, t, 0;\n\t"
-            "vote.sync.ballot.b32 v, p, 0xffffffff;\n\t"
-            "@!p not.b32 v, v;\n\t"
-            "and.b32 %0, %0, v;\n\t}"
-            : "+r"(peers)
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "@!p not.b32 %0, %0;\n\t}"
+            : "=r"(m[b])
             : "r"(d), "r"(1u << b));
     }
+    // AND-reduce the masks with 3-input LOP3s
+    uint32_t peers = m[0];
+    int b = 1;
+#pragma unroll
+    for (; b + 1 < NBITS; b += 2) asm("lop3.b32 %0, %0, %1, %2, 0x80;" : "+r"(peers) : "r"(m[b]), "r"(m[b + 1]));
+    if (b < NBITS) peers &= m[b];
     return peers;
 }
 
@@ -352,25 +357,20 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 else
                     peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d);
             }
-            // then the per-warp running counts, item by item (input order)
+            // then the per-warp running counts, item by item (input order):
+            // every peer reads the same counter (a broadcast), the highest
+            // peer alone stores the advanced count.
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
                 const bool ok = FULL || idx < valid;
-                const uint32_t d = digit_of_key<BITS>(keys[i], shift);
-                const int leader = 31 - __clz(peers[i]); // highest peer lane: one FLO
-                uint32_t before = 0;
-                if (lane == leader && ok) {
-                    if (dbg & 4) {
-                        before = atomicAdd(&wc[d], static_cast<uint32_t>(__popc(peers[i])));
-                    } else {
-                        before = wc[d];
-                        wc[d] = before + __popc(peers[i]);
-                    }
-                }
-                const uint32_t r = __shfl_sync(0xffffffffu, before, leader) + __popc(peers[i] & lt);
+                const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : 0u;
+                const uint32_t before = ok ? wc[d] : 0u;
+                const bool leader = (31 - __clz(peers[i])) == lane;
+                if (leader && ok) wc[d] = before + __popc(peers[i]);
+                const uint32_t r = before + __popc(peers[i] & lt);
                 __syncwarp();
-                if (i & 1) packed[i >> 1] |= r << 16;
+                if (i & 1) packed[i >> 1] = __byte_perm(packed[i >> 1], r, 0x5410);
                 else packed[i >> 1] = r;
             }
         };
