@@ -570,7 +570,12 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
     if constexpr (BITS != 8)
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
-    switch (onesweep_cfg()) {
+    int cfg = onesweep_cfg();
+    if (cfg == 0) cfg = n <= (uint64_t{1} << 21) ? 3 : (n <= (uint64_t{1} << 24) ? 1 : 2);
+    switch (cfg) {
+    case 3: // 256 x 16: 4096-key tiles so small inputs still fill 148 SMs
+        return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
     case 1:
         return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
