@@ -46,8 +46,41 @@ __device__ __forceinline__ void sort8(uint32_t (&v)[kNK]) {
     }
 }
 
+// Shared-memory index with one pad word per 32: the stride-4/stride-8 access
+// patterns of merge-path chunks (8 outputs per lane) become conflict-free.
+__device__ __forceinline__ uint32_t pad(uint32_t i) { return i + (i >> 5); }
+
 // Writes outputs [diag, diag+cnt) of merge(A, B) (ties taken from A first,
-// netsort.hpp:39) to dst[0..cnt).
+// netsort.hpp:39) into smem at logical indices dst0 .. dst0+cnt-1.  A and B
+// are logical index ranges [a0, a0+na), [b0, b0+nb) of the padded buffer S.
+__device__ __forceinline__ void merge_chunk_s(const uint32_t* S, uint32_t a0, int na, uint32_t b0, int nb, int diag,
+                                              int cnt, uint32_t* D, uint32_t dst0) {
+    int lo = max(0, diag - nb), hi = min(diag, na);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (S[pad(a0 + mid)] <= S[pad(b0 + diag - 1 - mid)]) lo = mid + 1;
+        else hi = mid;
+    }
+    int i = lo, j = diag - lo;
+    uint32_t av = i < na ? S[pad(a0 + i)] : 0u, bv = j < nb ? S[pad(b0 + j)] : 0u;
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) {
+        if (k < cnt) {
+            const bool take_a = i < na && (j >= nb || av <= bv);
+            if (take_a) {
+                D[pad(dst0 + k)] = av;
+                ++i;
+                av = i < na ? S[pad(a0 + i)] : 0u;
+            } else {
+                D[pad(dst0 + k)] = bv;
+                ++j;
+                bv = j < nb ? S[pad(b0 + j)] : 0u;
+            }
+        }
+    }
+}
+
+// Global-memory variant for the standalone merge_split.
 __device__ __forceinline__ void merge_chunk(const uint32_t* A, int na, const uint32_t* B, int nb, int diag, int cnt,
                                             uint32_t* dst) {
     int lo = max(0, diag - nb), hi = min(diag, na);
@@ -110,8 +143,9 @@ __global__ void __launch_bounds__(kNetThreads)
                          uint32_t len, int p, uint32_t L, int network, int run_stages, int full, int apc) {
     extern __shared__ __align__(16) uint32_t net_smem[];
     const uint32_t P = L * static_cast<uint32_t>(p);
+    const uint32_t padded = pad(static_cast<uint32_t>(apc) * P) + 1;
     uint32_t* bufA = net_smem;
-    uint32_t* bufB = net_smem + static_cast<uint32_t>(apc) * P;
+    uint32_t* bufB = net_smem + padded;
     const uint64_t array0 = static_cast<uint64_t>(blockIdx.x) * apc;
     const int na = static_cast<int>(min(static_cast<uint64_t>(apc), num_arrays - array0));
     const int tid = threadIdx.x;
@@ -120,7 +154,7 @@ __global__ void __launch_bounds__(kNetThreads)
     const uint32_t tot = static_cast<uint32_t>(na) * P;
     for (uint32_t idx = tid; idx < tot; idx += kNetThreads) {
         const uint32_t a = idx / P, e = idx - a * P;
-        bufA[idx] = e < len ? __ldg(in + (array0 + a) * len + e) : kPad;
+        bufA[pad(idx)] = e < len ? __ldg(in + (array0 + a) * len + e) : kPad;
     }
     __syncthreads();
 
@@ -131,16 +165,16 @@ __global__ void __launch_bounds__(kNetThreads)
     for (uint32_t it = tid; it < items; it += kNetThreads) {
         const uint32_t a = it / (p * cb), rem = it - a * p * cb;
         const uint32_t w = rem / cb, c = rem - w * cb;
-        uint32_t* blk = bufA + a * P + w * L;
+        const uint32_t b0 = a * P + w * L;
         const uint32_t ob = c * kNK;
         const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
         uint32_t v[kNK];
 #pragma unroll
-        for (int k = 0; k < kNK; ++k) v[k] = k < cnt ? blk[ob + k] : kPad;
+        for (int k = 0; k < kNK; ++k) v[k] = k < cnt ? bufA[pad(b0 + ob + k)] : kPad;
         sort8(v);
 #pragma unroll
         for (int k = 0; k < kNK; ++k)
-            if (k < cnt) blk[ob + k] = v[k];
+            if (k < cnt) bufA[pad(b0 + ob + k)] = v[k];
     }
     __syncthreads();
     // (b) bottom-up merge-path merges inside each block
@@ -155,8 +189,8 @@ __global__ void __launch_bounds__(kNetThreads)
             const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
             const uint32_t ps = (ob / (2 * width)) * (2 * width);
             const uint32_t a_end = min(ps + width, L), b_end = min(ps + 2 * width, L);
-            merge_chunk(src + bs + ps, static_cast<int>(a_end - ps), src + bs + a_end, static_cast<int>(b_end - a_end),
-                        static_cast<int>(ob - ps), cnt, dst + bs + ob);
+            merge_chunk_s(src, bs + ps, static_cast<int>(a_end - ps), bs + a_end, static_cast<int>(b_end - a_end),
+                          static_cast<int>(ob - ps), cnt, dst, bs + ob);
         }
         __syncthreads();
         uint32_t* t = src;
@@ -174,19 +208,17 @@ __global__ void __launch_bounds__(kNetThreads)
             const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
             bool keep_low = false;
             const int q = network == 0 ? btn_partner(s, i, keep_low) : oet_partner(s, i, p, keep_low);
-            uint32_t* out_blk = dst + a * P + static_cast<uint32_t>(i) * L;
+            const uint32_t my0 = a * P + static_cast<uint32_t>(i) * L;
             if (q < 0) {
-                const uint32_t* in_blk = src + a * P + static_cast<uint32_t>(i) * L;
 #pragma unroll
                 for (int k = 0; k < kNK; ++k)
-                    if (k < cnt) out_blk[ob + k] = in_blk[ob + k];
+                    if (k < cnt) dst[pad(my0 + ob + k)] = src[pad(my0 + ob + k)];
                 continue;
             }
             const int lo_w = min(i, q), hi_w = max(i, q);
-            const uint32_t* A = src + a * P + static_cast<uint32_t>(lo_w) * L;
-            const uint32_t* B = src + a * P + static_cast<uint32_t>(hi_w) * L;
             const int diag = static_cast<int>((keep_low ? 0u : L) + ob);
-            merge_chunk(A, static_cast<int>(L), B, static_cast<int>(L), diag, cnt, out_blk + ob);
+            merge_chunk_s(src, a * P + static_cast<uint32_t>(lo_w) * L, static_cast<int>(L),
+                          a * P + static_cast<uint32_t>(hi_w) * L, static_cast<int>(L), diag, cnt, dst, my0 + ob);
         }
         __syncthreads();
         uint32_t* t = src;
@@ -198,10 +230,10 @@ __global__ void __launch_bounds__(kNetThreads)
     if (full) {
         for (uint32_t idx = tid; idx < static_cast<uint32_t>(na) * len; idx += kNetThreads) {
             const uint32_t a = idx / len, e = idx - a * len;
-            out[(array0 + a) * len + e] = src[a * P + e];
+            out[(array0 + a) * len + e] = src[pad(a * P + e)];
         }
     } else {
-        for (uint32_t idx = tid; idx < tot; idx += kNetThreads) out[array0 * P + idx] = src[idx];
+        for (uint32_t idx = tid; idx < tot; idx += kNetThreads) out[array0 * P + idx] = src[pad(idx)];
     }
 }
 
@@ -236,11 +268,12 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     const uint32_t P = L * static_cast<uint32_t>(p);
     if (P == 0 || P > kNetMaxPadded) return -1;
     const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
-    const size_t smem = 2ull * apc * P * sizeof(uint32_t);
+    const size_t padded = static_cast<size_t>(apc) * P + (static_cast<size_t>(apc) * P >> 5) + 1;
+    const size_t smem = 2ull * padded * sizeof(uint32_t);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(block_network_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(2 * kNetMaxPadded * sizeof(uint32_t)));
+                             static_cast<int>(2 * (kNetMaxPadded + kNetMaxPadded / 32 + 1) * sizeof(uint32_t)));
         attr = true;
     }
     const uint64_t grid = (num_arrays + apc - 1) / apc;
