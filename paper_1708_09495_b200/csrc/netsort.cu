@@ -6,11 +6,11 @@
 // several) array(s) entirely in shared memory.  The p BSP workers become p
 // blocks of L = ceil(len/p) keys inside the CTA; the reference's supersteps
 // become __syncthreads() between ping-pong shared-memory buffers:
-//   superstep 0  -- local sort of every block (netsort.hpp:167): 8-key
-//                   register sorting networks, then bottom-up merge-path
+//   superstep 0  -- local sort of every block (netsort.hpp:167): 16-key
+//                   register sorting networks (Batcher), then merge-path
 //                   merges inside each block;
 //   superstep s  -- merge_split of every (worker, partner) pair of stage s
-//                   (netsort.hpp:170-179): each thread produces 8 consecutive
+//                   (netsort.hpp:170-179): each thread produces 16 consecutive
 //                   outputs of the pair's merged sequence after a merge-path
 //                   binary search; the keep_low worker takes outputs [0, L),
 //                   its partner [L, 2L); idle OET edge workers copy.
@@ -27,7 +27,7 @@ namespace bsg {
 
 namespace {
 
-constexpr int kNK = 8;          // outputs per thread-chunk
+constexpr int kNK = 16;         // outputs per thread-chunk
 constexpr int kNetThreads = 256;
 constexpr uint32_t kPad = 0xFFFFFFFFu;
 
@@ -37,12 +37,22 @@ __device__ __forceinline__ void cas(uint32_t& a, uint32_t& b) {
     b = hi;
 }
 
-// Odd-even transposition network on 8 registers (28 comparators).
-__device__ __forceinline__ void sort8(uint32_t (&v)[kNK]) {
+// Batcher's odd-even merge sort network on N registers (63 comparators for
+// N = 16), fully unrolled.
+template <int N>
+__device__ __forceinline__ void sort_regs(uint32_t (&v)[N]) {
 #pragma unroll
-    for (int r = 0; r < kNK; ++r) {
+    for (int p = 1; p < N; p <<= 1) {
 #pragma unroll
-        for (int j = r & 1; j + 1 < kNK; j += 2) cas(v[j], v[j + 1]);
+        for (int k = p; k >= 1; k >>= 1) {
+#pragma unroll
+            for (int j = k % p; j + k < N; j += 2 * k) {
+#pragma unroll
+                for (int i = 0; i < k; ++i) {
+                    if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p)) cas(v[i + j], v[i + j + k]);
+                }
+            }
+        }
     }
 }
 
@@ -67,15 +77,13 @@ __device__ __forceinline__ void merge_chunk_s(const uint32_t* S, uint32_t a0, in
     for (int k = 0; k < kNK; ++k) {
         if (k < cnt) {
             const bool take_a = i < na && (j >= nb || av <= bv);
-            if (take_a) {
-                D[pad(dst0 + k)] = av;
-                ++i;
-                av = i < na ? S[pad(a0 + i)] : 0u;
-            } else {
-                D[pad(dst0 + k)] = bv;
-                ++j;
-                bv = j < nb ? S[pad(b0 + j)] : 0u;
-            }
+            D[pad(dst0 + k)] = take_a ? av : bv;
+            i += take_a ? 1 : 0;
+            j += take_a ? 0 : 1;
+            const bool more = take_a ? i < na : j < nb;
+            const uint32_t nxt = more ? S[pad(take_a ? a0 + i : b0 + j)] : 0u;
+            av = take_a ? nxt : av;
+            bv = take_a ? bv : nxt;
         }
     }
 }
@@ -161,7 +169,7 @@ __global__ void __launch_bounds__(kNetThreads)
     const uint32_t cb = (L + kNK - 1) / kNK; // chunks per block
     const uint32_t items = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cb;
 
-    // superstep 0: local sort of every block.  (a) 8-key register networks
+    // superstep 0: local sort of every block.  (a) 16-key register sorting networks
     for (uint32_t it = tid; it < items; it += kNetThreads) {
         const uint32_t a = it / (p * cb), rem = it - a * p * cb;
         const uint32_t w = rem / cb, c = rem - w * cb;
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(kNetThreads)
         uint32_t v[kNK];
 #pragma unroll
         for (int k = 0; k < kNK; ++k) v[k] = k < cnt ? bufA[pad(b0 + ob + k)] : kPad;
-        sort8(v);
+        sort_regs<kNK>(v);
 #pragma unroll
         for (int k = 0; k < kNK; ++k)
             if (k < cnt) bufA[pad(b0 + ob + k)] = v[k];
