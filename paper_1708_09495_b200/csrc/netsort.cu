@@ -37,23 +37,72 @@ __device__ __forceinline__ void cas(uint32_t& a, uint32_t& b) {
     b = hi;
 }
 
-// Batcher's odd-even merge sort network on N registers (63 comparators for
-// N = 16), fully unrolled.
-template <int N>
-__device__ __forceinline__ void sort_regs(uint32_t (&v)[N]) {
-#pragma unroll
-    for (int p = 1; p < N; p <<= 1) {
-#pragma unroll
-        for (int k = p; k >= 1; k >>= 1) {
-#pragma unroll
-            for (int j = k % p; j + k < N; j += 2 * k) {
-#pragma unroll
-                for (int i = 0; i < k; ++i) {
-                    if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p)) cas(v[i + j], v[i + j + k]);
-                }
-            }
-        }
-    }
+// Batcher's odd-even merge sort network on 16 registers (63 comparators,
+// generated and checked against all 2^16 zero-one inputs).
+__device__ __forceinline__ void sort16(uint32_t (&v)[16]) {
+    cas(v[0], v[1]);
+    cas(v[2], v[3]);
+    cas(v[4], v[5]);
+    cas(v[6], v[7]);
+    cas(v[8], v[9]);
+    cas(v[10], v[11]);
+    cas(v[12], v[13]);
+    cas(v[14], v[15]);
+    cas(v[0], v[2]);
+    cas(v[1], v[3]);
+    cas(v[4], v[6]);
+    cas(v[5], v[7]);
+    cas(v[8], v[10]);
+    cas(v[9], v[11]);
+    cas(v[12], v[14]);
+    cas(v[13], v[15]);
+    cas(v[1], v[2]);
+    cas(v[5], v[6]);
+    cas(v[9], v[10]);
+    cas(v[13], v[14]);
+    cas(v[0], v[4]);
+    cas(v[1], v[5]);
+    cas(v[2], v[6]);
+    cas(v[3], v[7]);
+    cas(v[8], v[12]);
+    cas(v[9], v[13]);
+    cas(v[10], v[14]);
+    cas(v[11], v[15]);
+    cas(v[2], v[4]);
+    cas(v[3], v[5]);
+    cas(v[10], v[12]);
+    cas(v[11], v[13]);
+    cas(v[1], v[2]);
+    cas(v[3], v[4]);
+    cas(v[5], v[6]);
+    cas(v[9], v[10]);
+    cas(v[11], v[12]);
+    cas(v[13], v[14]);
+    cas(v[0], v[8]);
+    cas(v[1], v[9]);
+    cas(v[2], v[10]);
+    cas(v[3], v[11]);
+    cas(v[4], v[12]);
+    cas(v[5], v[13]);
+    cas(v[6], v[14]);
+    cas(v[7], v[15]);
+    cas(v[4], v[8]);
+    cas(v[5], v[9]);
+    cas(v[6], v[10]);
+    cas(v[7], v[11]);
+    cas(v[2], v[4]);
+    cas(v[3], v[5]);
+    cas(v[6], v[8]);
+    cas(v[7], v[9]);
+    cas(v[10], v[12]);
+    cas(v[11], v[13]);
+    cas(v[1], v[2]);
+    cas(v[3], v[4]);
+    cas(v[5], v[6]);
+    cas(v[7], v[8]);
+    cas(v[9], v[10]);
+    cas(v[11], v[12]);
+    cas(v[13], v[14]);
 }
 
 // Shared-memory index with one pad word per 32: the stride-4/stride-8 access
@@ -179,7 +228,7 @@ __global__ void __launch_bounds__(kNetThreads)
         uint32_t v[kNK];
 #pragma unroll
         for (int k = 0; k < kNK; ++k) v[k] = k < cnt ? bufA[pad(b0 + ob + k)] : kPad;
-        sort_regs<kNK>(v);
+        sort16(v);
 #pragma unroll
         for (int k = 0; k < kNK; ++k)
             if (k < cnt) bufA[pad(b0 + ob + k)] = v[k];
