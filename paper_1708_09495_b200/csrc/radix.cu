@@ -216,8 +216,11 @@ __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
 
 // Lanes of the warp holding the same digit (bit-serial ballot multisplit):
 // per bit one predicate test, one VOTE, a predicated invert and an AND.
+// `neg1` is a runtime -1 (kernel argument) so that ptxas keeps the
+// conditional complement ~v = v*(-1) + (-1) as an IMAD on the FMA pipe instead
+// of an IADD3/LOP3 on the (half-rate, saturated) integer ALU pipe.
 template <int NBITS>
-__device__ __forceinline__ uint32_t peers_ballot(uint32_t d) {
+__device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
     uint32_t m[NBITS];
 #pragma unroll
     for (int b = 0; b < NBITS; ++b) {
@@ -225,9 +228,9 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d) {
             "and.b32 t, %1, %2;\n\t"
             "setp.ne.u32 p, t, 0;\n\t"
             "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
-            "@!p not.b32 %0, %0;\n\t}"
+            "@!p mad.lo.s32 %0, %0, %3, %3;\n\t}"
             : "=r"(m[b])
-            : "r"(d), "r"(1u << b));
+            : "r"(d), "r"(1u << b), "r"(neg1));
     }
     // AND-reduce the masks with 3-input LOP3s
     uint32_t peers = m[0];
@@ -260,7 +263,7 @@ template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
                     int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
-                    uint32_t* __restrict__ tile_counter, int use_tma, int dbg) {
+                    uint32_t* __restrict__ tile_counter, int use_tma, int dbg, int32_t neg1) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     using Off = typename L::Off;
     constexpr int RADIX = L::RADIX;
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 else if (RANK == 1 || (RANK == 2 && (i & 3) == 0) || (RANK == 3 && (i & 1) == 0))
                     peers[i] = __match_any_sync(0xffffffffu, d);
                 else
-                    peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d);
+                    peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
             }
             // then the per-warp running counts, item by item (input order):
             // every peer reads the same counter (a broadcast), the highest
@@ -531,7 +534,8 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
         uint32_t* st = status + c * words_per_chunk;
         const uint64_t* base = base_for_pass + c * static_cast<uint64_t>(passes_stride) * RADIX;
         TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
-        kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0, dbg);
+        kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0, dbg,
+                                                   -1);
         ++launches;
     }
     return launches;
