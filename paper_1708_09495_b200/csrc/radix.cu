@@ -205,6 +205,13 @@ __global__ void final_copy_kernel(const PassPlan* __restrict__ plan, uint32_t* o
 // Persistent CTAs: while tile k is ranked/scattered, the TMA engine already
 // streams tile k+1 into the other shared-memory buffer.
 // ---------------------------------------------------------------------------
+// The same byte digit computed on the FMA pipe (two IMADs) instead of the
+// integer ALU pipe: (k << (24 - shift)) then the high word of (x * 256).
+// `mul` = 1 << (24 - shift) is a runtime value so ptxas keeps the IMADs.
+__device__ __forceinline__ uint32_t digit8_fma(uint32_t k, uint32_t mul) {
+    return __umulhi(k * mul, 256u);
+}
+
 template <int BITS>
 __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
     if constexpr (BITS == 8) {
@@ -311,6 +318,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
 
     const uint32_t lt = lanemask_lt();
+    const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
     for (uint32_t k = 0;; ++k) {
         const int cur = k & 1;
         __syncthreads(); // s_tile[cur] visible; previous tile's buffer/counters free
@@ -353,7 +361,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
                 const bool ok = FULL || idx < valid;
-                const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : static_cast<uint32_t>(RADIX);
+                const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
+                                      : static_cast<uint32_t>(RADIX);
                 if (dbg & 2) peers[i] = 1u << lane;
                 else if (RANK == 1 || (RANK == 2 && (i & 3) == 0) || (RANK == 3 && (i & 1) == 0))
                     peers[i] = __match_any_sync(0xffffffffu, d);
@@ -367,7 +376,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
                 const bool ok = FULL || idx < valid;
-                const uint32_t d = ok ? digit_of_key<BITS>(keys[i], shift) : 0u;
+                const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)) : 0u;
                 const uint32_t before = ok ? wc[d] : 0u;
                 const bool leader = (31 - __clz(peers[i])) == lane;
                 if (leader && ok) wc[d] = before + __popc(peers[i]);
