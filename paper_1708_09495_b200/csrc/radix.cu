@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             const uint32_t idx = wbase + i * 32 + lane;
             if (full || idx < valid) {
                 const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
-                buf[wc[BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
+                buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
         }
 
@@ -476,8 +476,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = j * THREADS + tid;
                 const uint32_t key = buf[i];
-                dst[static_cast<Off>(s_delta[BITS == 8 ? digit8_fma(key, dmul) : digit_of_key<BITS>(key, shift)] + i)] =
-                    key;
+                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
             }
         } else {
             for (uint32_t i = tid; i < valid; i += THREADS) {
