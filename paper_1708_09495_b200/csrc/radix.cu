@@ -248,6 +248,10 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
     return peers;
 }
 
+// Phase-cycle instrumentation (dbg bit 8): thread 0 of every CTA accumulates
+// clock64 deltas per phase.  Development aid only.
+__device__ unsigned long long g_phase_cycles[8];
+
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 struct OnesweepSmem {
     static constexpr int RADIX = 1 << BITS;
@@ -335,7 +339,16 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         uint32_t* buf = s_in + cur * TILE;
         // non-TMA body / unaligned tail straight from global
         const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
+        long long t_ph = (dbg & 8) ? clock64() : 0;
+        auto phase = [&](int ph) {
+            if ((dbg & 8) && tid == 0) {
+                const long long now = clock64();
+                atomicAdd(&g_phase_cycles[ph], static_cast<unsigned long long>(now - t_ph));
+                t_ph = now;
+            }
+        };
         mbar_wait_parity(&s_bar[cur], (k >> 1) & 1);
+        phase(0);
 
         // ---- warp-local stable ranks + per-warp digit counts --------------
         // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS); item i of lane l is
@@ -388,7 +401,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         };
         if (full) rank_items(std::true_type{});
         else rank_items(std::false_type{});
+        phase(1);
         __syncthreads();
+        phase(2);
 
         // ---- per-digit: warp prefix, tile count, publish aggregate ---------
         uint32_t tile_cnt = 0;
@@ -420,6 +435,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 
         }
         __syncthreads();
+        phase(3);
 
         // ---- stage the tile in digit order (in place: keys are in registers)
 #pragma unroll
@@ -431,6 +447,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             }
         }
 
+        phase(4);
         // ---- decoupled look-back: LB_WIN predecessors per round trip ------
         // (each warp's load covers 32 consecutive digits of one predecessor:
         // one coalesced 128-byte request per predecessor per warp)
@@ -469,6 +486,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         }
         __syncthreads();
 
+        phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
         for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
         if (full) {
@@ -484,6 +502,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
             }
         }
+        phase(6);
     }
 }
 
@@ -727,3 +746,14 @@ int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uin
 }
 
 } // namespace bsg
+
+// Development aid: reads (and optionally clears) the one-sweep phase-cycle
+// accumulators filled when BSG_OS_DBG has bit 8 set.
+extern "C" int bsg_debug_phase_cycles(unsigned long long* out8, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out8, bsg::g_phase_cycles, sizeof(unsigned long long) * 8);
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        e = cudaMemcpyToSymbol(bsg::g_phase_cycles, z, sizeof(z));
+    }
+    return e == cudaSuccess ? 0 : 3;
+}
