@@ -466,8 +466,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             incl = warp_inclusive_scan(tile_cnt);
             if (lane == 31) s_scan[dw] = incl;
         }
-        if constexpr (SVC) asm volatile("bar.sync 1, %0;" ::"n"(SCAN_WARPS * 32) : "memory");
-        else __syncthreads();
+        if constexpr (SVC) {
+            if (dig_warp) asm volatile("bar.sync 1, %0;" ::"n"(SCAN_WARPS * 32) : "memory");
+        } else {
+            __syncthreads();
+        }
         if (dig) {
             excl = incl - tile_cnt;
 #pragma unroll
