@@ -205,6 +205,13 @@ __global__ void final_copy_kernel(const PassPlan* __restrict__ plan, uint32_t* o
 // Persistent CTAs: while tile k is ranked/scattered, the TMA engine already
 // streams tile k+1 into the other shared-memory buffer.
 // ---------------------------------------------------------------------------
+// The same byte digit computed on the FMA pipe (two IMADs) instead of the
+// integer ALU pipe: (k << (24 - shift)) then the high word of (x * 256).
+// `mul` = 1 << (24 - shift) is a runtime value so ptxas keeps the IMADs.
+__device__ __forceinline__ uint32_t digit8_fma(uint32_t k, uint32_t mul) {
+    return __umulhi(k * mul, 256u);
+}
+
 template <int BITS>
 __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
     if constexpr (BITS == 8) {
@@ -214,15 +221,11 @@ __device__ __forceinline__ uint32_t digit_of_key(uint32_t k, int shift) {
     }
 }
 
-// The same byte digit on the FMA pipe (two IMADs) instead of the integer ALU
-// pipe: x = k << (24 - shift), digit = high word of x * 256.  `mul` is a
-// runtime value so ptxas keeps the IMADs.
-__device__ __forceinline__ uint32_t digit8_fma(uint32_t k, uint32_t mul) { return __umulhi(k * mul, 256u); }
-
 // Lanes of the warp holding the same digit (bit-serial ballot multisplit):
-// per bit one predicate test, one VOTE, a predicated complement and a share of
-// a 3-input AND.  `neg1` is a runtime -1 so the complement ~v = v*(-1)+(-1)
-// stays an IMAD on the FMA pipe instead of the saturated integer ALU pipe.
+// per bit one predicate test, one VOTE, a predicated invert and an AND.
+// `neg1` is a runtime -1 (kernel argument) so that ptxas keeps the
+// conditional complement ~v = v*(-1) + (-1) as an IMAD on the FMA pipe instead
+// of an IADD3/LOP3 on the (half-rate, saturated) integer ALU pipe.
 template <int NBITS>
 __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
     uint32_t m[NBITS];
@@ -236,6 +239,7 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
             : "=r"(m[b])
             : "r"(d), "r"(1u << b), "r"(neg1));
     }
+    // AND-reduce the masks with 3-input LOP3s
     uint32_t peers = m[0];
     int b = 1;
 #pragma unroll
@@ -248,23 +252,15 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
 // clock64 deltas per phase.  Development aid only.
 __device__ unsigned long long g_phase_cycles[8];
 
-// Work split of a CTA.  SVC (1024-thread, 8-bit): warps [0, RW) rank, stage and
-// write a RW*32*ITEMS-key tile; the last SW = RADIX/32 "service" warps own one
-// digit per thread, publish the tile aggregate, run the look-back while the
-// rank warps stage, and help writing.  Otherwise every warp ranks and the
-// first RADIX threads also do the digit work.
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 struct OnesweepSmem {
     static constexpr int RADIX = 1 << BITS;
     static constexpr int WARPS = THREADS / 32;
-    static constexpr bool SVC = (THREADS == 1024 && BITS == 8);
-    static constexpr int SW = SVC ? RADIX / 32 : 0;   // service warps
-    static constexpr int RW = WARPS - SW;             // rank warps
-    static constexpr int TILE = RW * 32 * ITEMS;
+    static constexpr int TILE = THREADS * ITEMS;
     using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
     static constexpr size_t in_off = 0;                                          // 2 x TILE u32
-    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // RW*RADIX u32
-    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * RW * RADIX; // RADIX Off
+    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // WARPS*RADIX u32
+    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX Off
     static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
     static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
     static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // 2 tile ids
@@ -272,41 +268,8 @@ struct OnesweepSmem {
     static constexpr size_t bytes = bar_off + 16;
 };
 
-// Decoupled look-back for one digit: LB_WIN predecessors per round trip (each
-// warp's load covers 32 consecutive digits of one predecessor: one coalesced
-// 128-byte request).  Returns the exclusive prefix of the digit's count over
-// all earlier tiles of the chunk.
-template <int RADIX>
-__device__ __forceinline__ uint32_t lookback(const uint32_t* status, uint32_t tile, int d) {
-    constexpr int LB_WIN = 32;
-    uint32_t prefix = 0;
-    int64_t t = static_cast<int64_t>(tile) - 1;
-    while (true) {
-        uint32_t sv[LB_WIN];
-#pragma unroll
-        for (int j = 0; j < LB_WIN; ++j)
-            sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + d]) : kFlagInc;
-        int used = 0;
-        bool done = false, stop = false;
-#pragma unroll
-        for (int j = 0; j < LB_WIN; ++j) {
-            if (!stop) {
-                if ((sv[j] & ~kValMask) == 0) {
-                    stop = true;
-                } else {
-                    prefix += sv[j] & kValMask;
-                    ++used;
-                    if (sv[j] & kFlagInc) done = stop = true;
-                }
-            }
-        }
-        if (done) return prefix;
-        t -= used;
-    }
-}
-
-// dbg bits (timing experiments only; output is wrong when 1 or 2 is set):
-//   1 = skip look-back waits, 2 = trivial ranks, 8 = phase cycle counters.
+// dbg bits (timing experiments only; output is wrong when set):
+//   1 = skip look-back waits, 2 = unstable atomic ranks instead of match/ballot.
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
@@ -315,12 +278,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     using Off = typename L::Off;
     constexpr int RADIX = L::RADIX;
-    constexpr int RW = L::RW;
+    constexpr int WARPS = L::WARPS;
     constexpr int TILE = L::TILE;
-    constexpr bool SVC = L::SVC;
     static_assert(ITEMS % 2 == 0, "ranks are packed in pairs");
     static_assert(RADIX <= THREADS, "one thread per digit");
-    static_assert(TILE % THREADS == 0 || !SVC, "write loop covers the tile in whole rounds");
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
     uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + L::wcnt_off);
@@ -338,11 +299,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const bool ranker = warp < RW;
-    // digit owned by this thread: service threads (SVC) or the first RADIX threads
-    const int dg = SVC ? tid - RW * 32 : tid;
-    const bool dig = dg >= 0 && dg < RADIX;
 
+    // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
     auto issue = [&](uint32_t tile, int b) {
         if (tile >= ntiles) return;
         const uint32_t start = tile * TILE;
@@ -361,7 +319,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         s_tile[0] = t0;
         issue(t0, 0);
     }
-    for (int i = tid; i < RW * RADIX; i += THREADS) s_wcnt[i] = 0;
+    for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
 
     const uint32_t lt = lanemask_lt();
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
@@ -393,8 +351,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         phase(0);
 
         // ---- warp-local stable ranks + per-warp digit counts --------------
-        // Rank warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS); item i of lane
-        // l is key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
+        // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS); item i of lane l is
+        // key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
         const uint32_t wbase = warp * (32 * ITEMS);
         uint32_t* wc = s_wcnt + warp * RADIX;
         uint32_t keys[ITEMS];
@@ -411,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                     keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
                 }
             }
-            // all multisplit masks first: independent, latencies overlap
+            // all match-any / ballot masks first: independent, latencies overlap
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
@@ -419,8 +377,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
                                       : static_cast<uint32_t>(RADIX);
                 if (dbg & 2) peers[i] = 1u << lane;
-                else if (RANK == 1) peers[i] = __match_any_sync(0xffffffffu, d);
-                else peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
+                else if (RANK == 1 || (RANK == 2 && (i & 3) == 0) || (RANK == 3 && (i & 1) == 0))
+                    peers[i] = __match_any_sync(0xffffffffu, d);
+                else
+                    peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
             }
             // then the per-warp running counts, item by item (input order):
             // every peer reads the same counter (a broadcast), the highest
@@ -439,94 +399,99 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 else packed[i >> 1] = r;
             }
         };
-        if (ranker) {
-            if (full) rank_items(std::true_type{});
-            else rank_items(std::false_type{});
-        }
+        if (full) rank_items(std::true_type{});
+        else rank_items(std::false_type{});
         phase(1);
         __syncthreads();
         phase(2);
 
         // ---- per-digit: warp prefix, tile count, publish aggregate ---------
-        constexpr int SCAN_WARPS = (RADIX + 31) / 32;
-        const int dw = SVC ? warp - RW : warp; // index of this digit warp
-        const bool dig_warp = SVC ? warp >= RW : warp < SCAN_WARPS;
-        uint32_t tile_cnt = 0, excl = 0;
-        if (dig) {
+        uint32_t tile_cnt = 0;
+        if (tid < RADIX) {
 #pragma unroll
-            for (int w = 0; w < RW; ++w) {
-                const uint32_t c = s_wcnt[w * RADIX + dg];
-                s_wcnt[w * RADIX + dg] = tile_cnt;
+            for (int w = 0; w < WARPS; ++w) {
+                const uint32_t c = s_wcnt[w * RADIX + tid];
+                s_wcnt[w * RADIX + tid] = tile_cnt;
                 tile_cnt += c;
             }
-            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + dg], (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
+            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
+                           (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
         }
+        constexpr int SCAN_WARPS = (RADIX + 31) / 32;
         uint32_t incl = 0;
-        if (dig_warp) {
+        if (warp < SCAN_WARPS) {
             incl = warp_inclusive_scan(tile_cnt);
-            if (lane == 31) s_scan[dw] = incl;
+            if (lane == 31) s_scan[warp] = incl;
         }
-        if constexpr (SVC) {
-            if (dig_warp) asm volatile("bar.sync 1, %0;" ::"n"(SCAN_WARPS * 32) : "memory");
-        } else {
-            __syncthreads();
-        }
-        if (dig) {
-            excl = incl - tile_cnt;
+        __syncthreads();
+        if (tid < RADIX) {
+            uint32_t excl = incl - tile_cnt;
 #pragma unroll
             for (int w = 0; w < SCAN_WARPS; ++w)
-                if (w < dw) excl += s_scan[w];
-            s_excl[dg] = excl;
+                if (w < warp) excl += s_scan[w];
+            s_excl[tid] = excl;
 #pragma unroll
-            for (int w = 0; w < RW; ++w) s_wcnt[w * RADIX + dg] += excl;
+            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
+
         }
         __syncthreads();
         phase(3);
 
-        if constexpr (SVC) {
-            if (ranker) {
-                // ---- stage the tile in digit order (in place, keys in registers)
+        // ---- stage the tile in digit order (in place: keys are in registers)
 #pragma unroll
-                for (int i = 0; i < ITEMS; ++i) {
-                    const uint32_t idx = wbase + i * 32 + lane;
-                    if (full || idx < valid) {
-                        const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
-                        buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
-                    }
-                }
-                phase(4);
-            } else if (dig) {
-                // ---- look-back, concurrently with the staging ----------------
-                const uint32_t prefix = (tile > 0 && !(dbg & 1)) ? lookback<RADIX>(status, tile, dg) : 0u;
-                if (tile > 0)
-                    st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + dg], kFlagInc | (prefix + tile_cnt));
-                s_delta[dg] = static_cast<Off>(digit_base[dg] + prefix - excl);
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const uint32_t idx = wbase + i * 32 + lane;
-                if (full || idx < valid) {
-                    const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
-                    buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
-                }
-            }
-            phase(4);
-            if (dig) {
-                const uint32_t prefix = (tile > 0 && !(dbg & 1)) ? lookback<RADIX>(status, tile, dg) : 0u;
-                if (tile > 0)
-                    st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + dg], kFlagInc | (prefix + tile_cnt));
-                s_delta[dg] = static_cast<Off>(digit_base[dg] + prefix - excl);
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t idx = wbase + i * 32 + lane;
+            if (full || idx < valid) {
+                const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+                buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
         }
-        __syncthreads();
-        phase(5);
 
+        phase(4);
+        // ---- decoupled look-back: LB_WIN predecessors per round trip ------
+        // (each warp's load covers 32 consecutive digits of one predecessor:
+        // one coalesced 128-byte request per predecessor per warp)
+        if (tid < RADIX) {
+            constexpr int LB_WIN = 32;
+            uint32_t prefix = 0;
+            if (tile > 0 && !(dbg & 1)) {
+                int64_t t = static_cast<int64_t>(tile) - 1;
+                while (true) {
+                    uint32_t sv[LB_WIN];
+#pragma unroll
+                    for (int j = 0; j < LB_WIN; ++j)
+                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                             : kFlagInc;
+                    int used = 0;
+                    bool done = false, stop = false;
+#pragma unroll
+                    for (int j = 0; j < LB_WIN; ++j) {
+                        if (!stop) {
+                            if ((sv[j] & ~kValMask) == 0) {
+                                stop = true;
+                            } else {
+                                prefix += sv[j] & kValMask;
+                                ++used;
+                                if (sv[j] & kFlagInc) done = stop = true;
+                            }
+                        }
+                    }
+                    if (done) break;
+                    t -= used;
+                }
+            }
+            if (tile > 0)
+                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
+        }
+        __syncthreads();
+
+        phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
-        for (int i = tid; i < RW * RADIX; i += THREADS) s_wcnt[i] = 0;
+        for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
         if (full) {
 #pragma unroll 4
-            for (int j = 0; j < TILE / THREADS; ++j) {
+            for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = j * THREADS + tid;
                 const uint32_t key = buf[i];
                 dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
@@ -607,11 +572,17 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
-    // RANK 0 = ballot multisplit (default), 1 = match-any (measured ~40 SM-cycles per warp-item on B200)
+    // RANK 0 = ballot multisplit (default), 1 = match-any, 2/3 = match-any on 1/4 / 1/2 of the items
     if constexpr (BITS == 8) {
         switch (onesweep_rank_mode()) {
         case 1:
             return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 1>(plan, pass, n, shift, base_for_pass,
+                                                                        passes_stride, status, stream, use_tma);
+        case 2:
+            return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 2>(plan, pass, n, shift, base_for_pass,
+                                                                        passes_stride, status, stream, use_tma);
+        case 3:
+            return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 3>(plan, pass, n, shift, base_for_pass,
                                                                         passes_stride, status, stream, use_tma);
         default:
             break;
