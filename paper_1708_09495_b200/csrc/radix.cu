@@ -252,62 +252,24 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
 // clock64 deltas per phase.  Development aid only.
 __device__ unsigned long long g_phase_cycles[8];
 
-// Shared-memory plan of the pass: three tile buffers (tile k is ranked in
-// one while tile k-1, already staged, is written out of another and tile k+1
-// streams into the third), 16-bit per-warp digit counters (tile offsets stay
-// below 2^16), two delta tables (tiles k-1 and k).
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 struct OnesweepSmem {
     static constexpr int RADIX = 1 << BITS;
     static constexpr int WARPS = THREADS / 32;
     static constexpr int TILE = THREADS * ITEMS;
-    static_assert(TILE <= 65536, "16-bit tile offsets");
     using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
-    static constexpr size_t in_off = 0;                                              // 3 x TILE u32
-    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 3 * TILE;         // WARPS*RADIX u16
-    static constexpr size_t delta_off = wcnt_off + sizeof(uint16_t) * WARPS * RADIX; // 2 x RADIX Off
-    static constexpr size_t excl_off = delta_off + sizeof(Off) * 2 * RADIX;          // RADIX u32
-    static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;          // 32 u32
-    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;             // 3 tile ids + 3 valid
-    static constexpr size_t bar_off = (misc_off + 32 + 7) & ~size_t{7};              // 3 mbarriers
-    static constexpr size_t bytes = bar_off + 3 * 8;
+    static constexpr size_t in_off = 0;                                          // 2 x TILE u32
+    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // WARPS*RADIX u32
+    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX Off
+    static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
+    static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
+    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // 2 tile ids
+    static constexpr size_t bar_off = misc_off + 16;                              // 2 mbarriers
+    static constexpr size_t bytes = bar_off + 16;
 };
 
-// Decoupled look-back for one digit: LB_WIN predecessors per round trip (each
-// warp's load covers 32 consecutive digits of one predecessor: one coalesced
-// 128-byte request).  Returns the exclusive prefix of the digit's count over
-// the earlier tiles of the chunk.
-template <int RADIX>
-__device__ __forceinline__ uint32_t lookback(const uint32_t* status, uint32_t tile, int d) {
-    constexpr int LB_WIN = 32;
-    uint32_t prefix = 0;
-    int64_t t = static_cast<int64_t>(tile) - 1;
-    while (true) {
-        uint32_t sv[LB_WIN];
-#pragma unroll
-        for (int j = 0; j < LB_WIN; ++j)
-            sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + d]) : kFlagInc;
-        int used = 0;
-        bool done = false, stop = false;
-#pragma unroll
-        for (int j = 0; j < LB_WIN; ++j) {
-            if (!stop) {
-                if ((sv[j] & ~kValMask) == 0) {
-                    stop = true;
-                } else {
-                    prefix += sv[j] & kValMask;
-                    ++used;
-                    if (sv[j] & kFlagInc) done = stop = true;
-                }
-            }
-        }
-        if (done) return prefix;
-        t -= used;
-    }
-}
-
-// dbg bits (timing experiments only; output is wrong when 1 or 2 is set):
-//   1 = skip look-back waits, 2 = trivial ranks, 8 = phase cycle counters.
+// dbg bits (timing experiments only; output is wrong when set):
+//   1 = skip look-back waits, 2 = unstable atomic ranks instead of match/ballot.
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
@@ -322,13 +284,12 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     static_assert(RADIX <= THREADS, "one thread per digit");
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
-    uint16_t* s_wcnt = reinterpret_cast<uint16_t*>(smem + L::wcnt_off);
+    uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + L::wcnt_off);
     Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
     uint32_t* s_excl = reinterpret_cast<uint32_t*>(smem + L::excl_off);
     uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
-    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);   // [3]
-    uint32_t* s_valid = s_tile + 4;                                        // [3]
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);      // [3]
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
 
     if (!plan->active[pass]) return;
     const uint32_t* __restrict__ src = plan->src[pass] + chunk_off;
@@ -339,14 +300,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     const int lane = tid & 31;
     const int warp = tid >> 5;
 
-    // claims the next tile and starts its TMA load into buffer b
-    auto claim = [&](int b) {
-        const uint32_t tile = atomicAdd(tile_counter, 1u);
-        s_tile[b] = tile;
+    // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
+    auto issue = [&](uint32_t tile, int b) {
         if (tile >= ntiles) return;
         const uint32_t start = tile * TILE;
         const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - start);
-        s_valid[b] = valid;
         const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&s_bar[b], vec * 4);
@@ -354,43 +312,32 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     };
 
     if (tid == 0) {
-        for (int b = 0; b < 3; ++b) mbar_init(&s_bar[b], 1);
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
         fence_mbar_init();
-        claim(0);
-        claim(1);
+        const uint32_t t0 = atomicAdd(tile_counter, 1u);
+        s_tile[0] = t0;
+        issue(t0, 0);
     }
-    for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
+    for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
 
     const uint32_t lt = lanemask_lt();
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
-    uint16_t* wc = s_wcnt + warp * RADIX;
-    const uint32_t wbase = warp * (32 * ITEMS);
-
-    // writes the staged tile in buffer bp (digit runs, coalesced within runs)
-    auto write_key = [&](const uint32_t* bufp, const Off* deltap, uint32_t i) {
-        const uint32_t key = bufp[i];
-        dst[static_cast<Off>(deltap[digit_of_key<BITS>(key, shift)] + i)] = key;
-    };
-
     for (uint32_t k = 0;; ++k) {
-        const int b = k % 3;
-        const int bp = (k + 2) % 3; // buffer of tile k-1
-        __syncthreads(); // s_tile/s_valid of tiles k and k-1 visible, delta(k-1) complete
-        const uint32_t tile = s_tile[b];
-        const bool have_prev = k > 0;
-        const uint32_t* bufp = s_in + bp * TILE;
-        const Off* deltap = s_delta + ((k + 1) & 1) * RADIX;
-        const uint32_t valid_prev = have_prev ? s_valid[bp] : 0u;
-        if (tile >= ntiles) {
-            // drain: write the last staged tile
-            for (uint32_t i = tid; i < valid_prev; i += THREADS) write_key(bufp, deltap, i);
-            break;
+        const int cur = k & 1;
+        __syncthreads(); // s_tile[cur] visible; previous tile's buffer/counters free
+        const uint32_t tile = s_tile[cur];
+        if (tile >= ntiles) break;
+        if (tid == 0) {
+            const uint32_t nxt = atomicAdd(tile_counter, 1u);
+            s_tile[cur ^ 1] = nxt;
+            issue(nxt, cur ^ 1);
         }
         const uint32_t tile_start = tile * TILE;
-        const uint32_t valid = s_valid[b];
+        const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - tile_start);
         const bool full = valid == TILE;
-        const bool full_prev = valid_prev == TILE;
-        uint32_t* buf = s_in + b * TILE;
+        uint32_t* buf = s_in + cur * TILE;
+        // non-TMA body / unaligned tail straight from global
         const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
         long long t_ph = (dbg & 8) ? clock64() : 0;
         auto phase = [&](int ph) {
@@ -400,13 +347,14 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 t_ph = now;
             }
         };
-        mbar_wait_parity(&s_bar[b], (k / 3) & 1);
+        mbar_wait_parity(&s_bar[cur], (k >> 1) & 1);
         phase(0);
 
-        // ---- warp-local stable ranks + per-warp digit counts, interleaved
-        //      with the write-out of the previous (already staged) tile ------
+        // ---- warp-local stable ranks + per-warp digit counts --------------
         // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS); item i of lane l is
         // key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
+        const uint32_t wbase = warp * (32 * ITEMS);
+        uint32_t* wc = s_wcnt + warp * RADIX;
         uint32_t keys[ITEMS];
         uint32_t packed[ITEMS / 2];
         auto rank_items = [&](auto full_tag) {
@@ -415,12 +363,13 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
-                if (FULL) keys[i] = idx < vec ? buf[idx] : __ldg(src + tile_start + idx);
-                else keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
+                if (FULL) {
+                    keys[i] = idx < vec ? buf[idx] : __ldg(src + tile_start + idx);
+                } else {
+                    keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
+                }
             }
-            // all multisplit masks first (independent), each followed by one
-            // key of the previous tile's write-out (load/store pipe work that
-            // overlaps the ALU-bound ballots)
+            // all match-any / ballot masks first: independent, latencies overlap
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
@@ -428,10 +377,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
                                       : static_cast<uint32_t>(RADIX);
                 if (dbg & 2) peers[i] = 1u << lane;
-                else if (RANK == 1) peers[i] = __match_any_sync(0xffffffffu, d);
-                else peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
-                const uint32_t wi = i * THREADS + tid;
-                if (have_prev && (full_prev || wi < valid_prev)) write_key(bufp, deltap, wi);
+                else if (RANK == 1 || (RANK == 2 && (i & 3) == 0) || (RANK == 3 && (i & 1) == 0))
+                    peers[i] = __match_any_sync(0xffffffffu, d);
+                else
+                    peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
             }
             // then the per-warp running counts, item by item (input order):
             // every peer reads the same counter (a broadcast), the highest
@@ -443,7 +392,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)) : 0u;
                 const uint32_t before = ok ? wc[d] : 0u;
                 const bool leader = (31 - __clz(peers[i])) == lane;
-                if (leader && ok) wc[d] = static_cast<uint16_t>(before + __popc(peers[i]));
+                if (leader && ok) wc[d] = before + __popc(peers[i]);
                 const uint32_t r = before + __popc(peers[i] & lt);
                 __syncwarp();
                 if (i & 1) packed[i >> 1] = __byte_perm(packed[i >> 1], r, 0x5410);
@@ -452,8 +401,6 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         };
         if (full) rank_items(std::true_type{});
         else rank_items(std::false_type{});
-        if (have_prev && !full_prev)  // remainder of a partial previous tile
-            for (uint32_t wi = ITEMS * THREADS + tid; wi < valid_prev; wi += THREADS) write_key(bufp, deltap, wi);
         phase(1);
         __syncthreads();
         phase(2);
@@ -464,7 +411,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 #pragma unroll
             for (int w = 0; w < WARPS; ++w) {
                 const uint32_t c = s_wcnt[w * RADIX + tid];
-                s_wcnt[w * RADIX + tid] = static_cast<uint16_t>(tile_cnt);
+                s_wcnt[w * RADIX + tid] = tile_cnt;
                 tile_cnt += c;
             }
             st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
@@ -484,13 +431,13 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 if (w < warp) excl += s_scan[w];
             s_excl[tid] = excl;
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] = static_cast<uint16_t>(s_wcnt[w * RADIX + tid] + excl);
+            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
+
         }
         __syncthreads();
         phase(3);
 
-        // ---- stage the tile in digit order (in place: keys are in registers);
-        //      each warp then zeroes its own counters for the next tile -------
+        // ---- stage the tile in digit order (in place: keys are in registers)
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const uint32_t idx = wbase + i * 32 + lane;
@@ -499,21 +446,63 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
         }
-        __syncwarp();
-        for (int i = lane; i < RADIX / 2; i += 32) reinterpret_cast<uint32_t*>(wc)[i] = 0;
-        phase(4);
 
-        // ---- decoupled look-back -> delta table of this tile ---------------
+        phase(4);
+        // ---- decoupled look-back: LB_WIN predecessors per round trip ------
+        // (each warp's load covers 32 consecutive digits of one predecessor:
+        // one coalesced 128-byte request per predecessor per warp)
         if (tid < RADIX) {
-            const uint32_t prefix = (tile > 0 && !(dbg & 1)) ? lookback<RADIX>(status, tile, tid) : 0u;
+            constexpr int LB_WIN = 32;
+            uint32_t prefix = 0;
+            if (tile > 0 && !(dbg & 1)) {
+                int64_t t = static_cast<int64_t>(tile) - 1;
+                while (true) {
+                    uint32_t sv[LB_WIN];
+#pragma unroll
+                    for (int j = 0; j < LB_WIN; ++j)
+                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                             : kFlagInc;
+                    int used = 0;
+                    bool done = false, stop = false;
+#pragma unroll
+                    for (int j = 0; j < LB_WIN; ++j) {
+                        if (!stop) {
+                            if ((sv[j] & ~kValMask) == 0) {
+                                stop = true;
+                            } else {
+                                prefix += sv[j] & kValMask;
+                                ++used;
+                                if (sv[j] & kFlagInc) done = stop = true;
+                            }
+                        }
+                    }
+                    if (done) break;
+                    t -= used;
+                }
+            }
             if (tile > 0)
                 st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
-            s_delta[(k & 1) * RADIX + tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
+            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
         }
-        // tile k-1's buffer is free (its write-out ran during the ranking):
-        // claim tile k+2 into it
-        if (tid == 0) claim(bp);
+        __syncthreads();
+
         phase(5);
+        // ---- write digit runs (coalesced within each run); reset counters --
+        for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
+        if (full) {
+#pragma unroll 4
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t i = j * THREADS + tid;
+                const uint32_t key = buf[i];
+                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
+            }
+        } else {
+            for (uint32_t i = tid; i < valid; i += THREADS) {
+                const uint32_t key = buf[i];
+                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
+            }
+        }
+        phase(6);
     }
 }
 
