@@ -268,9 +268,6 @@ int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in,
     const int run = full ? S : stages_limit;
     const uint64_t out_per = full ? len : padded;
     if (num_arrays && len && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
-    if (padded > kNetMaxPadded)
-        return fail(BSG_EINVAL, "block network: p*ceil(len/p) = " + std::to_string(padded) + " exceeds " +
-                                    std::to_string(kNetMaxPadded) + " keys per array (shared-memory resident)");
     if (stats) {
         std::vector<int32_t> partner(static_cast<size_t>(S) * p), keep(static_cast<size_t>(S) * p);
         bsg_network_schedule(network, p, partner.data(), keep.data(), S, &S);
@@ -291,9 +288,45 @@ int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in,
     const uint64_t n_in = num_arrays * len, n_out = num_arrays * out_per;
     return with_device_io(ctx, in, out, n_in, n_out, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
         if (num_arrays == 0 || len == 0) return BSG_OK;
-        const int l = launch_block_network(network, d_in, d_out, num_arrays, len, p, run, full, s);
-        if (l < 0) return cuda_fail(cudaGetLastError(), "block network launch");
-        ctx->launches += static_cast<uint64_t>(l);
+        if (padded <= kNetMaxPadded) { // shared-memory resident arrays: one CTA per array
+            const int l = launch_block_network(network, d_in, d_out, num_arrays, len, p, run, full, s);
+            if (l < 0) return cuda_fail(cudaGetLastError(), "block network launch");
+            ctx->launches += static_cast<uint64_t>(l);
+            return BSG_OK;
+        }
+        // large arrays: blocks live in global memory; local sort = the radix
+        // sort of each block (netsort.hpp:167 uses serial_radix_sort(., 256)),
+        // each merge-split stage = one merge-path kernel over all pairs.
+        cudaError_t e;
+        if ((e = ctx->stage_b.ensure(padded * 4)) != cudaSuccess) return cuda_fail(e, "network workspace");
+        if ((e = ctx->net_sched.ensure(padded * 4)) != cudaSuccess) return cuda_fail(e, "network workspace");
+        RadixWorkspace ws;
+        if (int rc = ctx->radix_ws(L, &ws)) return rc;
+        uint32_t* A = ctx->net_sched.as<uint32_t>();
+        uint32_t* B = ctx->stage_b.as<uint32_t>();
+        for (uint64_t a = 0; a < num_arrays; ++a) {
+            if ((e = cudaMemcpyAsync(A, d_in + a * len, static_cast<size_t>(len) * 4, cudaMemcpyDeviceToDevice, s)) !=
+                cudaSuccess)
+                return cuda_fail(e, "network copy");
+            if (padded > len && (e = cudaMemsetAsync(A + len, 0xFF, (padded - len) * 4, s)) != cudaSuccess)
+                return cuda_fail(e, "network pad");
+            for (int w = 0; w < p; ++w) {
+                const int l = launch_radix_sort8(A + static_cast<uint64_t>(w) * L, B + static_cast<uint64_t>(w) * L, L,
+                                                 ws, s, true);
+                if (l < 0) return cuda_fail(cudaGetLastError(), "network local sort");
+                ctx->launches += static_cast<uint64_t>(l);
+            }
+            uint32_t* cur = B;
+            uint32_t* oth = A;
+            for (int st = 0; st < run; ++st) {
+                if (launch_net_stage(cur, oth, p, static_cast<uint32_t>(L), network, st, s) < 0)
+                    return cuda_fail(cudaGetLastError(), "network stage");
+                ctx->launches += 1;
+                std::swap(cur, oth);
+            }
+            if ((e = cudaMemcpyAsync(d_out + a * out_per, cur, out_per * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+                return cuda_fail(e, "network copy out");
+        }
         return BSG_OK;
     });
 }

@@ -317,7 +317,47 @@ __global__ void __launch_bounds__(kMsThreads)
     }
 }
 
+
+// One merge-split stage of a large (global-memory) block network: every
+// output chunk of 16 keys of worker i's new block is produced by a merge-path
+// search over (block min(i,q), block max(i,q)) of the previous state.
+__global__ void __launch_bounds__(kMsThreads)
+    net_stage_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int p, uint32_t L, int network,
+                     int s) {
+    const uint64_t cb = (L + kNK - 1) / kNK;
+    const uint64_t items = cb * static_cast<uint64_t>(p);
+    for (uint64_t it = static_cast<uint64_t>(blockIdx.x) * kMsThreads + threadIdx.x; it < items;
+         it += static_cast<uint64_t>(gridDim.x) * kMsThreads) {
+        const int i = static_cast<int>(it / cb);
+        const uint32_t ob = static_cast<uint32_t>(it - static_cast<uint64_t>(i) * cb) * kNK;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
+        bool keep_low = false;
+        const int q = network == 0 ? btn_partner(s, i, keep_low) : oet_partner(s, i, p, keep_low);
+        uint32_t* out = dst + static_cast<uint64_t>(i) * L + ob;
+        if (q < 0) {
+            const uint32_t* in = src + static_cast<uint64_t>(i) * L + ob;
+            for (int k = 0; k < cnt; ++k) out[k] = in[k];
+            continue;
+        }
+        const int lo_w = min(i, q), hi_w = max(i, q);
+        uint32_t v[kNK];
+        merge_chunk(src + static_cast<uint64_t>(lo_w) * L, static_cast<int>(L), src + static_cast<uint64_t>(hi_w) * L,
+                    static_cast<int>(L), static_cast<int>((keep_low ? 0u : L) + ob), cnt, v);
+#pragma unroll
+        for (int k = 0; k < kNK; ++k)
+            if (k < cnt) out[k] = v[k];
+    }
+}
+
 } // namespace
+
+int launch_net_stage(const uint32_t* src, uint32_t* dst, int p, uint32_t L, int network, int s, cudaStream_t stream) {
+    const uint64_t items = ((L + kNK - 1) / kNK) * static_cast<uint64_t>(p);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((items + kMsThreads - 1) / kMsThreads, 148 * 16)));
+    TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
+    net_stage_kernel<<<grid, kMsThreads, 0, stream>>>(src, dst, p, L, network, s);
+    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
 
 int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p,
                          int run_stages, bool full, cudaStream_t stream) {

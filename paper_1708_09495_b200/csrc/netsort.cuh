@@ -15,6 +15,10 @@ constexpr uint64_t kNetMaxPadded = 16384;
 int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p,
                          int run_stages, bool full, cudaStream_t stream);
 
+// One merge-split stage of a global-memory block network (arrays larger than
+// kNetMaxPadded): src/dst hold p blocks of L keys.
+int launch_net_stage(const uint32_t* src, uint32_t* dst, int p, uint32_t L, int network, int s, cudaStream_t stream);
+
 // netsort.hpp:30-51 merge_split on device arrays.
 int launch_merge_split(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* low, uint32_t* high,
                        cudaStream_t stream);

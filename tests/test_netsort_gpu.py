@@ -96,3 +96,25 @@ def test_batched_vs_oracle(cuda, bsg, orc, length, p):
             exp, _ = orc.block_network(network, arrs[i], p)
             np.testing.assert_array_equal(got[i], exp)
         np.testing.assert_array_equal(got, np.sort(arrs, axis=1))
+
+
+@pytest.mark.parametrize("n,p", [(100000, 16), (1000000, 8), (16385, 2), (100003, 5)])
+def test_large_arrays_global_path(cuda, bsg, orc, n, p):
+    """Arrays larger than the shared-memory path (p*ceil(n/p) > 16384):
+    netsort_test.cpp:174-180 (10^5 keys, p up to 16) and acceptance sizes."""
+    keys = orc.generate_uniform_keys(n, 31 + p)
+    if (p & (p - 1)) == 0:
+        np.testing.assert_array_equal(bsg.netsort.btn_sort(bsg.SortInstance(keys, p, bsg.Algorithm.BTN)), np.sort(keys))
+    np.testing.assert_array_equal(bsg.netsort.oet_sort(bsg.SortInstance(keys, p, bsg.Algorithm.OET)), np.sort(keys))
+
+
+@pytest.mark.parametrize("network,p", [(0, 4), (0, 8), (1, 3), (1, 6)])
+def test_large_arrays_per_stage_states(cuda, bsg, orc, network, p):
+    n = 40000 - 40000 % p
+    keys = orc.generate_uniform_keys(n, 7 + p)
+    S = orc.schedule(network, p)[0].shape[0]
+    for s in range(S + 1):
+        got, st = bsg.netsort.block_network_batched(keys.reshape(1, n), p, network, s)
+        exp, est = orc.block_network(network, keys, p, s)
+        np.testing.assert_array_equal(got.reshape(-1), exp)
+        assert st == est
