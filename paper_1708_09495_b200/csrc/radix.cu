@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
             if (tile > 0 && !(dbg & 1)) {
                 int64_t t = static_cast<int64_t>(tile) - 1;
                 while (true) {
+                    if ((dbg & 8) && tid == 0) atomicAdd(&g_phase_cycles[7], 1ull);
                     uint32_t sv[LB_WIN];
 #pragma unroll
                     for (int j = 0; j < LB_WIN; ++j)

@@ -23,5 +23,6 @@ names = ["tma_wait", "rank(warp0)", "barrier_after_rank", "scan+2syncs", "stagin
 tot = sum(buf[:7])
 ctas = 148 * 3
 print(f"kernel {ms/cnt:.3f} ms/launch; cycles per CTA per launch ~ {ms/cnt*1e-3*1.95e9:.0f}")
+print(f"look-back round trips per tile (thread 0): {buf[7] / (3 * (n // 16384)):.2f}")
 for i in range(7):
     print(f"{names[i]:22s} {buf[i]/ctas:12.0f} cycles/CTA  {buf[i]/tot*100:5.1f}%")
