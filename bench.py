@@ -374,6 +374,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
     ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--distributed", action="store_true",
+                    help="run the NCCL PR path even with one rank (exercises the multi-GPU code on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))
@@ -382,7 +384,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world == 1:
+    if world == 1 and not args.distributed:
         run_single(args)
     else:
         run_multi(args, rank, world, local_rank)
