@@ -164,22 +164,27 @@ def run_reference(args, rank: int, world: int):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": _config(world),
+        "config": _config(world, None if world == 1 else "B"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": p, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def _config(world: int):
-    if world == 1:
+def _config(world: int, variant=None):
+    if world == 1 and variant is None:
         return {"workload": "config 2: single-GPU LSD radix sort (SR4: radix 2^8, 4 stable count-sort rounds) of "
                             "n=2^28 uint32 keys, generate_uniform_keys(n, derive_seed(1,0))",
                 "n": N_PER_GPU, "radix": 256, "rounds": 4, "parallelism": "single GPU",
                 "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush needed"}
-    return {"workload": f"config 5 (weak-scaled): PR4 parallel radix sort over {world} GPUs, 2^28 uint32 keys per GPU "
-                        f"(n={N_PER_GPU * world}), per round digit count + NCCL all-gather of counts + NCCL "
-                        f"all-to-all-v of keys + rebuild",
+    if variant == "A":
+        what = ("PR4 as run_parallel_radix: per round digit count + NCCL all-gather of counts + NCCL all-to-all-v "
+                "of keys + rebuild (4 exchanges; per-round states bit-identical to the reference)")
+    else:
+        what = ("variant B: top-digit histogram + NCCL all-gather of counts + one stable partition pass + ONE NCCL "
+                "all-to-all-v + local LSD sort (BASELINE config-5 formulation; same sorted concatenation)")
+    return {"workload": f"config 5 (weak-scaled) over {world} GPUs, 2^28 uint32 keys per GPU (n={N_PER_GPU * world}): "
+                        + what, "variant": variant,
             "n": N_PER_GPU * world, "n_per_gpu": N_PER_GPU, "radix": 256, "rounds": 4, "parallelism": f"dp{world}",
             "l2": "inputs larger than L2; no flush needed"}
 
@@ -292,7 +297,9 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     ctx = _lib.context(local_rank)
 
     def step(events=None):
-        return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events)
+        if args.pr_variant == "A":
+            return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events)
+        return D.parallel_radix_sort_single_exchange(d_in, a2a_events=events)
 
     for _ in range(args.warmup):
         out = step()
@@ -319,10 +326,11 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     # verification (untimed): local sortedness, boundaries, global checksum
     o64 = out.to(torch.int64) & 0xFFFFFFFF
     local_ok = bool((o64[1:] >= o64[:-1]).all()) if o64.numel() > 1 else True
-    ends = torch.tensor([o64[0].item(), o64[-1].item()], dtype=torch.int64, device=dev)
+    ends = torch.tensor([o64[0].item(), o64[-1].item()] if o64.numel() else [-1, -1], dtype=torch.int64, device=dev)
     allends = [torch.empty_like(ends) for _ in range(world)]
     dist.all_gather(allends, ends)
-    bounds_ok = all(allends[w][1].item() <= allends[w + 1][0].item() for w in range(world - 1))
+    nonempty = [e for e in allends if e[0].item() >= 0]
+    bounds_ok = all(nonempty[w][1].item() <= nonempty[w + 1][0].item() for w in range(len(nonempty) - 1))
     cs = torch.tensor([(d_in.to(torch.int64) & 0xFFFFFFFF).sum().item(), o64.sum().item(), int(local_ok)],
                       dtype=torch.float64, device=dev)
     dist.all_reduce(cs)
@@ -334,8 +342,11 @@ def run_multi(args, rank: int, world: int, local_rank: int):
 
     def e2e_step():
         blk = h_in.to(dev, non_blocking=True)
-        res = D.parallel_radix_sort(blk, n_total, radix=256)
-        h_out.copy_(res, non_blocking=True)
+        if args.pr_variant == "A":
+            res = D.parallel_radix_sort(blk, n_total, radix=256)
+        else:
+            res = D.parallel_radix_sort_single_exchange(blk)
+        h_out[: res.numel()].copy_(res, non_blocking=True)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -354,7 +365,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": n_total / (ms_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference generator, seeded per rank)",
-            "config": _config(world),
+            "config": _config(world, args.pr_variant),
             "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_total,
                     "d2h_bytes_per_step": 4 * n_total, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
@@ -374,6 +385,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
     ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pr-variant", choices=["A", "B"], default="B",
+                    help="multi-GPU algorithm: A = per-round PR4 (4 exchanges), B = single exchange")
     ap.add_argument("--distributed", action="store_true",
                     help="run the NCCL PR path even with one rank (exercises the multi-GPU code on one GPU)")
     args = ap.parse_args()

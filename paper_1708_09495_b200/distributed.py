@@ -16,6 +16,9 @@ The block a rank holds after round k is bit-identical to worker `rank`'s
 block in run_parallel_radix with plan.rounds = k.  The only host round trip
 per round is the 2p split sizes NCCL's all-to-all-v needs on the host.
 
+`parallel_radix_sort_single_exchange` is variant B of SURVEY §8(e) (the
+BASELINE config-5 formulation: one exchange, then a local sort).
+
 The step operations are injectable (``ops``) so the host orchestration can
 be exercised on CPU under gloo in tests; the product default is
 :class:`CudaStepOps`, which fails loudly without libbsg.so / a GPU.
@@ -74,6 +77,13 @@ class CudaStepOps:
         host = sr.cpu().tolist()  # the one host round trip per round: split sizes
         return host[:p], host[p:], sr[p:], delta
 
+    def sort(self, keys: torch.Tensor) -> torch.Tensor:
+        """Full LSD sort (serial_radix_sort) of a device block."""
+        out = torch.empty_like(keys)
+        _lib.check(self.L.bsg_radix_sort_u32(self.ctx.handle, keys.data_ptr(), out.data_ptr(), keys.numel(), 8,
+                                             _lib.MEM_DEVICE, self._stream()), "local sort")
+        return out
+
     def rebuild(self, recv: torch.Tensor, recv_counts_dev: torch.Tensor, p: int, rnd: int, bits: int,
                 delta: torch.Tensor, out_len: int) -> torch.Tensor:
         block = torch.empty(out_len, dtype=torch.int32, device=self.device)
@@ -119,3 +129,58 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
             a2a_events.append((e0, e1))
         block = ops.rebuild(recv_buf, recv_dev, p, rnd, bits, delta, partition_size_of(n_total, p, me))
     return block
+
+
+def digit_cuts(global_counts, p: int):
+    """Balanced cut points at top-digit boundaries: rank w receives the keys
+    whose top digit lies in [cuts[w], cuts[w+1]).  Deterministic on every rank
+    (computed from the same all-gathered counts)."""
+    total = int(sum(global_counts))
+    cuts = [0]
+    run = 0
+    d = 0
+    r = len(global_counts)
+    for w in range(1, p):
+        target = (total * w + p - 1) // p  # ceil(total*w/p): first w ranks hold >= w/p of the keys
+        while d < r and run < target:
+            run += int(global_counts[d])
+            d += 1
+        cuts.append(d)
+    cuts.append(r)
+    return cuts
+
+
+def parallel_radix_sort_single_exchange(block: torch.Tensor, group=None, ops=None,
+                                        a2a_events: Optional[list] = None) -> torch.Tensor:
+    """Variant B: the BASELINE config-5 formulation -- local
+    histogram of the top 8-bit digit, all-gather of the count vectors, one
+    stable local partition by that digit (count_sort_round round 3, r=2^8),
+    ONE all-to-all-v over NVLink, then a full local LSD sort of the received
+    keys.  Cuts fall on digit boundaries, so per-rank sizes vary by at most one
+    bucket; the concatenation of the ranks' outputs in rank order is the sorted
+    array (identical to run_parallel_radix's output).  Returns this rank's
+    sorted keys (int32 bit patterns)."""
+    p = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    if block.dtype == torch.uint32:
+        block = block.view(torch.int32)
+    if ops is None:
+        ops = CudaStepOps(block.device)
+    counts = ops.count(block, 3, 8)                                   # top digit, r = 2^8
+    counts_all = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
+    dist.all_gather_into_tensor(counts_all, counts, group=group)
+    cm = counts_all.view(p, -1).cpu()                                 # p x 256 (2 KiB per rank)
+    cuts = digit_cuts(cm.sum(0).tolist(), p)
+    part = ops.local_sort(block, 3, 8)                                # stable partition by the top digit
+    mine = cm[me]
+    send = [int(mine[cuts[w]:cuts[w + 1]].sum()) for w in range(p)]
+    recv = [int(cm[v, cuts[me]:cuts[me + 1]].sum()) for v in range(p)]
+    recv_buf = ops.keys(sum(recv))
+    if a2a_events is not None and block.is_cuda:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    dist.all_to_all_single(recv_buf, part, output_split_sizes=recv, input_split_sizes=send, group=group)
+    if a2a_events is not None and block.is_cuda:
+        e1.record()
+        a2a_events.append((e0, e1))
+    return ops.sort(recv_buf)

@@ -45,6 +45,9 @@ class HostOps:
         assert rc == 0
         return [int(x) for x in send], [int(x) for x in recv], recv, delta
 
+    def sort(self, keys):
+        return torch.from_numpy(np.sort(keys.numpy().view(np.uint32)).view(np.int32))
+
     def rebuild(self, recv, recv_counts, p, rnd, bits, delta, out_len):
         k = recv.numpy().view(np.uint32)
         src = np.repeat(np.arange(p), recv_counts.astype(np.int64))
@@ -115,3 +118,60 @@ def test_gloo_pr_matches_reference_rounds(world, orc):
         exp, _ = orc.parallel_radix(keys, world, radix, rounds)
         got = np.concatenate([out[r][ci] for r in range(world)])
         np.testing.assert_array_equal(got, exp, err_msg=f"case {ci} radix={radix} rounds={rounds}")
+
+
+def _worker_b(rank, world, port, cases, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1708_09495_b200 import distributed as D
+
+        ops = HostOps()
+        res = []
+        for keys in cases:
+            n = keys.size
+            off = D.partition_offset_of(n, world, rank)
+            sz = D.partition_size_of(n, world, rank)
+            blk = torch.from_numpy(keys[off:off + sz].view(np.int32).copy())
+            out = D.parallel_radix_sort_single_exchange(blk, ops=ops)
+            res.append(out.numpy().view(np.uint32).copy())
+        q.put((rank, res, None))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_single_exchange_variant(world, orc):
+    cases = [orc.generate_uniform_keys(40001, 3), orc.generate_uniform_keys(20000, 4) % 7,
+             np.array([5, 1, 4], np.uint32), np.array([], np.uint32)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_b, args=(r, world, port, cases, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(world):
+        rank, res, err = q.get(timeout=300)
+        assert err is None, err
+        out[rank] = res
+    for pr in procs:
+        pr.join(timeout=60)
+    for ci, keys in enumerate(cases):
+        got = np.concatenate([out[r][ci] for r in range(world)])
+        np.testing.assert_array_equal(got, np.sort(keys))
+        sizes = [out[r][ci].size for r in range(world)]
+        assert max(sizes) - min(sizes) <= 2 * int(np.bincount(keys >> 24, minlength=256).max()) + 1
+
+
+def test_digit_cuts_balanced():
+    from paper_1708_09495_b200.distributed import digit_cuts
+
+    assert digit_cuts([10] * 256, 4) == [0, 64, 128, 192, 256]
+    assert digit_cuts([0] * 256, 3)[0] == 0 and digit_cuts([0] * 256, 3)[-1] == 256
+    c = digit_cuts([1000] + [0] * 255, 2)
+    assert c[0] == 0 and c[-1] == 256

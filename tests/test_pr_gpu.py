@@ -100,6 +100,9 @@ def test_distributed_nccl_world1(cuda, bsg, orc):
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         keys = orc.generate_uniform_keys(100003, 9)
+        blk = torch.from_numpy(keys.view(np.int32)).cuda()
+        out = D.parallel_radix_sort_single_exchange(blk)
+        np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
         for radix in (256, 65536):
             for rounds in (1, None):
                 blk = torch.from_numpy(keys.view(np.int32)).cuda()
