@@ -19,10 +19,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 ms, cnt = ctx.kernel_time(_lib.K_ONESWEEP)
 L.bsg_debug_phase_cycles(buf, 1)
-names = ["tma_wait", "rank(warp0)", "barrier_after_rank", "scan+2syncs", "staging(warp0)", "lookback+sync", "write(warp0)", "-"]
-tot = sum(buf[:7])
+names = ["tma_wait", "rank(warp0)", "barrier_after_rank", "scan+2syncs", "staging(warp0)", "lookback(warp0)", "write(warp0)", "barrier_after_lookback"]
+tot = sum(buf[:8])
 ctas = 148 * 3
 print(f"kernel {ms/cnt:.3f} ms/launch; cycles per CTA per launch ~ {ms/cnt*1e-3*1.95e9:.0f}")
-print(f"look-back round trips per tile (thread 0): {buf[7] / (3 * (n // 16384)):.2f}")
-for i in range(7):
+for i in range(8):
     print(f"{names[i]:22s} {buf[i]/ctas:12.0f} cycles/CTA  {buf[i]/tot*100:5.1f}%")
