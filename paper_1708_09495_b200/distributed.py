@@ -184,3 +184,61 @@ def parallel_radix_sort_single_exchange(block: torch.Tensor, group=None, ops=Non
         e1.record()
         a2a_events.append((e0, e1))
     return ops.sort(recv_buf)
+
+
+def network_schedule(network: int, p: int):
+    """(partner, keep_low) per stage for this p (netsort.hpp:70-108)."""
+    S = ctypes.c_int(0)
+    L = _lib.lib()
+    _lib.check(L.bsg_network_schedule(network, p, None, None, 0, ctypes.byref(S)), "schedule")
+    import numpy as np
+
+    partner = np.empty(max(1, S.value * p), dtype=np.int32)
+    keep = np.empty(max(1, S.value * p), dtype=np.int32)
+    _lib.check(L.bsg_network_schedule(network, p, partner.ctypes.data, keep.ctypes.data, S.value, ctypes.byref(S)),
+               "schedule")
+    return [[(int(partner[s * p + i]), bool(keep[s * p + i])) for i in range(p)] for s in range(S.value)]
+
+
+class CudaNetworkOps(CudaStepOps):
+    """merge_split on device blocks (netsort.hpp:30-51)."""
+
+    def merge_keep(self, mine: torch.Tensor, theirs: torch.Tensor, keep_low: bool) -> torch.Tensor:
+        low = torch.empty_like(mine)
+        high = torch.empty_like(theirs)
+        _lib.check(self.L.bsg_merge_split_u32(self.ctx.handle, mine.data_ptr(), mine.numel(), theirs.data_ptr(),
+                                              theirs.numel(), low.data_ptr(), high.data_ptr(), _lib.MEM_DEVICE,
+                                              self._stream()), "merge_split")
+        return low if keep_low else high
+
+
+def block_network_sort(block: torch.Tensor, network: int = 0, stages: Optional[int] = None, group=None,
+                       ops=None) -> torch.Tensor:
+    """The paper's p-processor BTN (network 0) / OET (network 1) across ranks
+    (netsort.hpp:157-199 with one worker per GPU): the rank's
+    block (equal sizes on every rank, padded by the caller with 0xFFFFFFFF as
+    prepare_blocks does, netsort.hpp:124-141) is sorted locally, then every
+    stage swaps whole blocks with the stage partner over NCCL and keeps the low
+    or high half of the merge (merge_split).  `stages` < S stops early.
+    Returns the rank's final block; the blocks in rank order are sorted."""
+    p = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    if block.dtype == torch.uint32:
+        block = block.view(torch.int32)
+    if ops is None:
+        ops = CudaNetworkOps(block.device)
+    sched = network_schedule(network, p)
+    run = len(sched) if stages is None else max(0, min(int(stages), len(sched)))
+    state = ops.sort(block)                       # superstep 0: local sort (netsort.hpp:167)
+    for s in range(run):
+        q, keep_low = sched[s][me]
+        if q < 0:                                 # idle OET edge worker
+            continue
+        other = torch.empty_like(state)
+        if p > 1:
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, state, q, group),
+                                           dist.P2POp(dist.irecv, other, q, group)])
+            for r in reqs:
+                r.wait()
+        state = ops.merge_keep(state, other, keep_low)
+    return state

@@ -48,6 +48,10 @@ class HostOps:
     def sort(self, keys):
         return torch.from_numpy(np.sort(keys.numpy().view(np.uint32)).view(np.int32))
 
+    def merge_keep(self, mine, theirs, keep_low):
+        lo, hi = self.orc.merge_split(mine.numpy().view(np.uint32), theirs.numpy().view(np.uint32))
+        return torch.from_numpy((lo if keep_low else hi).view(np.int32).copy())
+
     def rebuild(self, recv, recv_counts, p, rnd, bits, delta, out_len):
         k = recv.numpy().view(np.uint32)
         src = np.repeat(np.arange(p), recv_counts.astype(np.int64))
@@ -175,3 +179,54 @@ def test_digit_cuts_balanced():
     assert digit_cuts([0] * 256, 3)[0] == 0 and digit_cuts([0] * 256, 3)[-1] == 256
     c = digit_cuts([1000] + [0] * 255, 2)
     assert c[0] == 0 and c[-1] == 256
+
+
+def _worker_net(rank, world, port, cases, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1708_09495_b200 import distributed as D
+
+        ops = HostOps()
+        res = []
+        for keys, network, stages in cases:
+            L = keys.size // world
+            blk = torch.from_numpy(keys[rank * L:(rank + 1) * L].view(np.int32).copy())
+            out = D.block_network_sort(blk, network, stages, ops=ops)
+            res.append(out.numpy().view(np.uint32).copy())
+        q.put((rank, res, None))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,networks", [(2, (0, 1)), (3, (1,)), (4, (0, 1))])
+def test_gloo_block_networks_match_reference_stages(world, networks, orc):
+    """BTN/OET with one worker per rank; after every stage the
+    rank-ordered blocks equal run_block_network's block states."""
+    keys = orc.generate_uniform_keys(1200, 11)
+    cases = []
+    for network in networks:
+        S = orc.schedule(network, world)[0].shape[0]
+        for stages in range(S + 1):
+            cases.append((keys, network, stages))
+    ctx = mp.get_context("spawn")
+    qq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_net, args=(r, world, port, cases, qq)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(world):
+        rank, res, err = qq.get(timeout=300)
+        assert err is None, err
+        out[rank] = res
+    for pr in procs:
+        pr.join(timeout=60)
+    for ci, (k, network, stages) in enumerate(cases):
+        exp, _ = orc.block_network(network, k, world, stages)
+        got = np.concatenate([out[r][ci] for r in range(world)])
+        np.testing.assert_array_equal(got, exp, err_msg=f"network {network} stages {stages}")

@@ -103,6 +103,12 @@ def test_distributed_nccl_world1(cuda, bsg, orc):
         blk = torch.from_numpy(keys.view(np.int32)).cuda()
         out = D.parallel_radix_sort_single_exchange(blk)
         np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
+        # SURVEY §8(f)1 block network with one worker per rank (p = 1 here:
+        # local sort only, zero stages)
+        for network in (0, 1):
+            blk = torch.from_numpy(keys[:4096].view(np.int32)).cuda()
+            out = D.block_network_sort(blk, network)
+            np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys[:4096]))
         for radix in (256, 65536):
             for rounds in (1, None):
                 blk = torch.from_numpy(keys.view(np.int32)).cuda()
