@@ -257,10 +257,11 @@ struct OnesweepSmem {
     static constexpr int RADIX = 1 << BITS;
     static constexpr int WARPS = THREADS / 32;
     static constexpr int TILE = THREADS * ITEMS;
+    static_assert(TILE <= 65536, "16-bit tile offsets");
     using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
     static constexpr size_t in_off = 0;                                          // 2 x TILE u32
-    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // WARPS*RADIX u32
-    static constexpr size_t delta_off = wcnt_off + sizeof(uint32_t) * WARPS * RADIX; // RADIX Off
+    static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // WARPS*RADIX u16
+    static constexpr size_t delta_off = wcnt_off + sizeof(uint16_t) * WARPS * RADIX; // RADIX Off
     static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
     static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
     static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // 2 tile ids
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     static_assert(RADIX <= THREADS, "one thread per digit");
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
-    uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + L::wcnt_off);
+    uint16_t* s_wcnt = reinterpret_cast<uint16_t*>(smem + L::wcnt_off); // tile offsets < 2^16
     Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
     uint32_t* s_excl = reinterpret_cast<uint32_t*>(smem + L::excl_off);
     uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         s_tile[0] = t0;
         issue(t0, 0);
     }
-    for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
+    for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
 
     const uint32_t lt = lanemask_lt();
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
@@ -354,12 +355,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         // Warp w owns keys [w*32*ITEMS, (w+1)*32*ITEMS); item i of lane l is
         // key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
         const uint32_t wbase = warp * (32 * ITEMS);
-        uint32_t* wc = s_wcnt + warp * RADIX;
+        uint16_t* wc = s_wcnt + warp * RADIX;
         uint32_t keys[ITEMS];
         uint32_t packed[ITEMS / 2];
         auto rank_items = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
-            uint32_t peers[ITEMS];
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
@@ -369,34 +369,40 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                     keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
                 }
             }
-            // all match-any / ballot masks first: independent, latencies overlap
+            // multisplit masks in batches of PB items (independent inside a
+            // batch), then the per-warp running counts of the batch, item by
+            // item (input order): every peer reads the same counter (a
+            // broadcast), the highest peer alone stores the advanced count.
+            constexpr int PB = ITEMS % 8 == 0 ? 8 : ITEMS;
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const uint32_t idx = wbase + i * 32 + lane;
-                const bool ok = FULL || idx < valid;
-                const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
-                                      : static_cast<uint32_t>(RADIX);
-                if (dbg & 2) peers[i] = 1u << lane;
-                else if (RANK == 1)
-                    peers[i] = __match_any_sync(0xffffffffu, d);
-                else
-                    peers[i] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
-            }
-            // then the per-warp running counts, item by item (input order):
-            // every peer reads the same counter (a broadcast), the highest
-            // peer alone stores the advanced count.
+            for (int i0 = 0; i0 < ITEMS; i0 += PB) {
+                uint32_t peers[PB];
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const uint32_t idx = wbase + i * 32 + lane;
-                const bool ok = FULL || idx < valid;
-                const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)) : 0u;
-                const uint32_t before = ok ? wc[d] : 0u;
-                const bool leader = (31 - __clz(peers[i])) == lane;
-                if (leader && ok) wc[d] = before + __popc(peers[i]);
-                const uint32_t r = before + __popc(peers[i] & lt);
-                __syncwarp();
-                if (i & 1) packed[i >> 1] = __byte_perm(packed[i >> 1], r, 0x5410);
-                else packed[i >> 1] = r;
+                for (int ii = 0; ii < PB; ++ii) {
+                    const int i = i0 + ii;
+                    const uint32_t idx = wbase + i * 32 + lane;
+                    const bool ok = FULL || idx < valid;
+                    const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
+                                          : static_cast<uint32_t>(RADIX);
+                    if (dbg & 2) peers[ii] = 1u << lane;
+                    else if (RANK == 1) peers[ii] = __match_any_sync(0xffffffffu, d);
+                    else peers[ii] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
+                }
+#pragma unroll
+                for (int ii = 0; ii < PB; ++ii) {
+                    const int i = i0 + ii;
+                    const uint32_t idx = wbase + i * 32 + lane;
+                    const bool ok = FULL || idx < valid;
+                    const uint32_t d =
+                        ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)) : 0u;
+                    const uint32_t before = ok ? wc[d] : 0u;
+                    const bool leader = (31 - __clz(peers[ii])) == lane;
+                    if (leader && ok) wc[d] = static_cast<uint16_t>(before + __popc(peers[ii]));
+                    const uint32_t r = before + __popc(peers[ii] & lt);
+                    __syncwarp();
+                    if (i & 1) packed[i >> 1] = __byte_perm(packed[i >> 1], r, 0x5410);
+                    else packed[i >> 1] = r;
+                }
             }
         };
         if (full) rank_items(std::true_type{});
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 #pragma unroll
             for (int w = 0; w < WARPS; ++w) {
                 const uint32_t c = s_wcnt[w * RADIX + tid];
-                s_wcnt[w * RADIX + tid] = tile_cnt;
+                s_wcnt[w * RADIX + tid] = static_cast<uint16_t>(tile_cnt);
                 tile_cnt += c;
             }
             st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 if (w < warp) excl += s_scan[w];
             s_excl[tid] = excl;
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] += excl;
+            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] = static_cast<uint16_t>(s_wcnt[w * RADIX + tid] + excl);
 
         }
         __syncthreads();
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 
         phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
-        for (int i = tid; i < WARPS * RADIX; i += THREADS) s_wcnt[i] = 0;
+        for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
         if (full) {
 #pragma unroll 4
             for (int j = 0; j < ITEMS; ++j) {
@@ -509,13 +515,16 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 
 constexpr int kMinTile = 4096;
 
-inline int onesweep_cfg() {
+// 0 = auto by n; otherwise a fixed THREADS x ITEMS row (see launch_onesweep_pass).
+// Initialised from BSG_OS_CFG; bsg_debug_set_onesweep_cfg overrides it (tests).
+inline int& onesweep_cfg_ref() {
     static int cfg = [] {
         const char* e = getenv("BSG_OS_CFG");
         return e ? atoi(e) : 0;
     }();
     return cfg;
 }
+inline int onesweep_cfg() { return onesweep_cfg_ref(); }
 inline int onesweep_dbg() {
     static int d = [] {
         const char* e = getenv("BSG_OS_DBG");
@@ -595,20 +604,34 @@ template <int BITS>
 int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                          int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
     const bool wide = n > 0xFFFFFFFFull;
-    if (wide)
-        return launch_onesweep_cfg<BITS, 1024, 16, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+    if (wide) // n > 2^32: 24-key rows, the large-n configuration
+        return launch_onesweep_cfg<BITS, 1024, 24, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                         stream, use_tma);
     if constexpr (BITS != 8)
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     int cfg = onesweep_cfg();
-    if (cfg == 0) cfg = n <= (uint64_t{1} << 21) ? 3 : (n <= (uint64_t{1} << 24) ? 1 : 2);
+    // measured on B200 (profiles/r01_onesweep_cfg_sweep.txt): 512x16 up to
+    // 2^21 keys, 1024x16 up to 2^23, 1024x24 (24576-key tiles) beyond
+    if (cfg == 0) cfg = n <= (uint64_t{1} << 21) ? 1 : (n <= (uint64_t{1} << 23) ? 2 : 4);
     switch (cfg) {
     case 3: // 256 x 16: 4096-key tiles so small inputs still fill 148 SMs
         return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     case 1:
         return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    case 4:
+        return launch_onesweep_cfg<BITS, 1024, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                          stream, use_tma);
+    case 5:
+        return launch_onesweep_cfg<BITS, 1024, 20, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                          stream, use_tma);
+    case 6:
+        return launch_onesweep_cfg<BITS, 512, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    case 7:
+        return launch_onesweep_cfg<BITS, 256, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     default: // 1024 threads x 16 keys: 16384-key tiles, one CTA per SM
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
@@ -748,6 +771,14 @@ int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uin
 }
 
 } // namespace bsg
+
+// Test aid: pins the one-sweep configuration (0 = auto, 1..7 fixed rows) so
+// parity tests cover every instantiation; returns the previous value.
+extern "C" int bsg_debug_set_onesweep_cfg(int cfg) {
+    const int prev = bsg::onesweep_cfg_ref();
+    bsg::onesweep_cfg_ref() = cfg;
+    return prev;
+}
 
 // Development aid: reads (and optionally clears) the one-sweep phase-cycle
 // accumulators filled when BSG_OS_DBG has bit 8 set.

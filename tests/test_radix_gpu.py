@@ -160,3 +160,29 @@ def test_unaligned_device_pointers(cuda, bsg, orc, offset):
     assert L.bsg_radix_sort_u32(ctx.handle, sub.data_ptr(), out.data_ptr(), n, 8, 1, st) == 0
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys[offset:]))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
+def test_every_onesweep_configuration(cuda, bsg, orc, cfg):
+    """Each THREADS x ITEMS instantiation (auto picks by n) against the oracle,
+    on ragged sizes around its tile: partial last tiles, single tiles, ties."""
+    L = bsg._lib.lib()
+    prev = L.bsg_debug_set_onesweep_cfg(cfg)
+    try:
+        for n in (1, 4095, 4097, 24577, 3 * 24576 + 7, 1000003):
+            keys = orc.generate_uniform_keys(n, 31 + n + cfg)
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), orc.serial_radix_sort(keys, 256))
+            for rnd in (0, 3):
+                np.testing.assert_array_equal(bsg.radix.count_sort_round(keys, rnd, 256),
+                                              orc.count_sort_round(keys, rnd, 256))
+        narrow = (orc.generate_uniform_keys(200003, 5) & 0x0F0F).astype(np.uint32)  # heavy ties
+        np.testing.assert_array_equal(bsg.radix.serial_radix_sort(narrow, 256), orc.serial_radix_sort(narrow, 256))
+    finally:
+        L.bsg_debug_set_onesweep_cfg(prev)
+
+
+def test_auto_configuration_boundaries(cuda, bsg, orc):
+    """Sizes either side of the auto-selection thresholds (2^21, 2^23)."""
+    for n in ((1 << 21), (1 << 21) + 1, (1 << 23) + 1):
+        keys = orc.generate_uniform_keys(n, n)
+        np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), orc.serial_radix_sort(keys, 256))
