@@ -396,7 +396,10 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
     if (p < 1 || me < 0 || me >= p) return fail(BSG_EINVAL, "pr_plan: worker index out of range");
     (void)round;
     CallGuard g(ctx);
-    cudaError_t e = ctx->pr_recv.ensure(static_cast<uint64_t>(p) * sizeof(uint64_t));
+    // scratch for launch_pr_plan: split[p], coltot[r], dstart[r], colchunk[r/1024], rowchunk[p][r/1024]
+    const uint64_t chunks = ((uint64_t{1} << radix_log2) + 1023) / 1024;
+    cudaError_t e = ctx->pr_recv.ensure(
+        (static_cast<uint64_t>(p) * (1 + chunks) + (uint64_t{2} << radix_log2) + chunks) * sizeof(uint64_t));
     if (e != cudaSuccess) return cuda_fail(e, "pr_plan scratch");
     const int l = launch_pr_plan(counts, n, p, me, radix_log2, send_counts, recv_counts, rebuild_delta,
                                  static_cast<cudaStream_t>(stream), ctx->pr_recv.as<uint64_t>());

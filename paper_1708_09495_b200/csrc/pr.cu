@@ -14,10 +14,12 @@
 //   rebuild -- gather_slices (radix.hpp:295-333): walking (digit, source) in
 //              order is a stable digit scatter of the source-major receive
 //              buffer, block[delta[v][d] + j] = recv[j].
-// In-process (p logical workers on one GPU) the exchange is fused into the
-// rebuild: it reads each source's slice straight from that source's sorted
-// block.  Across GPUs, paper_1708_09495_b200/distributed.py interleaves the
-// same steps with NCCL all-gather / all-to-all-v.
+// In-process (p logical workers on one GPU, run_parallel_radix_local) the
+// count matrix is read off the sorted blocks (run starts), the routing is
+// O(p r) table work, and the exchange + rebuild of all workers is a single
+// scatter of the sorted blocks.  Across GPUs,
+// paper_1708_09495_b200/distributed.py interleaves the count / plan / local /
+// rebuild steps with NCCL all-gather / all-to-all-v.
 #include <algorithm>
 #include <vector>
 
@@ -49,88 +51,6 @@ __device__ __forceinline__ int part_owner(uint64_t n, int p, uint64_t pos) {
 __device__ __forceinline__ uint64_t overlap(uint64_t a0, uint64_t a1, uint64_t b0, uint64_t b1) {
     const uint64_t lo = a0 > b0 ? a0 : b0, hi = a1 < b1 ? a1 : b1;
     return hi > lo ? hi - lo : 0;
-}
-
-// Block-wide exclusive scan of one uint64 per thread; returns the block total.
-__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t& excl, uint64_t* s_warp) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t incl = warp_inclusive_scan(v);
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    uint64_t pre = 0, total = 0;
-    for (int w = 0; w < kPlanThreads / 32; ++w) {
-        if (w < warp) pre += s_warp[w];
-        total += s_warp[w];
-    }
-    excl = pre + incl - v;
-    __syncthreads();
-    return total;
-}
-
-__global__ void __launch_bounds__(kPlanThreads)
-    pr_plan1_kernel(const uint64_t* __restrict__ counts, uint64_t n, int p, int me, int radix,
-                    uint64_t* __restrict__ send_counts, uint64_t* __restrict__ recv_counts,
-                    int64_t* __restrict__ delta, uint64_t* __restrict__ split) {
-    extern __shared__ uint64_t s_send[]; // p entries
-    __shared__ uint64_t s_warp[kPlanThreads / 32];
-    __shared__ uint64_t s_red[2][kPlanThreads / 32];
-    const int v = blockIdx.x;
-    const int tid = threadIdx.x;
-    if (v == me)
-        for (int w = tid; w < p; w += kPlanThreads) s_send[w] = 0;
-    __syncthreads();
-    const uint64_t lo_me = part_offset(n, p, me), hi_me = lo_me + part_size(n, p, me);
-    uint64_t run_start = 0, run_local = 0, acc_recv = 0, acc_split = 0;
-    for (int d0 = 0; d0 < radix; d0 += kPlanThreads) {
-        const int d = d0 + tid;
-        uint64_t col = 0, before = 0, cv = 0;
-        if (d < radix) {
-            for (int u = 0; u < p; ++u) {
-                const uint64_t c = counts[static_cast<uint64_t>(u) * radix + d];
-                col += c;
-                if (u < v) before += c;
-                if (u == v) cv = c;
-            }
-        }
-        uint64_t ex_col, ex_cv;
-        const uint64_t tot_col = block_excl_scan(col, ex_col, s_warp);
-        const uint64_t tot_cv = block_excl_scan(cv, ex_cv, s_warp);
-        if (d < radix) {
-            const uint64_t np = run_start + ex_col + before; // next_pos[d] of worker v
-            const uint64_t ls = run_local + ex_cv;           // local start of digit d in v's sorted block
-            acc_recv += overlap(np, np + cv, lo_me, hi_me);
-            acc_split += overlap(np, np + cv, 0, lo_me);
-            delta[static_cast<uint64_t>(v) * radix + d] = static_cast<int64_t>(np) - static_cast<int64_t>(ls);
-            if (v == me && cv) {
-                const int w0 = part_owner(n, p, np), w1 = part_owner(n, p, np + cv - 1);
-                for (int w = w0; w <= w1; ++w) {
-                    const uint64_t lo = part_offset(n, p, w);
-                    const uint64_t o = overlap(np, np + cv, lo, lo + part_size(n, p, w));
-                    if (o) atomicAdd(reinterpret_cast<unsigned long long*>(&s_send[w]), static_cast<unsigned long long>(o));
-                }
-            }
-        }
-        run_start += tot_col;
-        run_local += tot_cv;
-    }
-    // block reductions of acc_recv / acc_split
-    const uint64_t r1 = warp_sum(acc_recv), r2 = warp_sum(acc_split);
-    if ((tid & 31) == 0) {
-        s_red[0][tid >> 5] = r1;
-        s_red[1][tid >> 5] = r2;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        uint64_t a = 0, b = 0;
-        for (int w = 0; w < kPlanThreads / 32; ++w) {
-            a += s_red[0][w];
-            b += s_red[1][w];
-        }
-        recv_counts[v] = a;
-        split[v] = b;
-    }
-    if (v == me)
-        for (int w = tid; w < p; w += kPlanThreads) send_counts[w] = s_send[w];
 }
 
 __global__ void __launch_bounds__(kPlanThreads)
@@ -177,11 +97,6 @@ __global__ void __launch_bounds__(kRebuildThreads)
     }
 }
 
-__global__ void pr_src_ptrs_kernel(const uint32_t* sorted, uint64_t n, int p, const uint64_t* __restrict__ split,
-                                   const uint32_t** out_ptrs) {
-    for (int v = threadIdx.x; v < p; v += blockDim.x) out_ptrs[v] = sorted + part_offset(n, p, v) + split[v];
-}
-
 // 16-bit digit histogram: 65536 16-bit counters packed in 128 KiB of shared
 // memory; a counter that reaches 2^15 carries 2^15 to the global uint64 bin.
 constexpr int kHist16Threads = 1024;
@@ -206,6 +121,240 @@ __global__ void __launch_bounds__(kHist16Threads)
         const uint32_t c = (h16[d >> 1] >> ((d & 1) * 16)) & 0xFFFFu;
         if (c) atomicAdd(&counts[d], static_cast<unsigned long long>(c));
     }
+}
+
+// ---- in-process round (p logical workers on one GPU) ----------------------
+// The rebuild of every worker together is one scatter of the locally sorted
+// blocks: key i of worker v's sorted block with digit d lands at
+//   np(v,d) + (i - ls(v,d)),  np(v,d) = start[d] + sum_{u<v} cnt(u,d)
+// (radix.hpp:257-290 next_pos / gather order), ls(v,d) = first index of d in
+// v's sorted block.  All tables are O(p r) work.
+
+// ls(v,d) for d in [0, r]: lower bound of digit d in v's sorted block (the
+// block's digit counts are ls(v,d+1) - ls(v,d), as count_digits would give).
+__global__ void pr_run_starts_kernel(const uint32_t* __restrict__ sorted, uint64_t n, int p, int shift,
+                                     uint32_t mask, int radix, uint64_t* __restrict__ starts) {
+    const int v = blockIdx.y;
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d > static_cast<uint32_t>(radix)) return;
+    const uint64_t off = part_offset(n, p, v), len = part_size(n, p, v);
+    const uint32_t* blk = sorted + off;
+    uint64_t lo = 0, hi = len;
+    if (d == static_cast<uint32_t>(radix)) lo = len;
+    else
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (((__ldg(blk + mid) >> shift) & mask) < d) lo = mid + 1;
+            else hi = mid;
+        }
+    starts[static_cast<uint64_t>(v) * (radix + 1) + d] = lo;
+}
+
+// Digit tables are processed in chunks of kDigChunk digits, one CTA each
+// (coalesced, no single-CTA loops over r).
+constexpr int kDigChunk = 1024;
+
+// Block-wide exclusive scan (kDigChunk threads); returns the block total.
+__device__ __forceinline__ uint64_t chunk_excl_scan(uint64_t v, uint64_t& excl) {
+    __shared__ uint64_t s_warp[kDigChunk / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t incl = warp_inclusive_scan(v);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t pre = 0, total = 0;
+    for (int w = 0; w < kDigChunk / 32; ++w) {
+        const uint64_t x = s_warp[w];
+        pre += w < warp ? x : 0;
+        total += x;
+    }
+    excl = pre + incl - v;
+    __syncthreads();
+    return total;
+}
+
+// Sum of tab[0 .. k) computed by warp 0 and broadcast (k <= a few hundred).
+__device__ __forceinline__ uint64_t chunk_base(const uint64_t* tab, int k) {
+    __shared__ uint64_t s_base;
+    if (threadIdx.x < 32) {
+        uint64_t acc = 0;
+        for (int i = threadIdx.x; i < k; i += 32) acc += tab[i];
+        acc = warp_sum(acc);
+        if (threadIdx.x == 0) s_base = acc;
+    }
+    __syncthreads();
+    return s_base;
+}
+
+// Column prefix over workers from the run starts: gd[v][d] = sum_{u<v}
+// cnt(u,d) - ls(v,d); coltot[d] = sum_u cnt(u,d); colchunk[c] = chunk sums.
+__global__ void __launch_bounds__(kDigChunk)
+    pr_col_prefix_kernel(const uint64_t* __restrict__ starts, int p, int radix, int64_t* __restrict__ gd,
+                         uint64_t* __restrict__ coltot, uint64_t* __restrict__ colchunk) {
+    const int d = blockIdx.x * kDigChunk + threadIdx.x;
+    uint64_t before = 0;
+    if (d < radix) {
+        for (int v = 0; v < p; ++v) {
+            const uint64_t* row = starts + static_cast<uint64_t>(v) * (radix + 1);
+            const uint64_t ls = row[d], c = row[d + 1] - ls;
+            gd[static_cast<uint64_t>(v) * radix + d] = static_cast<int64_t>(before) - static_cast<int64_t>(ls);
+            before += c;
+        }
+        coltot[d] = before;
+    }
+    uint64_t ex;
+    const uint64_t tot = chunk_excl_scan(before, ex);
+    if (threadIdx.x == 0) colchunk[blockIdx.x] = tot;
+}
+
+// start[d] = exclusive scan of coltot over all digits (digit_starts).
+__global__ void __launch_bounds__(kDigChunk)
+    pr_digit_start_kernel(const uint64_t* __restrict__ coltot, const uint64_t* __restrict__ colchunk, int radix,
+                          uint64_t* __restrict__ start) {
+    const uint64_t base = chunk_base(colchunk, blockIdx.x);
+    const int d = blockIdx.x * kDigChunk + threadIdx.x;
+    const uint64_t c = d < radix ? coltot[d] : 0;
+    uint64_t ex;
+    chunk_excl_scan(c, ex);
+    if (d < radix) start[d] = base + ex;
+}
+
+// Exchange + rebuild of all workers: one coalesced scatter (digit runs of a
+// sorted block land on consecutive positions).
+constexpr int kScatterThreads = 256, kScatterItems = 16;
+__global__ void __launch_bounds__(kScatterThreads)
+    pr_scatter_kernel(const uint32_t* __restrict__ sorted, uint64_t n, int p, int shift, uint32_t mask, int radix,
+                      const uint64_t* __restrict__ start, const int64_t* __restrict__ gd, uint32_t* __restrict__ out) {
+    const int v = blockIdx.y;
+    const uint64_t off = part_offset(n, p, v), len = part_size(n, p, v);
+    const uint32_t* blk = sorted + off;
+    const int64_t* gdv = gd + static_cast<uint64_t>(v) * radix;
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * kScatterThreads;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kScatterThreads + threadIdx.x; i < len; i += step) {
+        const uint32_t key = __ldg(blk + i);
+        const uint32_t d = (key >> shift) & mask;
+        out[static_cast<uint64_t>(static_cast<int64_t>(__ldg(start + d)) + __ldg(gdv + d) + static_cast<int64_t>(i))] =
+            key;
+    }
+}
+
+// BSP accounting only (RunStats): send[v][w] = keys of worker v's block that
+// land in worker w's partition (the slices of radix.hpp:276-289).
+constexpr int kSendThreads = 256;
+__global__ void __launch_bounds__(kSendThreads)
+    pr_send_counts_kernel(const uint64_t* __restrict__ starts, const uint64_t* __restrict__ start,
+                          const int64_t* __restrict__ gd, uint64_t n, int p, int radix, uint64_t* __restrict__ send) {
+    extern __shared__ unsigned long long s_cnt[]; // p entries
+    const int v = blockIdx.y;
+    for (int w = threadIdx.x; w < p; w += kSendThreads) s_cnt[w] = 0;
+    __syncthreads();
+    const int d = blockIdx.x * kSendThreads + threadIdx.x;
+    if (d < radix) {
+        const uint64_t* row = starts + static_cast<uint64_t>(v) * (radix + 1);
+        const uint64_t ls = row[d], cv = row[d + 1] - ls;
+        if (cv) {
+            const uint64_t np = static_cast<uint64_t>(static_cast<int64_t>(start[d]) + gd[static_cast<uint64_t>(v) * radix + d] +
+                                                      static_cast<int64_t>(ls));
+            const int w0 = part_owner(n, p, np), w1 = part_owner(n, p, np + cv - 1);
+            for (int w = w0; w <= w1; ++w) {
+                const uint64_t lo = part_offset(n, p, w);
+                const uint64_t o = overlap(np, np + cv, lo, lo + part_size(n, p, w));
+                if (o) atomicAdd(&s_cnt[w], static_cast<unsigned long long>(o));
+            }
+        }
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < p; w += kSendThreads)
+        if (s_cnt[w]) atomicAdd(reinterpret_cast<unsigned long long*>(send + static_cast<uint64_t>(v) * p + w), s_cnt[w]);
+}
+
+// ---- routing plan of one worker `me` (distributed path, bsg_pr_plan) ------
+// Same O(p r) tables as the in-process round, from the gathered count matrix:
+//   col:  delta[v][d] = sum_{u<v} cnt(u,d) (temporary), coltot[d]
+//   scan: dstart[d] = exclusive scan of coltot (digit_starts)
+//   row:  one CTA per source v: ls(v,d) = row prefix of cnt(v,.), np(v,d) =
+//         dstart[d] + before(v,d); recv/split overlaps with me's partition;
+//         send slices of me (radix.hpp:276-289); delta[v][d] = np - ls.
+//   adj:  pr_plan2_kernel rebases delta onto me's receive buffer.
+__global__ void __launch_bounds__(kDigChunk)
+    pr_plan_col_kernel(const uint64_t* __restrict__ counts, int p, int radix, int64_t* __restrict__ delta,
+                       uint64_t* __restrict__ coltot, uint64_t* __restrict__ colchunk) {
+    const int d = blockIdx.x * kDigChunk + threadIdx.x;
+    uint64_t before = 0;
+    if (d < radix) {
+        for (int v = 0; v < p; ++v) {
+            delta[static_cast<uint64_t>(v) * radix + d] = static_cast<int64_t>(before);
+            before += counts[static_cast<uint64_t>(v) * radix + d];
+        }
+        coltot[d] = before;
+    }
+    uint64_t ex;
+    const uint64_t tot = chunk_excl_scan(before, ex);
+    if (threadIdx.x == 0) colchunk[blockIdx.x] = tot;
+}
+
+// rowchunk[v][c] = sum of cnt(v, chunk c)
+__global__ void __launch_bounds__(kDigChunk)
+    pr_plan_rowchunk_kernel(const uint64_t* __restrict__ counts, int radix, uint64_t* __restrict__ rowchunk) {
+    const int v = blockIdx.y, d = blockIdx.x * kDigChunk + threadIdx.x;
+    const uint64_t c = d < radix ? counts[static_cast<uint64_t>(v) * radix + d] : 0;
+    uint64_t ex;
+    const uint64_t tot = chunk_excl_scan(c, ex);
+    if (threadIdx.x == 0) rowchunk[static_cast<uint64_t>(v) * gridDim.x + blockIdx.x] = tot;
+}
+
+// One CTA per (digit chunk, source v).  recv_counts / split / send_counts
+// must be zero on entry (accumulated with atomics).
+__global__ void __launch_bounds__(kDigChunk)
+    pr_plan_row_kernel(const uint64_t* __restrict__ counts, const uint64_t* __restrict__ dstart,
+                       const uint64_t* __restrict__ rowchunk, uint64_t n, int p, int me, int radix,
+                       uint64_t* __restrict__ send_counts, uint64_t* __restrict__ recv_counts,
+                       int64_t* __restrict__ delta, uint64_t* __restrict__ split) {
+    extern __shared__ unsigned long long s_send[]; // p entries (v == me only)
+    __shared__ uint64_t s_red[2][kDigChunk / 32];
+    const int v = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (v == me)
+        for (int w = tid; w < p; w += kDigChunk) s_send[w] = 0;
+    const uint64_t lbase = chunk_base(rowchunk + static_cast<uint64_t>(v) * gridDim.x, blockIdx.x);
+    const int d = blockIdx.x * kDigChunk + tid;
+    const uint64_t cv = d < radix ? counts[static_cast<uint64_t>(v) * radix + d] : 0;
+    uint64_t ex;
+    chunk_excl_scan(cv, ex);
+    uint64_t acc_recv = 0, acc_split = 0;
+    if (d < radix) {
+        const uint64_t ls = lbase + ex;
+        int64_t* dp = delta + static_cast<uint64_t>(v) * radix + d;
+        const uint64_t np = dstart[d] + static_cast<uint64_t>(*dp);
+        const uint64_t lo_me = part_offset(n, p, me), hi_me = lo_me + part_size(n, p, me);
+        acc_recv = overlap(np, np + cv, lo_me, hi_me);
+        acc_split = overlap(np, np + cv, 0, lo_me);
+        *dp = static_cast<int64_t>(np) - static_cast<int64_t>(ls);
+        if (v == me && cv) {
+            const int w0 = part_owner(n, p, np), w1 = part_owner(n, p, np + cv - 1);
+            for (int w = w0; w <= w1; ++w) {
+                const uint64_t lo = part_offset(n, p, w);
+                const uint64_t o = overlap(np, np + cv, lo, lo + part_size(n, p, w));
+                if (o) atomicAdd(&s_send[w], static_cast<unsigned long long>(o));
+            }
+        }
+    }
+    const uint64_t r1 = warp_sum(acc_recv), r2 = warp_sum(acc_split);
+    if (lane == 0) {
+        s_red[0][warp] = r1;
+        s_red[1][warp] = r2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t a = 0, b = 0;
+        for (int w = 0; w < kDigChunk / 32; ++w) {
+            a += s_red[0][w];
+            b += s_red[1][w];
+        }
+        if (a) atomicAdd(reinterpret_cast<unsigned long long*>(recv_counts + v), static_cast<unsigned long long>(a));
+        if (b) atomicAdd(reinterpret_cast<unsigned long long*>(split + v), static_cast<unsigned long long>(b));
+    }
+    if (v == me)
+        for (int w = tid; w < p; w += kDigChunk)
+            if (s_send[w]) atomicAdd(reinterpret_cast<unsigned long long*>(send_counts + w), s_send[w]);
 }
 
 } // namespace
@@ -237,14 +386,27 @@ int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round
 }
 
 int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, uint64_t* send_counts,
-                   uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* split) {
-    if (!split || p > kMaxP) return -1;
+                   uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* scratch) {
+    if (!scratch || p > kMaxP) return -1;
     const int radix = 1 << bits;
+    const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+    uint64_t* split = scratch;                 // [p]
+    uint64_t* coltot = split + p;              // [radix]
+    uint64_t* dstart = coltot + radix;         // [radix]
+    uint64_t* colchunk = dstart + radix;       // [chunks]
+    uint64_t* rowchunk = colchunk + chunks;    // [p][chunks]
     TimedScope ts(3 /*BSG_K_PR*/, stream);
-    pr_plan1_kernel<<<p, kPlanThreads, sizeof(uint64_t) * p, stream>>>(counts, n, p, me, radix, send_counts,
-                                                                        recv_counts, rebuild_delta, split);
+    if (cudaMemsetAsync(split, 0, p * sizeof(uint64_t), stream) != cudaSuccess ||
+        cudaMemsetAsync(recv_counts, 0, p * sizeof(uint64_t), stream) != cudaSuccess ||
+        cudaMemsetAsync(send_counts, 0, p * sizeof(uint64_t), stream) != cudaSuccess)
+        return -1;
+    pr_plan_col_kernel<<<chunks, kDigChunk, 0, stream>>>(counts, p, radix, rebuild_delta, coltot, colchunk);
+    pr_plan_rowchunk_kernel<<<dim3(chunks, p), kDigChunk, 0, stream>>>(counts, radix, rowchunk);
+    pr_digit_start_kernel<<<chunks, kDigChunk, 0, stream>>>(coltot, colchunk, radix, dstart);
+    pr_plan_row_kernel<<<dim3(chunks, p), kDigChunk, sizeof(uint64_t) * p, stream>>>(
+        counts, dstart, rowchunk, n, p, me, radix, send_counts, recv_counts, rebuild_delta, split);
     pr_plan2_kernel<<<p, kPlanThreads, 0, stream>>>(n, p, me, radix, recv_counts, split, rebuild_delta);
-    return cudaGetLastError() == cudaSuccess ? 2 : -1;
+    return cudaGetLastError() == cudaSuccess ? 5 : -1;
 }
 
 int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shift, const int64_t* rebuild_delta,
@@ -263,25 +425,28 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
                              bsg_run_stats* stats, cudaStream_t stream) {
     if (p > kMaxP) return fail(BSG_EINVAL, "parallel radix sort: p must be <= 1024 on one GPU");
     const int radix = 1 << bits;
+    const uint32_t mask = static_cast<uint32_t>(radix - 1);
     const uint64_t pp = static_cast<uint64_t>(p) * p;
     cudaError_t e;
     if ((e = ctx->pr_block.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
     if ((e = ctx->pr_sorted.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
-    if ((e = ctx->pr_counts.ensure(static_cast<uint64_t>(p) * radix * 8)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if ((e = ctx->pr_counts.ensure(static_cast<uint64_t>(p) * (radix + 1) * 8)) != cudaSuccess)
+        return cuda_fail(e, "pr workspace");
     if ((e = ctx->pr_delta.ensure(static_cast<uint64_t>(p) * radix * 8)) != cudaSuccess) return cuda_fail(e, "pr workspace");
-    if ((e = ctx->pr_misc.ensure(pp * 8 * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
+    if ((e = ctx->pr_misc.ensure(pp * 8 + static_cast<uint64_t>(radix) * 16 + 64 * 8)) != cudaSuccess)
+        return cuda_fail(e, "pr workspace");
     if (bits == 16 && (e = ctx->stage_b.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
     RadixWorkspace ws;
     if (int rc = ctx->radix_ws(std::max<uint64_t>(n / p + 1, 1), &ws)) return rc;
 
     uint32_t* A = ctx->pr_block.as<uint32_t>();
     uint32_t* S = ctx->pr_sorted.as<uint32_t>();
-    uint64_t* counts = ctx->pr_counts.as<uint64_t>();
-    int64_t* delta = ctx->pr_delta.as<int64_t>();
-    uint64_t* send = ctx->pr_misc.as<uint64_t>();
-    uint64_t* recv = send + pp;
-    uint64_t* split = recv + pp;
-    const uint32_t** srcp = reinterpret_cast<const uint32_t**>(split + pp);
+    uint64_t* starts = ctx->pr_counts.as<uint64_t>(); // [p][radix+1]
+    int64_t* gd = ctx->pr_delta.as<int64_t>();        // [p][radix]
+    uint64_t* send = ctx->pr_misc.as<uint64_t>();     // [p][p]
+    uint64_t* coltot = send + pp;                      // [radix]
+    uint64_t* dstart = coltot + radix;                 // [radix]
+    uint64_t* colchunk = dstart + radix;               // [radix / kDigChunk]
 
     if (n && (e = cudaMemcpyAsync(A, in, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
         return cuda_fail(e, "pr copy in");
@@ -293,13 +458,10 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         launches += static_cast<uint64_t>(l);
         return true;
     };
+    const uint64_t max_len = n / p + (n % p ? 1 : 0);
     for (int round = 0; round < rounds && n; ++round) {
         const int shift = round * bits;
-        for (int w = 0; w < p; ++w) {
-            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
-            if (!add(launch_pr_count(ctx, A + off, sz, round, bits, counts + static_cast<uint64_t>(w) * radix, stream)))
-                return cuda_fail(cudaGetLastError(), "pr count");
-        }
+        // local stable pass of every worker (sort_and_scatter's count_sort_round)
         for (int w = 0; w < p; ++w) {
             const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
             if (sz == 0) continue;
@@ -313,26 +475,28 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
                     return cuda_fail(cudaGetLastError(), "pr local pass");
             }
         }
-        for (int me = 0; me < p; ++me) {
-            const uint64_t off = bsg_partition_offset_of(n, p, me), sz = bsg_partition_size_of(n, p, me);
-            if (!add(launch_pr_plan(counts, n, p, me, bits, send + static_cast<uint64_t>(me) * p,
-                                    recv + static_cast<uint64_t>(me) * p, delta, stream,
-                                    split + static_cast<uint64_t>(me) * p)))
-                return cuda_fail(cudaGetLastError(), "pr plan");
-            pr_src_ptrs_kernel<<<1, 256, 0, stream>>>(S, n, p, split + static_cast<uint64_t>(me) * p,
-                                                       srcp + static_cast<uint64_t>(me) * p);
-            ++launches;
-            if (sz) {
-                const uint64_t want = (sz + kRebuildThreads * 8 - 1) / (kRebuildThreads * 8);
-                const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
-                pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(
-                    nullptr, sz, p, recv + static_cast<uint64_t>(me) * p, srcp + static_cast<uint64_t>(me) * p,
-                    static_cast<uint32_t>(radix - 1), shift, radix, delta, A + off);
-                ++launches;
-            }
-            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr rebuild");
+        {
+            TimedScope ts(3 /*BSG_K_PR*/, stream);
+            // per-worker digit counts (count_digits) as run starts of the sorted blocks
+            pr_run_starts_kernel<<<dim3((radix + 1 + 255) / 256, p), 256, 0, stream>>>(S, n, p, shift, mask, radix,
+                                                                                      starts);
+            // count matrix -> routing (digit_starts + next_pos)
+            const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+            pr_col_prefix_kernel<<<chunks, kDigChunk, 0, stream>>>(starts, p, radix, gd, coltot, colchunk);
+            pr_digit_start_kernel<<<chunks, kDigChunk, 0, stream>>>(coltot, colchunk, radix, dstart);
+            // exchange + rebuild of all workers
+            const uint64_t want = (max_len + kScatterThreads * kScatterItems - 1) / (kScatterThreads * kScatterItems);
+            const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(
+                1, std::min<uint64_t>(want, std::max<uint64_t>(1, kSmCountB200 * 8 / static_cast<uint64_t>(p)))));
+            pr_scatter_kernel<<<dim3(gx, p), kScatterThreads, 0, stream>>>(S, n, p, shift, mask, radix, dstart, gd, A);
+            launches += 4;
         }
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
         if (stats) {
+            if ((e = cudaMemsetAsync(send, 0, pp * 8, stream)) != cudaSuccess) return cuda_fail(e, "pr stats");
+            pr_send_counts_kernel<<<dim3((radix + kSendThreads - 1) / kSendThreads, p), kSendThreads, p * 8, stream>>>(
+                starts, dstart, gd, n, p, radix, send);
+            ++launches;
             if ((e = cudaMemcpyAsync(h_send.data(), send, pp * 8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess ||
                 (e = cudaStreamSynchronize(stream)) != cudaSuccess)
                 return cuda_fail(e, "pr stats");

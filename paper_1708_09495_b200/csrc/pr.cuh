@@ -15,10 +15,11 @@ int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round
                     cudaStream_t stream);
 
 // Routing plan of worker `me` from the p x r count matrix (radix.hpp:248-290).
-// split (optional, p entries): index in each source's sorted block where the
-// slice for `me` begins.
+// scratch: p(1 + c) + 2r + c uint64 words of device workspace, c = ceil(r /
+// 1024) (split = the index in each source's sorted block where the slice for
+// `me` begins, column totals, digit starts, chunk sums).
 int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, uint64_t* send_counts,
-                   uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* split = nullptr);
+                   uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* scratch);
 
 // gather_slices (radix.hpp:295-333) as a stable scatter of the source-major
 // receive buffer: block[delta[src][digit] + j] = recv[j].

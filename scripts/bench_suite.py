@@ -53,7 +53,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="C1,C2,C4,PR", help="comma-separated sections: C1,C2,C4,PR")
     args = ap.parse_args()
+    only = set(args.only.split(","))
     ref = maybe_reference()
     ctx = _lib.context(0)
     L = _lib.lib()
@@ -67,7 +69,21 @@ def main():
     def sort_dev(t, out, bits):
         _lib.check(L.bsg_radix_sort_u32(ctx.handle, t.data_ptr(), out.data_ptr(), t.numel(), bits, 1, st))
 
-    # ---- C1 -------------------------------------------------------------
+    if "C1" in only:
+        c1(ref, sort_dev, emit)
+    if "C2" in only:
+        c2(args, ref, ctx, sort_dev, emit)
+    if "C4" in only:
+        c4(args, ref, ctx, L, st, emit)
+    if "PR" in only:
+        pr_rows(args, ref, L, ctx, st, emit)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump({"host_threads": os.cpu_count(), "gpu": torch.cuda.get_device_name(0), "rows": rows,
+                       "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}, f, indent=1)
+
+
+def c1(ref, sort_dev, emit):
     n = 1 << 20
     keys = bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0))
     t = torch.from_numpy(keys.view(np.int32)).cuda()
@@ -80,6 +96,8 @@ def main():
         row.update({"cpu_ref_ms": tc * 1e3, "cpu_cores": 1, "speedup": tc * 1e3 / ms})
     emit(row)
 
+
+def c2(args, ref, ctx, sort_dev, emit):
     # ---- C2 / C3 ----------------------------------------------------------
     n = 1 << 28
     inputs = [("uniform", bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0)))]
@@ -111,6 +129,8 @@ def main():
             emit(row)
         del t, out
 
+
+def c4(args, ref, ctx, L, st, emit):
     # ---- C4 ---------------------------------------------------------------
     num, ln = 1 << 16, 4096
     keys = bsg.generate_uniform_keys(num * ln, bsg.derive_seed(1, 0))
@@ -147,6 +167,8 @@ def main():
                       "gpu_keys_per_s": num2 * ln2 / ms * 1e3})
     del t, out
 
+
+def pr_rows(args, ref, L, ctx, st, emit):
     # ---- PR with logical workers on one GPU ------------------------------
     n = 1 << 26
     keys = bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0))
@@ -157,16 +179,14 @@ def main():
             def runp():
                 _lib.check(L.bsg_parallel_radix_sort_u32(ctx.handle, t.data_ptr(), out.data_ptr(), n, p, radix_log2, -1,
                                                          None, 1, st))
-            ms = gpu_time(runp, reps=3, warm=1)
-            row = {"row": f"{nm} p={p} logical workers, 1 GPU", "n": n, "gpu_ms": ms, "gpu_keys_per_s": n / ms * 1e3}
+            ms = gpu_time(runp, reps=5, warm=2)
+            ok = bool(torch.equal(out.to(torch.int64) & 0xFFFFFFFF, torch.sort(t.to(torch.int64) & 0xFFFFFFFF).values))
+            row = {"row": f"{nm} p={p} logical workers, 1 GPU", "n": n, "gpu_ms": ms, "gpu_keys_per_s": n / ms * 1e3,
+                   "verified": ok}
             if ref is not None and not args.quick:
                 tc, _ = ref.time_parallel_radix(keys, p, 1 << radix_log2)
                 row.update({"cpu_ref_ms": tc * 1e3, "cpu_threads": p, "speedup": tc * 1e3 / ms})
             emit(row)
-    if args.out:
-        with open(args.out, "w") as f:
-            json.dump({"host_threads": os.cpu_count(), "gpu": torch.cuda.get_device_name(0), "rows": rows,
-                       "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}, f, indent=1)
 
 
 if __name__ == "__main__":

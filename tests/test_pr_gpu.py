@@ -117,3 +117,16 @@ def test_distributed_nccl_world1(cuda, bsg, orc):
                 np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), exp)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p", [3, 8, 64])
+def test_large_blocks_per_round(cuda, bsg, orc, p):
+    """Multi-tile worker blocks: per-round states and RunStats vs the oracle."""
+    keys = orc.generate_uniform_keys((1 << 20) + 777, 1000 + p)
+    for radix in (256, 65536):
+        rounds = 32 // (radix.bit_length() - 1)
+        for k in sorted({1, rounds}):
+            res = pr(bsg, keys, p, radix, k)
+            exp, est = orc.parallel_radix(keys, p, radix, k)
+            np.testing.assert_array_equal(res.output, exp)
+            assert res.stats == est
