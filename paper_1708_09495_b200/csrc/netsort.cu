@@ -27,9 +27,26 @@ namespace bsg {
 
 namespace {
 
-constexpr int kNK = 16;         // outputs per thread-chunk
-constexpr int kNetThreads = 256;
+constexpr int kNK = 16;         // keys per thread-chunk: register sort, global merges
+#ifndef BSG_NET_MK
+#define BSG_NET_MK 16
+#endif
+constexpr int kMK = BSG_NET_MK;
+#ifndef BSG_NET_MINB
+#define BSG_NET_MINB 5
+#endif
+#ifndef BSG_NET_SORT32
+#define BSG_NET_SORT32 1
+#endif // outputs per thread-chunk of the shared-memory merges
 constexpr uint32_t kPad = 0xFFFFFFFFu;
+
+// x / d without a division instruction sequence: m = ceil(2^32 / d) is exact
+// for x * d < 2^32 (indices and divisors here are < 2^16).
+struct FastDiv {
+    uint32_t d, m;
+    __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv), m(dv > 1 ? 0xFFFFFFFFu / dv + 1u : 0u) {}
+    __device__ __forceinline__ uint32_t div(uint32_t x) const { return d > 1 ? __umulhi(x, m) : x; }
+};
 
 __device__ __forceinline__ void cas(uint32_t& a, uint32_t& b) {
     const uint32_t lo = min(a, b), hi = max(a, b);
@@ -109,9 +126,17 @@ __device__ __forceinline__ void sort16(uint32_t (&v)[16]) {
 // patterns of merge-path chunks (8 outputs per lane) become conflict-free.
 __device__ __forceinline__ uint32_t pad(uint32_t i) { return i + (i >> 5); }
 
-// Writes outputs [diag, diag+cnt) of merge(A, B) (ties taken from A first,
-// netsort.hpp:39) into smem at logical indices dst0 .. dst0+cnt-1.  A and B
-// are logical index ranges [a0, a0+na), [b0, b0+nb) of the padded buffer S.
+// Writes outputs [diag, diag+cnt) of merge(A, B) (netsort.hpp:30-51) into
+// smem at logical indices dst0 .. dst0+cnt-1.  A and B are logical index
+// ranges [a0, a0+na), [b0, b0+nb) of the padded buffer S.
+//
+// After the merge-path split (i, j) of `diag`, the next kNK outputs are the
+// kNK smallest of A[i, i+kNK) u B[j, j+kNK) (MAX past the ends): with x
+// ascending and y ascending, min(x[k], y[kNK-1-k]) is that set as a bitonic
+// sequence, sorted by a 4-stage bitonic network.  Only key values are
+// produced, so which of two equal keys is taken (or a MAX pad instead of a
+// real 0xFFFFFFFF key) cannot change the output.
+template <int K>
 __device__ __forceinline__ void merge_chunk_s(const uint32_t* S, uint32_t a0, int na, uint32_t b0, int nb, int diag,
                                               int cnt, uint32_t* D, uint32_t dst0) {
     int lo = max(0, diag - nb), hi = min(diag, na);
@@ -120,49 +145,53 @@ __device__ __forceinline__ void merge_chunk_s(const uint32_t* S, uint32_t a0, in
         if (S[pad(a0 + mid)] <= S[pad(b0 + diag - 1 - mid)]) lo = mid + 1;
         else hi = mid;
     }
-    int i = lo, j = diag - lo;
-    uint32_t av = i < na ? S[pad(a0 + i)] : 0u, bv = j < nb ? S[pad(b0 + j)] : 0u;
+    const int i = lo, j = diag - lo;
+    const int ra = na - i, rb = nb - j;
+    const uint32_t pa = a0 + i, pb = b0 + j;
+    uint32_t x[K], y[K];
 #pragma unroll
-    for (int k = 0; k < kNK; ++k) {
-        if (k < cnt) {
-            const bool take_a = i < na && (j >= nb || av <= bv);
-            D[pad(dst0 + k)] = take_a ? av : bv;
-            i += take_a ? 1 : 0;
-            j += take_a ? 0 : 1;
-            const bool more = take_a ? i < na : j < nb;
-            const uint32_t nxt = more ? S[pad(take_a ? a0 + i : b0 + j)] : 0u;
-            av = take_a ? nxt : av;
-            bv = take_a ? bv : nxt;
-        }
+    for (int k = 0; k < K; ++k) {
+        x[k] = k < ra ? S[pad(pa + k)] : kPad;
+        y[k] = k < rb ? S[pad(pb + k)] : kPad;
     }
+#pragma unroll
+    for (int k = 0; k < K; ++k) x[k] = min(x[k], y[K - 1 - k]);
+#pragma unroll
+    for (int d = K / 2; d >= 1; d >>= 1)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if ((k & d) == 0) cas(x[k], x[k + d]);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (k < cnt) D[pad(dst0 + k)] = x[k];
 }
 
-// Global-memory variant for the standalone merge_split.
+// Global-memory variant (standalone merge_split, large-array stages): same
+// merge-path split + bitonic selection of the next kNK outputs.
 __device__ __forceinline__ void merge_chunk(const uint32_t* A, int na, const uint32_t* B, int nb, int diag, int cnt,
                                             uint32_t* dst) {
+    (void)cnt;
     int lo = max(0, diag - nb), hi = min(diag, na);
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (A[mid] <= B[diag - 1 - mid]) lo = mid + 1;
+        if (__ldg(A + mid) <= __ldg(B + diag - 1 - mid)) lo = mid + 1;
         else hi = mid;
     }
-    int i = lo, j = diag - lo;
-    uint32_t av = i < na ? A[i] : 0u, bv = j < nb ? B[j] : 0u;
+    const int i = lo, j = diag - lo;
+    const int ra = na - i, rb = nb - j;
+    uint32_t y[kNK];
 #pragma unroll
     for (int k = 0; k < kNK; ++k) {
-        if (k < cnt) {
-            const bool take_a = i < na && (j >= nb || av <= bv);
-            if (take_a) {
-                dst[k] = av;
-                ++i;
-                av = i < na ? A[i] : 0u;
-            } else {
-                dst[k] = bv;
-                ++j;
-                bv = j < nb ? B[j] : 0u;
-            }
-        }
+        dst[k] = k < ra ? __ldg(A + i + k) : kPad;
+        y[k] = k < rb ? __ldg(B + j + k) : kPad;
     }
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) dst[k] = min(dst[k], y[kNK - 1 - k]);
+#pragma unroll
+    for (int d = kNK / 2; d >= 1; d >>= 1)
+#pragma unroll
+        for (int k = 0; k < kNK; ++k)
+            if ((k & d) == 0) cas(dst[k], dst[k + d]);
 }
 
 // bitonic_schedule (netsort.hpp:76-88) for stage s, worker i.
@@ -195,7 +224,11 @@ __device__ __forceinline__ int oet_partner(int r, int i, int p, bool& keep_low) 
     return i - 1;
 }
 
-__global__ void __launch_bounds__(kNetThreads)
+// THREADS x MINB: 256 x 5 for padded arrays <= 8192 keys (several CTAs per
+// SM), 1024 x 1 above, where the two shared-memory copies allow one CTA per
+// SM (keeps 32 warps resident instead of 8).
+template <int kNetThreads, int MINB>
+__global__ void __launch_bounds__(kNetThreads, MINB)
     block_network_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t num_arrays,
                          uint32_t len, int p, uint32_t L, int network, int run_stages, int full, int apc) {
     extern __shared__ __align__(16) uint32_t net_smem[];
@@ -209,22 +242,64 @@ __global__ void __launch_bounds__(kNetThreads)
 
     // prepare_blocks: load + pad (netsort.hpp:131-139)
     const uint32_t tot = static_cast<uint32_t>(na) * P;
+    const FastDiv divP(P);
     for (uint32_t idx = tid; idx < tot; idx += kNetThreads) {
-        const uint32_t a = idx / P, e = idx - a * P;
+        const uint32_t a = divP.div(idx), e = idx - a * P;
         bufA[pad(idx)] = e < len ? __ldg(in + (array0 + a) * len + e) : kPad;
     }
     __syncthreads();
 
-    const uint32_t cb = (L + kNK - 1) / kNK; // chunks per block
+#if BSG_NET_SORT32
+    // superstep 0: local sort of every block.  (a) 32-key register sorts
+    // (two Batcher 16-networks + a bitonic merge), one chunk per thread
+    constexpr int kSK = 2 * kNK;
+    const uint32_t cb = (L + kSK - 1) / kSK; // sort chunks per block
     const uint32_t items = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cb;
-
-    // superstep 0: local sort of every block.  (a) 16-key register sorting networks
+    const FastDiv div_pcb(static_cast<uint32_t>(p) * cb), div_cb(cb);
     for (uint32_t it = tid; it < items; it += kNetThreads) {
-        const uint32_t a = it / (p * cb), rem = it - a * p * cb;
-        const uint32_t w = rem / cb, c = rem - w * cb;
+        const uint32_t a = div_pcb.div(it), rem = it - a * p * cb;
+        const uint32_t w = div_cb.div(rem), c = rem - w * cb;
         const uint32_t b0 = a * P + w * L;
-        const uint32_t ob = c * kNK;
-        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
+        const uint32_t ob = c * kSK;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kSK), L - ob));
+        uint32_t v[kNK], u[kNK];
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) {
+            v[k] = k < cnt ? bufA[pad(b0 + ob + k)] : kPad;
+            u[k] = k + kNK < cnt ? bufA[pad(b0 + ob + kNK + k)] : kPad;
+        }
+        sort16(v);
+        sort16(u);
+        // half-cleaner of v ++ reverse(u): v = 16 smallest, u = 16 largest (bitonic each)
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) cas(v[k], u[kNK - 1 - k]);
+#pragma unroll
+        for (int d = kNK / 2; d >= 1; d >>= 1)
+#pragma unroll
+            for (int k = 0; k < kNK; ++k)
+                if ((k & d) == 0) {
+                    cas(v[k], v[k + d]);
+                    cas(u[k], u[k + d]);
+                }
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) {
+            if (k < cnt) bufA[pad(b0 + ob + k)] = v[k];
+            if (k + kNK < cnt) bufA[pad(b0 + ob + kNK + k)] = u[k];
+        }
+    }
+    __syncthreads();
+#else
+    // superstep 0: local sort of every block.  (a) 16-key register sorting networks
+    constexpr int kSK = kNK;
+    const uint32_t cb = (L + kSK - 1) / kSK; // sort chunks per block
+    const uint32_t items = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cb;
+    const FastDiv div_pcb(static_cast<uint32_t>(p) * cb), div_cb(cb);
+    for (uint32_t it = tid; it < items; it += kNetThreads) {
+        const uint32_t a = div_pcb.div(it), rem = it - a * p * cb;
+        const uint32_t w = div_cb.div(rem), c = rem - w * cb;
+        const uint32_t b0 = a * P + w * L;
+        const uint32_t ob = c * kSK;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kSK), L - ob));
         uint32_t v[kNK];
 #pragma unroll
         for (int k = 0; k < kNK; ++k) v[k] = k < cnt ? bufA[pad(b0 + ob + k)] : kPad;
@@ -234,19 +309,23 @@ __global__ void __launch_bounds__(kNetThreads)
             if (k < cnt) bufA[pad(b0 + ob + k)] = v[k];
     }
     __syncthreads();
+#endif
     // (b) bottom-up merge-path merges inside each block
     uint32_t* src = bufA;
     uint32_t* dst = bufB;
-    for (uint32_t width = kNK; width < L; width *= 2) {
-        for (uint32_t it = tid; it < items; it += kNetThreads) {
-            const uint32_t a = it / (p * cb), rem = it - a * p * cb;
-            const uint32_t w = rem / cb, c = rem - w * cb;
+    const uint32_t cbm = (L + kMK - 1) / kMK; // merge chunks per block
+    const uint32_t mitems = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cbm;
+    const FastDiv div_pcbm(static_cast<uint32_t>(p) * cbm), div_cbm(cbm);
+    for (uint32_t width = kSK; width < L; width *= 2) {
+        for (uint32_t it = tid; it < mitems; it += kNetThreads) {
+            const uint32_t a = div_pcbm.div(it), rem = it - a * p * cbm;
+            const uint32_t w = div_cbm.div(rem), c = rem - w * cbm;
             const uint32_t bs = a * P + w * L;
-            const uint32_t ob = c * kNK;
-            const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
-            const uint32_t ps = (ob / (2 * width)) * (2 * width);
+            const uint32_t ob = c * kMK;
+            const int cnt = static_cast<int>(min(static_cast<uint32_t>(kMK), L - ob));
+            const uint32_t ps = ob & ~(2 * width - 1); // width is a power of two
             const uint32_t a_end = min(ps + width, L), b_end = min(ps + 2 * width, L);
-            merge_chunk_s(src, bs + ps, static_cast<int>(a_end - ps), bs + a_end, static_cast<int>(b_end - a_end),
+            merge_chunk_s<kMK>(src, bs + ps, static_cast<int>(a_end - ps), bs + a_end, static_cast<int>(b_end - a_end),
                           static_cast<int>(ob - ps), cnt, dst, bs + ob);
         }
         __syncthreads();
@@ -257,24 +336,24 @@ __global__ void __launch_bounds__(kNetThreads)
 
     // supersteps 1..S: merge_split stages
     for (int s = 0; s < run_stages; ++s) {
-        for (uint32_t it = tid; it < items; it += kNetThreads) {
-            const uint32_t a = it / (p * cb), rem = it - a * p * cb;
-            const int i = static_cast<int>(rem / cb);
-            const uint32_t c = rem - static_cast<uint32_t>(i) * cb;
-            const uint32_t ob = c * kNK;
-            const int cnt = static_cast<int>(min(static_cast<uint32_t>(kNK), L - ob));
+        for (uint32_t it = tid; it < mitems; it += kNetThreads) {
+            const uint32_t a = div_pcbm.div(it), rem = it - a * p * cbm;
+            const int i = static_cast<int>(div_cbm.div(rem));
+            const uint32_t c = rem - static_cast<uint32_t>(i) * cbm;
+            const uint32_t ob = c * kMK;
+            const int cnt = static_cast<int>(min(static_cast<uint32_t>(kMK), L - ob));
             bool keep_low = false;
             const int q = network == 0 ? btn_partner(s, i, keep_low) : oet_partner(s, i, p, keep_low);
             const uint32_t my0 = a * P + static_cast<uint32_t>(i) * L;
             if (q < 0) {
 #pragma unroll
-                for (int k = 0; k < kNK; ++k)
+                for (int k = 0; k < kMK; ++k)
                     if (k < cnt) dst[pad(my0 + ob + k)] = src[pad(my0 + ob + k)];
                 continue;
             }
             const int lo_w = min(i, q), hi_w = max(i, q);
             const int diag = static_cast<int>((keep_low ? 0u : L) + ob);
-            merge_chunk_s(src, a * P + static_cast<uint32_t>(lo_w) * L, static_cast<int>(L),
+            merge_chunk_s<kMK>(src, a * P + static_cast<uint32_t>(lo_w) * L, static_cast<int>(L),
                           a * P + static_cast<uint32_t>(hi_w) * L, static_cast<int>(L), diag, cnt, dst, my0 + ob);
         }
         __syncthreads();
@@ -285,8 +364,9 @@ __global__ void __launch_bounds__(kNetThreads)
 
     // concatenate (+ strip the pad when the network ran to completion)
     if (full) {
+        const FastDiv div_len(len);
         for (uint32_t idx = tid; idx < static_cast<uint32_t>(na) * len; idx += kNetThreads) {
-            const uint32_t a = idx / len, e = idx - a * len;
+            const uint32_t a = div_len.div(idx), e = idx - a * len;
             out[(array0 + a) * len + e] = src[pad(a * P + e)];
         }
     } else {
@@ -356,7 +436,7 @@ int launch_net_stage(const uint32_t* src, uint32_t* dst, int p, uint32_t L, int 
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((items + kMsThreads - 1) / kMsThreads, 148 * 16)));
     TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
     net_stage_kernel<<<grid, kMsThreads, 0, stream>>>(src, dst, p, L, network, s);
-    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p,
@@ -367,18 +447,26 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
     const size_t padded = static_cast<size_t>(apc) * P + (static_cast<size_t>(apc) * P >> 5) + 1;
     const size_t smem = 2ull * padded * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(block_network_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(2 * (kNetMaxPadded + kNetMaxPadded / 32 + 1) * sizeof(uint32_t)));
-        attr = true;
-    }
     const uint64_t grid = (num_arrays + apc - 1) / apc;
     if (grid > 0x7FFFFFFFull) return -1;
+    static const bool attr = [] {
+        const int max_smem = static_cast<int>(2 * (kNetMaxPadded + kNetMaxPadded / 32 + 1) * sizeof(uint32_t));
+        cudaFuncSetAttribute(block_network_kernel<256, BSG_NET_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_smem);
+        cudaFuncSetAttribute(block_network_kernel<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        return true;
+    }();
+    (void)attr;
+    const uint64_t resident = static_cast<uint64_t>(apc) * P;
+    const bool big = resident > 8192;
     TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
-    block_network_kernel<<<static_cast<unsigned>(grid), kNetThreads, smem, stream>>>(in, out, num_arrays, len, p, L,
-                                                                                   network, run_stages, full ? 1 : 0, apc);
-    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    if (!big)
+        block_network_kernel<256, BSG_NET_MINB><<<static_cast<unsigned>(grid), 256, smem, stream>>>(
+            in, out, num_arrays, len, p, L, network, run_stages, full ? 1 : 0, apc);
+    else
+        block_network_kernel<1024, 1><<<static_cast<unsigned>(grid), 1024, smem, stream>>>(
+            in, out, num_arrays, len, p, L, network, run_stages, full ? 1 : 0, apc);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_merge_split(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* low, uint32_t* high,
@@ -389,7 +477,7 @@ int launch_merge_split(const uint32_t* a, uint64_t na, const uint32_t* b, uint64
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((chunks + kMsThreads - 1) / kMsThreads, 148 * 16));
     merge_split_kernel<<<grid, kMsThreads, 0, stream>>>(a, static_cast<uint32_t>(na), b, static_cast<uint32_t>(nb), low,
                                                        high);
-    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 } // namespace bsg

@@ -374,7 +374,7 @@ int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round
         const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200)));
         hist16_kernel<<<grid, kHist16Threads, 32768 * 4, stream>>>(block, len, 16 * round,
                                                                    reinterpret_cast<unsigned long long*>(counts));
-        return cudaGetLastError() == cudaSuccess ? 1 : -1;
+        return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
     }
     const uint64_t chunks = len ? (len + kChunkKeys - 1) / kChunkKeys : 1;
     if (ctx->cnt32.ensure(chunks * 256 * sizeof(uint32_t)) != cudaSuccess) return -1;
@@ -406,7 +406,7 @@ int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, 
     pr_plan_row_kernel<<<dim3(chunks, p), kDigChunk, sizeof(uint64_t) * p, stream>>>(
         counts, dstart, rowchunk, n, p, me, radix, send_counts, recv_counts, rebuild_delta, split);
     pr_plan2_kernel<<<p, kPlanThreads, 0, stream>>>(n, p, me, radix, recv_counts, split, rebuild_delta);
-    return cudaGetLastError() == cudaSuccess ? 5 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 5 : -1;
 }
 
 int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shift, const int64_t* rebuild_delta,
@@ -418,7 +418,7 @@ int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shi
     TimedScope ts(3 /*BSG_K_PR*/, stream);
     pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(recv, recv_len, p, recv_counts, nullptr, (1u << bits) - 1u,
                                                            shift, 1 << bits, rebuild_delta, block);
-    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int p, int bits, int rounds,

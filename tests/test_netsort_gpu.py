@@ -118,3 +118,19 @@ def test_large_arrays_per_stage_states(cuda, bsg, orc, network, p):
         exp, est = orc.block_network(network, keys, p, s)
         np.testing.assert_array_equal(got.reshape(-1), exp)
         assert st == est
+
+
+@pytest.mark.parametrize("network,p", [(0, 2), (0, 8), (1, 3), (1, 7)])
+def test_resident_1024_thread_path_per_stage(cuda, bsg, orc, network, p):
+    """Padded arrays of 8193..16384 keys run on the 1024-thread instantiation;
+    ragged lengths (pads inside the last block), every truncated stage."""
+    for n in (8193 + p, 12001, 16384 - 16384 % p):
+        if n // p * p != n and network == 0:
+            n -= n % p
+        keys = orc.generate_uniform_keys(n, 99 + n + p)
+        S = orc.schedule(network, p)[0].shape[0]
+        for s in sorted({0, 1, S // 2, S}):
+            got, st = bsg.netsort.block_network_batched(keys.reshape(1, n), p, network, s)
+            exp, est = orc.block_network(network, keys, p, s)
+            np.testing.assert_array_equal(got.reshape(-1), exp)
+            assert st == est
