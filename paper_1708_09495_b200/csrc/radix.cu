@@ -31,6 +31,9 @@
 #include "radix.cuh"
 #include "timer.cuh"
 
+#ifndef BSG_LB_WIN
+#define BSG_LB_WIN 16
+#endif
 namespace bsg {
 
 namespace {
@@ -263,7 +266,8 @@ struct OnesweepSmem {
     static constexpr size_t wcnt_off = in_off + sizeof(uint32_t) * 2 * TILE;     // WARPS*RADIX u16
     static constexpr size_t delta_off = wcnt_off + sizeof(uint16_t) * WARPS * RADIX; // RADIX Off
     static constexpr size_t excl_off = delta_off + sizeof(uint64_t) * RADIX;     // RADIX u32
-    static constexpr size_t scan_off = excl_off + sizeof(uint32_t) * RADIX;      // 32 u32
+    static constexpr size_t tcnt_off = excl_off + sizeof(uint32_t) * RADIX;      // RADIX u32
+    static constexpr size_t scan_off = tcnt_off + sizeof(uint32_t) * RADIX;      // 32 u32
     static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // 2 tile ids
     static constexpr size_t bar_off = misc_off + 16;                              // 2 mbarriers
     static constexpr size_t bytes = bar_off + 16;
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     uint16_t* s_wcnt = reinterpret_cast<uint16_t*>(smem + L::wcnt_off); // tile offsets < 2^16
     Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
     uint32_t* s_excl = reinterpret_cast<uint32_t*>(smem + L::excl_off);
+    uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem + L::tcnt_off);
     uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
     uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
@@ -363,8 +368,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
-                if (FULL) {
-                    keys[i] = idx < vec ? buf[idx] : __ldg(src + tile_start + idx);
+                if (FULL) { // whole tile delivered by TMA
+                    keys[i] = buf[idx];
                 } else {
                     keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
                 }
@@ -405,42 +410,57 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 }
             }
         };
-        if (full) rank_items(std::true_type{});
+        // full TMA tiles rank straight from shared memory; partial tiles and
+        // misaligned (non-TMA) bodies take the guarded path
+        if (full && vec == static_cast<uint32_t>(TILE)) rank_items(std::true_type{});
         else rank_items(std::false_type{});
         phase(1);
         __syncthreads();
         phase(2);
 
         // ---- per-digit: warp prefix, tile count, publish aggregate ---------
-        uint32_t tile_cnt = 0;
-        if (tid < RADIX) {
+        // Thread t < RADIX/2 owns digits 2t, 2t+1: one 32-bit word holds both
+        // 16-bit counters (counts and offsets < 2^16: packed adds never carry).
+        uint32_t tile_cnt = 0; // digit tid's count, valid for tid < RADIX (see below)
+        constexpr int PAIRS = RADIX / 2;
+        uint32_t* wc32 = reinterpret_cast<uint32_t*>(s_wcnt);
+        uint32_t run2 = 0;
+        if (tid < PAIRS) {
 #pragma unroll
             for (int w = 0; w < WARPS; ++w) {
-                const uint32_t c = s_wcnt[w * RADIX + tid];
-                s_wcnt[w * RADIX + tid] = static_cast<uint16_t>(tile_cnt);
-                tile_cnt += c;
+                const uint32_t c2 = wc32[w * PAIRS + tid];
+                wc32[w * PAIRS + tid] = run2;
+                run2 += c2;
             }
-            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid],
-                           (tile == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
+            const uint32_t lo = run2 & 0xFFFFu, hi = run2 >> 16;
+            const uint32_t flag = tile == 0 ? kFlagInc : kFlagAgg;
+            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + 2 * tid], flag | lo);
+            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + 2 * tid + 1], flag | hi);
         }
-        constexpr int SCAN_WARPS = (RADIX + 31) / 32;
-        uint32_t incl = 0;
+        constexpr int SCAN_WARPS = (PAIRS + 31) / 32;
+        uint32_t pair_incl = 0, pair_sum = 0;
         if (warp < SCAN_WARPS) {
-            incl = warp_inclusive_scan(tile_cnt);
-            if (lane == 31) s_scan[warp] = incl;
+            pair_sum = (run2 & 0xFFFFu) + (run2 >> 16);
+            pair_incl = warp_inclusive_scan(pair_sum);
+            if (lane == 31) s_scan[warp] = pair_incl;
         }
         __syncthreads();
-        if (tid < RADIX) {
-            uint32_t excl = incl - tile_cnt;
+        if (tid < PAIRS) {
+            uint32_t excl = pair_incl - pair_sum;
 #pragma unroll
             for (int w = 0; w < SCAN_WARPS; ++w)
                 if (w < warp) excl += s_scan[w];
-            s_excl[tid] = excl;
+            const uint32_t excl_hi = excl + (run2 & 0xFFFFu);
+            s_excl[2 * tid] = excl;
+            s_excl[2 * tid + 1] = excl_hi;
+            s_tcnt[2 * tid] = run2 & 0xFFFFu;
+            s_tcnt[2 * tid + 1] = run2 >> 16;
+            const uint32_t add2 = excl | (excl_hi << 16);
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w) s_wcnt[w * RADIX + tid] = static_cast<uint16_t>(s_wcnt[w * RADIX + tid] + excl);
-
+            for (int w = 0; w < WARPS; ++w) wc32[w * PAIRS + tid] += add2;
         }
         __syncthreads();
+        if (tid < RADIX) tile_cnt = s_tcnt[tid];
         phase(3);
 
         // ---- stage the tile in digit order (in place: keys are in registers)
@@ -458,7 +478,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         // (each warp's load covers 32 consecutive digits of one predecessor:
         // one coalesced 128-byte request per predecessor per warp)
         if (tid < RADIX) {
-            constexpr int LB_WIN = 32;
+            constexpr int LB_WIN = BSG_LB_WIN;
             uint32_t prefix = 0;
             if (tile > 0 && !(dbg & 1)) {
                 int64_t t = static_cast<int64_t>(tile) - 1;
