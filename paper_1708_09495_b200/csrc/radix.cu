@@ -274,7 +274,8 @@ struct OnesweepSmem {
 };
 
 // dbg bits (timing experiments only; output is wrong when set):
-//   1 = skip look-back waits, 2 = unstable atomic ranks instead of match/ballot.
+//   1 = skip look-back waits, 2 = trivial ranks, 4 = skip the write-out,
+//   8 = per-phase clock64 accumulation (bsg_debug_phase_cycles), 16 = skip staging.
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
 
     const uint32_t lt = lanemask_lt();
+    const uint32_t gt = ~(lt | (1u << lane));
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
     for (uint32_t k = 0;; ++k) {
         const int cur = k & 1;
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                     const uint32_t d =
                         ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)) : 0u;
                     const uint32_t before = ok ? wc[d] : 0u;
-                    const bool leader = (31 - __clz(peers[ii])) == lane;
+                    const bool leader = (peers[ii] & gt) == 0u; // highest peer: no peer above it
                     if (leader && ok) wc[d] = static_cast<uint16_t>(before + __popc(peers[ii]));
                     const uint32_t r = before + __popc(peers[ii] & lt);
                     __syncwarp();
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const uint32_t idx = wbase + i * 32 + lane;
-            if (full || idx < valid) {
+            if ((full || idx < valid) && !(dbg & 16)) {
                 const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
                 buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
             }
@@ -516,7 +518,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
         phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
         for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
-        if (full) {
+        if (dbg & 4) {
+            // timing experiment only: skip the write-out
+        } else if (full) {
 #pragma unroll 4
             for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = j * THREADS + tid;
