@@ -276,11 +276,17 @@ struct OnesweepSmem {
 // dbg bits (timing experiments only; output is wrong when set):
 //   1 = skip look-back waits, 2 = trivial ranks, 4 = skip the write-out,
 //   8 = per-phase clock64 accumulation (bsg_debug_phase_cycles), 16 = skip staging.
+// One stable pass over chunk_n keys of src (tiles claimed dynamically from
+// *tile_counter) into dst; digit_base[d] = destination index of digit d's
+// first key of the chunk.  `bar_parity` carries the two mbarriers' phase
+// parities across calls (the fused small-n sort runs several passes in one
+// launch); `init_bars` initialises them on the first call.
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
-__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
-    onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
-                    int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
-                    uint32_t* __restrict__ tile_counter, int use_tma, int dbg, int32_t neg1) {
+__device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const uint32_t* __restrict__ src,
+                                               uint32_t* __restrict__ dst, uint32_t chunk_n, int shift,
+                                               const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+                                               uint32_t* __restrict__ tile_counter, int use_tma, int dbg,
+                                               int32_t neg1, bool init_bars, uint32_t& bar_parity) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     using Off = typename L::Off;
     constexpr int RADIX = L::RADIX;
@@ -288,7 +294,6 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     constexpr int TILE = L::TILE;
     static_assert(ITEMS % 2 == 0, "ranks are packed in pairs");
     static_assert(RADIX <= THREADS, "one thread per digit");
-    extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
     uint16_t* s_wcnt = reinterpret_cast<uint16_t*>(smem + L::wcnt_off); // tile offsets < 2^16
     Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
@@ -298,9 +303,6 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
 
-    if (!plan->active[pass]) return;
-    const uint32_t* __restrict__ src = plan->src[pass] + chunk_off;
-    uint32_t* __restrict__ dst = plan->dst[pass];
     const uint32_t ntiles = (chunk_n + TILE - 1) / TILE;
 
     const int tid = threadIdx.x;
@@ -319,9 +321,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     };
 
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        fence_mbar_init();
+        if (init_bars) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            fence_mbar_init();
+        }
         const uint32_t t0 = atomicAdd(tile_counter, 1u);
         s_tile[0] = t0;
         issue(t0, 0);
@@ -355,7 +359,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                 t_ph = now;
             }
         };
-        mbar_wait_parity(&s_bar[cur], (k >> 1) & 1);
+        mbar_wait_parity(&s_bar[cur], (bar_parity >> cur) & 1u);
+        bar_parity ^= 1u << cur;
         phase(0);
 
         // ---- warp-local stable ranks + per-warp digit counts --------------
@@ -537,6 +542,19 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     }
 }
 
+template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
+__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
+    onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
+                    int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+                    uint32_t* __restrict__ tile_counter, int use_tma, int dbg, int32_t neg1) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    if (!plan->active[pass]) return;
+    uint32_t parity = 0;
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, RANK>(smem, plan->src[pass] + chunk_off, plan->dst[pass], chunk_n,
+                                                     shift, digit_base, status, tile_counter, use_tma, dbg, neg1,
+                                                     true, parity);
+}
+
 constexpr int kMinTile = 4096;
 
 // 0 = auto by n; otherwise a fixed THREADS x ITEMS row (see launch_onesweep_pass).
@@ -675,7 +693,189 @@ uint64_t status_words_for(uint64_t n) {
 
 } // namespace
 
-uint64_t onesweep_status_words(uint64_t n) { return status_words_for<8>(n); }
+// ---------------------------------------------------------------------------
+// Fused small-n SR4 (C1: latency, SURVEY §8(d) "CUDA Graph or persistent
+// kernel"): one cooperative launch runs the 4-digit histogram, the digit
+// scans + pass plan (computed redundantly by every CTA), and the four
+// one-sweep passes, with grid barriers in between, instead of ~10 launches.
+// Workspace (zeroed by one memset): hist[4][256] | barrier word (+31 pad) |
+// 4 x per-pass look-back regions [tile counter (+31)][tiles][256].
+// ---------------------------------------------------------------------------
+constexpr int kSmallThreads = 512, kSmallItems = 16;
+constexpr uint64_t kSmallMaxKeys = uint64_t{1} << 21;
+constexpr int kSmallHistCopies = 4;
+
+uint64_t small_region_words(uint64_t n) {
+    constexpr uint64_t tile = kSmallThreads * kSmallItems;
+    return 32 + ((n + tile - 1) / tile) * 256;
+}
+uint64_t small_ws_words(uint64_t n) { return 1024 + 32 + 4 * small_region_words(n); }
+
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (ld_acquire_gpu(ctr) < target) __nanosleep(64);
+        __threadfence();
+        fence_proxy_async_global(); // next pass's TMA loads read the previous pass's stores
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 2)
+    small_sort_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t* __restrict__ tmp,
+                      uint32_t n, uint32_t* __restrict__ ws, uint32_t region_words, int use_tma, int32_t neg1) {
+    using L = OnesweepSmem<8, kSmallThreads, kSmallItems, false>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* s_base = reinterpret_cast<uint64_t*>(smem + L::bytes); // [4][256]
+    __shared__ const uint32_t* s_src[4];
+    __shared__ uint32_t* s_dst[4];
+    __shared__ int s_active[4];
+    __shared__ const uint32_t* s_final;
+    __shared__ int s_copy;
+    __shared__ uint64_t s_warp[kSmallThreads / 32];
+    uint32_t* g_hist = ws;
+    uint32_t* g_bar = ws + 1024;
+    uint32_t* regions = ws + 1056;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t G = gridDim.x;
+
+    // ---- digit histograms of all four passes (replicated smem counters) --
+    uint32_t* s_h = reinterpret_cast<uint32_t*>(smem); // aliases the tile buffers
+    for (int i = tid; i < kSmallHistCopies * 1024; i += kSmallThreads) s_h[i] = 0;
+    __syncthreads();
+    {
+        uint32_t* h = s_h + (warp % kSmallHistCopies) * 1024;
+        const uint32_t stride = G * kSmallThreads;
+        for (uint32_t i = blockIdx.x * kSmallThreads + tid; i < n; i += stride) {
+            const uint32_t k = __ldg(in + i);
+            atomicAdd(&h[k & 255u], 1u);
+            atomicAdd(&h[256 + ((k >> 8) & 255u)], 1u);
+            atomicAdd(&h[512 + ((k >> 16) & 255u)], 1u);
+            atomicAdd(&h[768 + (k >> 24)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < 1024; i += kSmallThreads) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int c = 0; c < kSmallHistCopies; ++c) v += s_h[c * 1024 + i];
+        if (v) atomicAdd(&g_hist[i], v);
+    }
+    uint32_t bar_target = G;
+    grid_barrier(g_bar, bar_target);
+
+    // ---- digit bases + pass plan (scan_plan_kernel's logic, per CTA) -------
+    for (int p = 0; p < 4; ++p) {
+        const uint32_t total = tid < 256 ? __ldcg(&g_hist[p * 256 + tid]) : 0u;
+        const int ident = __syncthreads_or(tid < 256 && total == n);
+        const uint64_t incl = warp_inclusive_scan(static_cast<uint64_t>(total));
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        uint64_t excl = incl - total;
+        for (int w = 0; w < warp; ++w) excl += s_warp[w];
+        if (tid < 256) s_base[p * 256 + tid] = excl;
+        if (tid == 0) s_active[p] = !ident;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        int m = 0;
+        for (int p = 0; p < 4; ++p) m += s_active[p];
+        const bool forward = (in == out) && (m % 2 == 1);
+        const uint32_t* cur = in;
+        int j = 0;
+        for (int p = 0; p < 4; ++p) {
+            s_src[p] = nullptr;
+            s_dst[p] = nullptr;
+            if (!s_active[p]) continue;
+            uint32_t* d = forward ? ((j % 2 == 0) ? tmp : out) : (((m - 1 - j) % 2 == 0) ? out : tmp);
+            s_src[p] = cur;
+            s_dst[p] = d;
+            cur = d;
+            ++j;
+        }
+        s_final = cur;
+        s_copy = cur != out;
+    }
+    __syncthreads();
+
+    // ---- the executed passes, one grid barrier after each ------------------
+    uint32_t parity = 0;
+    bool first = true;
+    for (int p = 0; p < 4; ++p) {
+        if (!s_active[p]) continue;
+        uint32_t* region = regions + static_cast<uint64_t>(p) * region_words;
+        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0>(smem, s_src[p], s_dst[p], n, 8 * p,
+                                                               s_base + p * 256, region + 32, region, use_tma, 0,
+                                                               neg1, first, parity);
+        first = false;
+        bar_target += G;
+        grid_barrier(g_bar, bar_target);
+    }
+    if (s_copy) {
+        const uint32_t* src = s_final;
+        for (uint32_t i = blockIdx.x * kSmallThreads + tid; i < n; i += G * kSmallThreads) out[i] = __ldcg(src + i);
+    }
+}
+
+int& small_sort_flag() {
+    static int on = [] {
+        const char* e = getenv("BSG_SMALL");
+        return e ? atoi(e) : 1;
+    }();
+    return on;
+}
+bool small_sort_enabled() { return small_sort_flag() != 0; }
+
+// Returns launches (1) or 0 when the fused path does not apply, -1 on error.
+int launch_small_sort(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws, cudaStream_t stream,
+                      bool tma) {
+    if (n == 0 || n > kSmallMaxKeys || !small_sort_enabled()) return 0;
+    using L = OnesweepSmem<8, kSmallThreads, kSmallItems, false>;
+    const size_t smem = L::bytes + 4 * 256 * sizeof(uint64_t);
+    static int per_sm = -1;
+    static int sms = 0;
+    if (per_sm < 0) {
+        cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_sort_kernel, kSmallThreads, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (per_sm < 1) return 0;
+    const uint64_t region = small_region_words(n);
+    if (cudaMemsetAsync(ws.status, 0, small_ws_words(n) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    // grid: every tile gets a CTA, at least one CTA per SM for the histogram
+    // (measured: 2^20 keys 56 us at 148 CTAs vs 59 us at all 296 resident)
+    static const int gmin = [] {
+        const char* e = getenv("BSG_SMALL_GRID");
+        return e ? atoi(e) : kSmCountB200;
+    }();
+    const uint64_t tiles = (n + kSmallThreads * kSmallItems - 1) / (kSmallThreads * kSmallItems);
+    unsigned grid = static_cast<unsigned>(per_sm * sms);
+    if (gmin > 0) grid = static_cast<unsigned>(std::min<uint64_t>(grid, std::max<uint64_t>(tiles, gmin)));
+    const uint32_t* a_in = in;
+    uint32_t* a_out = out;
+    uint32_t* a_tmp = ws.tmp;
+    uint32_t a_n = static_cast<uint32_t>(n);
+    uint32_t* a_ws = ws.status;
+    uint32_t a_region = static_cast<uint32_t>(region);
+    int a_tma = tma ? 1 : 0;
+    int32_t a_neg1 = -1;
+    void* args[] = {&a_in, &a_out, &a_tmp, &a_n, &a_ws, &a_region, &a_tma, &a_neg1};
+    TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(small_sort_kernel), dim3(grid), dim3(kSmallThreads),
+                                    args, smem, stream) != cudaSuccess)
+        return -1;
+    return 1;
+}
+
+uint64_t onesweep_status_words(uint64_t n) {
+    const uint64_t w = status_words_for<8>(n);
+    return n <= kSmallMaxKeys ? std::max<uint64_t>(w, small_ws_words(n)) : w;
+}
+
 
 int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws,
                        cudaStream_t stream, bool allow_tma) {
@@ -683,6 +883,12 @@ int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const Radi
     constexpr int RADIX = 256;
     const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
     int launches = 0;
+    {
+        const bool tma = allow_tma && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
+                                        reinterpret_cast<uintptr_t>(ws.tmp)) & 15) == 0;
+        const int l = launch_small_sort(in, out, n, ws, stream, tma);
+        if (l != 0) return l;
+    }
     if (cudaMemsetAsync(ws.hist, 0, chunks * PASSES * RADIX * sizeof(uint32_t), stream) != cudaSuccess) return -1;
     for (uint64_t c = 0; c < chunks && n; ++c) {
         const uint64_t off = c * kChunkKeys;
@@ -801,6 +1007,14 @@ int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uin
 extern "C" int bsg_debug_set_onesweep_cfg(int cfg) {
     const int prev = bsg::onesweep_cfg_ref();
     bsg::onesweep_cfg_ref() = cfg;
+    return prev;
+}
+
+// Test aid: enables/disables the fused small-n sort (n <= 2^21); returns the
+// previous setting.
+extern "C" int bsg_debug_set_small_sort(int on) {
+    const int prev = bsg::small_sort_flag();
+    bsg::small_sort_flag() = on;
     return prev;
 }
 

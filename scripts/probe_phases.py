@@ -4,7 +4,7 @@ os.environ["BSG_OS_DBG"] = str(int(os.environ.get("BSG_OS_DBG", "0")) | 8)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1708_09495_b200 import _lib
-n = 1 << 28
+n = 1 << int(os.environ.get("LGN", "28"))
 t = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device='cuda')
 out = torch.empty_like(t)
 ctx = _lib.context(0); L = _lib.lib(); st = torch.cuda.current_stream().cuda_stream
@@ -21,7 +21,7 @@ ms, cnt = ctx.kernel_time(_lib.K_ONESWEEP)
 L.bsg_debug_phase_cycles(buf, 1)
 names = ["tma_wait", "rank(warp0)", "barrier_after_rank", "scan+2syncs", "staging(warp0)", "lookback(warp0)", "write(warp0)", "barrier_after_lookback"]
 tot = sum(buf[:8])
-ctas = 148 * 3
+ctas = min(148, (n + 8191) // 8192) * 3  # approximate for small n
 print(f"kernel {ms/cnt:.3f} ms/launch; cycles per CTA per launch ~ {ms/cnt*1e-3*1.95e9:.0f}")
 for i in range(8):
     print(f"{names[i]:22s} {buf[i]/ctas:12.0f} cycles/CTA  {buf[i]/tot*100:5.1f}%")

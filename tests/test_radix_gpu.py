@@ -186,3 +186,28 @@ def test_auto_configuration_boundaries(cuda, bsg, orc):
     for n in ((1 << 21), (1 << 21) + 1, (1 << 23) + 1):
         keys = orc.generate_uniform_keys(n, n)
         np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), orc.serial_radix_sort(keys, 256))
+
+
+@pytest.mark.parametrize("small", [0, 1])
+def test_small_n_both_paths(cuda, bsg, orc, small):
+    """n <= 2^21 runs the fused cooperative sort (one launch); the multi-launch
+    path must agree too.  Includes identity passes (narrow keys) and in-place."""
+    L = bsg._lib.lib()
+    prev = L.bsg_debug_set_small_sort(small)
+    try:
+        for n in (1, 2, 31, 8191, 8193, 100000, (1 << 20) + 3, 1 << 21):
+            keys = orc.generate_uniform_keys(n, 5 * n + small)
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), orc.serial_radix_sort(keys, 256))
+        for mask in (0xFF, 0xFF00FF, 0):  # 3, 2 and 0 identity passes
+            keys = orc.generate_uniform_keys(70001, 3) & np.uint32(mask)
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+        torch = cuda
+        keys = orc.generate_uniform_keys(300007, 11)
+        t = torch.from_numpy(keys.view(np.int32)).cuda()
+        ctx = bsg._lib.context(0)
+        st = torch.cuda.current_stream().cuda_stream
+        assert L.bsg_radix_sort_u32(ctx.handle, t.data_ptr(), t.data_ptr(), keys.size, 8, 1, st) == 0  # in place
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32), np.sort(keys))
+    finally:
+        L.bsg_debug_set_small_sort(prev)
