@@ -7,9 +7,13 @@ N = 1 (default): config 2 of BASELINE.json -- single-GPU LSD radix sort (SR4:
 radix 2^8, 4 stable count-sort rounds) of n = 2^28 uint32 keys drawn by the
 reference generator (generate_uniform_keys, core.hpp:93-99, seed
 derive_seed(1, 0), bench.hpp:86-88), device-resident; a step is one full sort.
-N > 1 (torchrun, one rank per GPU): the paper's PR4 parallel radix sort over
-NCCL, weak scaling with 2^28 keys per GPU (block-distributed; rank w's block
-is generate_uniform_keys(2^28, derive_seed(1, w))).
+N > 1 (torchrun, one rank per GPU): the paper's PR4 parallel radix sort,
+weak scaling with 2^28 keys per GPU (block-distributed; rank w's block is
+generate_uniform_keys(2^28, derive_seed(1, w))).  Default --pr-variant P:
+each round is ONE one-sweep pass per rank that stores every key at its final
+position in its owner's CUDA-IPC-mapped block over NVLink (counts all-gathered
+with NCCL; a 1-element all-reduce closes the round); A = the same rounds with
+NCCL all-to-all-v + rebuild; B = single NCCL exchange + local sort.
 
 --impl reference: the reference's own CPU implementation (its unmodified
 headers compiled into oracle/_ref/libbspref.so, else the oracle port) on
@@ -193,6 +197,11 @@ def _config(world: int, variant=None):
     if variant == "A":
         what = ("PR4 as run_parallel_radix: per round digit count + NCCL all-gather of counts + NCCL all-to-all-v "
                 "of keys + rebuild (4 exchanges; per-round states bit-identical to the reference)")
+    elif variant == "P":
+        what = ("PR4 as run_parallel_radix with the exchange fused into the pass: per round digit count + NCCL "
+                "all-gather of counts + ONE one-sweep pass per rank whose write-out stores every key at its final "
+                "position in its owner's IPC-mapped next-round block over NVLink + a 1-element all-reduce barrier "
+                "(per-round states bit-identical to the reference; the exchange timing covers pass + barrier)")
     else:
         what = ("variant B: top-digit histogram + NCCL all-gather of counts + one stable partition pass + ONE NCCL "
                 "all-to-all-v + local LSD sort (BASELINE config-5 formulation; same sorted concatenation)")
@@ -308,9 +317,28 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     d_in = torch.from_numpy(keys.view(np.int32)).to(dev)
     ctx = _lib.context(local_rank)
 
+    peer = None
+    if args.pr_variant == "P":
+        # map every rank's next-round blocks (CUDA IPC); if any rank cannot,
+        # all ranks agree to run variant B instead and say so in the JSON line
+        try:
+            peer = D.PeerBlocks(n_total, device=dev)
+            okflag = 1
+        except Exception as exc:  # noqa: BLE001
+            print(f"rank {rank}: peer mapping failed ({exc}); falling back to variant B", file=sys.stderr)
+            okflag = 0
+        flag = torch.tensor([okflag], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            args.fallback_from = "P"
+            args.pr_variant = "B"
+            peer = None
+
     def step(events=None):
         if args.pr_variant == "A":
             return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events)
+        if args.pr_variant == "P":
+            return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events, exchange="peer", peer=peer)
         return D.parallel_radix_sort_single_exchange(d_in, a2a_events=events)
 
     for _ in range(args.warmup):
@@ -356,6 +384,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         blk = h_in.to(dev, non_blocking=True)
         if args.pr_variant == "A":
             res = D.parallel_radix_sort(blk, n_total, radix=256)
+        elif args.pr_variant == "P":
+            res = D.parallel_radix_sort(blk, n_total, radix=256, exchange="peer", peer=peer)
         else:
             res = D.parallel_radix_sort_single_exchange(blk)
         h_out[: res.numel()].copy_(res, non_blocking=True)
@@ -377,7 +407,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": n_total / (ms_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference generator, seeded per rank)",
-            "config": _config(world, args.pr_variant),
+            "config": dict(_config(world, args.pr_variant),
+                           **({"fallback_from": args.fallback_from} if getattr(args, "fallback_from", None) else {})),
             "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_total,
                     "d2h_bytes_per_step": 4 * n_total, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
@@ -397,8 +428,9 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
     ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pr-variant", choices=["A", "B"], default="B",
-                    help="multi-GPU algorithm: A = per-round PR4 (4 exchanges), B = single exchange")
+    ap.add_argument("--pr-variant", choices=["A", "B", "P"], default="P",
+                    help="multi-GPU algorithm: A = per-round PR4 (4 NCCL exchanges), B = single exchange, "
+                         "P = per-round PR4 with the exchange + rebuild as one peer-store kernel over NVLink")
     ap.add_argument("--distributed", action="store_true",
                     help="run the NCCL PR path even with one rank (exercises the multi-GPU code on one GPU)")
     args = ap.parse_args()

@@ -205,6 +205,33 @@ int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len,
                    const uint64_t* recv_counts, int p, int round, int radix_log2,
                    const int64_t* rebuild_delta, uint32_t* block, void* stream);
 
+/* Fused exchange + rebuild over peer memory (NVLink): replaces the
+ * all-to-all-v of sort_and_scatter (radix.hpp:275-290) and gather_slices
+ * (radix.hpp:295-333) for one round of worker `me`.  `sorted` is me's block
+ * after its local stable pass (bsg_pr_local_sort), `counts_all` the gathered
+ * p x r digit-count matrix (device).  Every key is stored directly at its
+ * position in the next-round block of its owner: peer_blocks[w] (host array
+ * of p device pointers, CUDA-IPC mapped for w != me) holds worker w's
+ * Partition(n, p) block.  The caller orders the round with a barrier across
+ * workers after this call (all stores land before any owner reads). */
+int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_t len,
+                        const uint64_t* counts_all, uint64_t n, int p, int me,
+                        int round, int radix_log2, uint32_t* const* peer_blocks,
+                        void* stream);
+
+/* One whole PR round of worker `me` as ONE pass (r <= 2^8): the local stable
+ * pass of sort_and_scatter (radix.hpp:262-270) writes every key of `block`
+ * (me's current block, len = size_of(me)) directly at its final position in
+ * its owner's next-round block (peer_blocks as in bsg_pr_peer_scatter), i.e.
+ * count_sort_round + all-to-all-v + gather_slices fused.  counts_all is the
+ * gathered p x r count matrix of this round (bsg_pr_count_digits on every
+ * worker).  For r = 2^16 the call runs bsg_pr_local_sort + the peer scatter.
+ * Same ordering contract as bsg_pr_peer_scatter. */
+int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t len,
+                       const uint64_t* counts_all, uint64_t n, int p, int me,
+                       int round, int radix_log2, uint32_t* const* peer_blocks,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

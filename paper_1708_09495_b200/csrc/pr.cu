@@ -20,6 +20,7 @@
 // scatter of the sorted blocks.  Across GPUs,
 // paper_1708_09495_b200/distributed.py interleaves the count / plan / local /
 // rebuild steps with NCCL all-gather / all-to-all-v.
+#include <mutex>
 #include <algorithm>
 #include <vector>
 
@@ -357,6 +358,53 @@ __global__ void __launch_bounds__(kDigChunk)
             if (s_send[w]) atomicAdd(reinterpret_cast<unsigned long long*>(send_counts + w), s_send[w]);
 }
 
+// ---- fused exchange + rebuild over peer memory (bsg_pr_peer_scatter) -----
+// gd[d] = digit_start[d] + sum_{u<me} cnt(u,d) - ls(me,d): the destination of
+// key i (digit d) of me's sorted block is gd[d] + i (radix.hpp:257-290).
+// `before` holds sum_{u<me} cnt(u,d) (pr_plan_col_kernel's delta row me).
+__global__ void __launch_bounds__(kDigChunk)
+    pr_peer_gd_kernel(const uint64_t* __restrict__ cnt_me, const int64_t* __restrict__ before,
+                      const uint64_t* __restrict__ dstart, int radix, int64_t* __restrict__ gd) {
+    __shared__ uint64_t s_part[kDigChunk / 32];
+    // row prefix of me's counts up to this chunk
+    uint64_t acc = 0;
+    for (int d = threadIdx.x; d < static_cast<int>(blockIdx.x) * kDigChunk; d += kDigChunk) acc += cnt_me[d];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    uint64_t lbase = 0;
+    for (int w = 0; w < kDigChunk / 32; ++w) lbase += s_part[w];
+    const int d = blockIdx.x * kDigChunk + threadIdx.x;
+    const uint64_t c = d < radix ? cnt_me[d] : 0;
+    uint64_t ex;
+    chunk_excl_scan(c, ex);
+    if (d < radix)
+        gd[d] = static_cast<int64_t>(dstart[d]) + before[d] - static_cast<int64_t>(lbase + ex);
+}
+
+// Owner by p boundary compares (no per-key division, cf. radix.hpp:113-117).
+__global__ void __launch_bounds__(kScatterThreads)
+    pr_peer_scatter_kernel(const uint32_t* __restrict__ sorted, uint64_t len, int shift, uint32_t mask,
+                           const int64_t* __restrict__ gd, int p, const __grid_constant__ PeerTable tab) {
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * kScatterThreads;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kScatterThreads + threadIdx.x; i < len; i += step) {
+        const uint32_t key = __ldg(sorted + i);
+        const uint64_t pos = static_cast<uint64_t>(__ldg(gd + ((key >> shift) & mask)) + static_cast<int64_t>(i));
+        int w = 0;
+        for (int j = 1; j < p; ++j) w += pos >= tab.offset[j] ? 1 : 0;
+        tab.blocks[w][pos - tab.offset[w]] = key;
+    }
+    __threadfence_system(); // peer stores performed before the round's barrier
+}
+
+// digit_base[d] = digit_start[d] + sum_{u<me} cnt(u,d): global position of
+// the first digit-d key of me's block (one-sweep digit bases of the fused round)
+__global__ void pr_fused_base_kernel(const uint64_t* __restrict__ dstart, const int64_t* __restrict__ before_me,
+                                     int radix, uint64_t* __restrict__ base) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d < radix) base[d] = dstart[d] + static_cast<uint64_t>(before_me[d]);
+}
+
 } // namespace
 
 int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int bits, uint64_t* counts,
@@ -573,5 +621,133 @@ extern "C" int bsg_pr_plan_host(const uint64_t* counts, uint64_t n, int p, int m
         for (uint64_t d = 0; d < r; ++d) rebuild_delta[static_cast<uint64_t>(v) * r + d] += adj;
         recv_off += recv_counts[v];
     }
+    return BSG_OK;
+}
+
+// Fused exchange + rebuild of one PR round for worker `me` (see bsg.h).
+extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_t len, const uint64_t* counts_all,
+                                   uint64_t n, int p, int me, int round, int radix_log2, uint32_t* const* peer_blocks,
+                                   void* stream) {
+    using namespace bsg;
+    if (!ctx) return fail(BSG_EINVAL, "null context");
+    if (radix_log2 != 1 && radix_log2 != 2 && radix_log2 != 4 && radix_log2 != 8 && radix_log2 != 16)
+        return fail(BSG_EINVAL, "radix must be a power of two whose bit width divides 32");
+    if (p < 1 || p > kPeerMax || me < 0 || me >= p) return fail(BSG_EINVAL, "peer scatter: worker index out of range");
+    if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
+    if (len != bsg_partition_size_of(n, p, me)) return fail(BSG_EINVAL, "peer scatter: block size != size_of(me)");
+    if (!peer_blocks || !counts_all || (len && !sorted)) return fail(BSG_EINVAL, "null pointer");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dev(ctx->device);
+    tl_timer = &ctx->timer;
+    const int radix = 1 << radix_log2;
+    const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // scratch: before/delta [p][r] (int64), coltot [r], dstart [r], colchunk [chunks], gd [r]
+    const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks;
+    cudaError_t e = ctx->pr_delta.ensure(words * 8);
+    if (e != cudaSuccess) {
+        tl_timer = nullptr;
+        return cuda_fail(e, "peer scatter workspace");
+    }
+    int64_t* before = ctx->pr_delta.as<int64_t>();
+    uint64_t* coltot = reinterpret_cast<uint64_t*>(before + static_cast<uint64_t>(p) * radix);
+    uint64_t* dstart = coltot + radix;
+    int64_t* gd = reinterpret_cast<int64_t*>(dstart + radix);
+    uint64_t* colchunk = reinterpret_cast<uint64_t*>(gd + radix);
+    PeerTable tab{};
+    for (int w = 0; w < p; ++w) {
+        if (!peer_blocks[w] && bsg_partition_size_of(n, p, w)) {
+            tl_timer = nullptr;
+            return fail(BSG_EINVAL, "peer scatter: null peer block");
+        }
+        tab.blocks[w] = peer_blocks[w];
+        tab.offset[w] = bsg_partition_offset_of(n, p, w);
+    }
+    tab.offset[p] = n;
+    {
+        TimedScope ts(3 /*BSG_K_PR*/, st);
+        pr_plan_col_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all, p, radix, before, coltot, colchunk);
+        pr_digit_start_kernel<<<chunks, kDigChunk, 0, st>>>(coltot, colchunk, radix, dstart);
+        pr_peer_gd_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all + static_cast<uint64_t>(me) * radix,
+                                                        before + static_cast<uint64_t>(me) * radix, dstart, radix, gd);
+        ctx->launches += 3;
+        if (len) {
+            const uint64_t want = (len + kScatterThreads * kScatterItems - 1) / (kScatterThreads * kScatterItems);
+            const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
+            pr_peer_scatter_kernel<<<grid, kScatterThreads, 0, st>>>(sorted, len, round * radix_log2,
+                                                                     static_cast<uint32_t>(radix - 1), gd, p, tab);
+            ctx->launches += 1;
+        }
+    }
+    e = cudaPeekAtLastError();
+    tl_timer = nullptr;
+    if (e != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer scatter launch");
+    return BSG_OK;
+}
+
+// A whole PR round fused with its exchange (see bsg.h).
+extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t len, const uint64_t* counts_all,
+                                  uint64_t n, int p, int me, int round, int radix_log2, uint32_t* const* peer_blocks,
+                                  void* stream) {
+    using namespace bsg;
+    if (!ctx) return fail(BSG_EINVAL, "null context");
+    if (radix_log2 != 1 && radix_log2 != 2 && radix_log2 != 4 && radix_log2 != 8 && radix_log2 != 16)
+        return fail(BSG_EINVAL, "radix must be a power of two whose bit width divides 32");
+    if (p < 1 || p > kPeerMax || me < 0 || me >= p) return fail(BSG_EINVAL, "fused round: worker index out of range");
+    if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
+    if (len != bsg_partition_size_of(n, p, me)) return fail(BSG_EINVAL, "fused round: block size != size_of(me)");
+    if (len > kChunkKeys) return fail(BSG_EINVAL, "fused round: block larger than 2^29 keys");
+    if (!peer_blocks || !counts_all || (len && !block)) return fail(BSG_EINVAL, "null pointer");
+    if (radix_log2 == 16) {
+        cudaError_t e;
+        {
+            std::lock_guard<std::mutex> lock(ctx->mu);
+            DeviceGuard dev(ctx->device);
+            e = ctx->pr_sorted.ensure(std::max<uint64_t>(len, 4) * 4);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "fused round workspace");
+        uint32_t* sorted = ctx->pr_sorted.as<uint32_t>();
+        if (int rc = bsg_count_sort_round_u32(ctx, block, sorted, len, round, radix_log2, BSG_MEM_DEVICE, stream))
+            return rc;
+        return bsg_pr_peer_scatter(ctx, sorted, len, counts_all, n, p, me, round, radix_log2, peer_blocks, stream);
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dev(ctx->device);
+    tl_timer = &ctx->timer;
+    struct Reset {
+        ~Reset() { tl_timer = nullptr; }
+    } reset;
+    const int radix = 1 << radix_log2;
+    const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks;
+    cudaError_t e = ctx->pr_delta.ensure(words * 8);
+    if (e == cudaSuccess) e = ctx->status.ensure(onesweep_status_words(std::max<uint64_t>(len, 1)) * sizeof(uint32_t));
+    if (e != cudaSuccess) return cuda_fail(e, "fused round workspace");
+    int64_t* before = ctx->pr_delta.as<int64_t>();
+    uint64_t* coltot = reinterpret_cast<uint64_t*>(before + static_cast<uint64_t>(p) * radix);
+    uint64_t* dstart = coltot + radix;
+    uint64_t* base = dstart + radix;
+    uint64_t* colchunk = base + radix;
+    PeerTable tab{};
+    for (int w = 0; w < p; ++w) {
+        if (!peer_blocks[w] && bsg_partition_size_of(n, p, w)) return fail(BSG_EINVAL, "fused round: null peer block");
+        tab.blocks[w] = peer_blocks[w];
+        tab.offset[w] = bsg_partition_offset_of(n, p, w);
+    }
+    tab.offset[p] = n;
+    {
+        TimedScope ts(3 /*BSG_K_PR*/, st);
+        pr_plan_col_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all, p, radix, before, coltot, colchunk);
+        pr_digit_start_kernel<<<chunks, kDigChunk, 0, st>>>(coltot, colchunk, radix, dstart);
+        pr_fused_base_kernel<<<(radix + 255) / 256, 256, 0, st>>>(dstart, before + static_cast<uint64_t>(me) * radix,
+                                                                 radix, base);
+        ctx->launches += 3;
+    }
+    const int l = launch_onesweep_peer(block, len, radix_log2, round * radix_log2, base, ctx->status.as<uint32_t>(),
+                                       tab, p, st);
+    if (l < 0) return cuda_fail(cudaGetLastError(), "fused round launch");
+    ctx->launches += static_cast<uint64_t>(l);
+    if ((e = cudaPeekAtLastError()) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fused round launch");
     return BSG_OK;
 }

@@ -281,9 +281,29 @@ struct OnesweepSmem {
 // first key of the chunk.  `bar_parity` carries the two mbarriers' phase
 // parities across calls (the fused small-n sort runs several passes in one
 // launch); `init_bars` initialises them on the first call.
-template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
+// Output sinks of the write-out: one array, or the owners' blocks of a PR round.
+struct PlainSink {
+    uint32_t* __restrict__ dst;
+    template <typename Off>
+    __device__ __forceinline__ void store(Off pos, uint32_t key) const {
+        dst[pos] = key;
+    }
+};
+struct PeerSink {
+    const PeerTable* tab; // kernel parameter space
+    int p;
+    template <typename Off>
+    __device__ __forceinline__ void store(Off pos, uint32_t key) const {
+        const uint64_t g = static_cast<uint64_t>(pos);
+        int w = 0;
+        for (int j = 1; j < p; ++j) w += g >= tab->offset[j] ? 1 : 0; // owner: p compares, no division
+        tab->blocks[w][g - tab->offset[w]] = key;
+    }
+};
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK, typename Sink = PlainSink>
 __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const uint32_t* __restrict__ src,
-                                               uint32_t* __restrict__ dst, uint32_t chunk_n, int shift,
+                                               Sink dst, uint32_t chunk_n, int shift,
                                                const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                                                uint32_t* __restrict__ tile_counter, int use_tma, int dbg,
                                                int32_t neg1, bool init_bars, uint32_t& bar_parity) {
@@ -530,12 +550,12 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = j * THREADS + tid;
                 const uint32_t key = buf[i];
-                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
+                dst.store(static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i), key);
             }
         } else {
             for (uint32_t i = tid; i < valid; i += THREADS) {
                 const uint32_t key = buf[i];
-                dst[static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i)] = key;
+                dst.store(static_cast<Off>(s_delta[digit_of_key<BITS>(key, shift)] + i), key);
             }
         }
         phase(6);
@@ -550,7 +570,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     extern __shared__ __align__(128) uint8_t smem[];
     if (!plan->active[pass]) return;
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, RANK>(smem, plan->src[pass] + chunk_off, plan->dst[pass], chunk_n,
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, RANK>(smem, plan->src[pass] + chunk_off, PlainSink{plan->dst[pass]}, chunk_n,
                                                      shift, digit_base, status, tile_counter, use_tma, dbg, neg1,
                                                      true, parity);
 }
@@ -806,7 +826,7 @@ __global__ void __launch_bounds__(kSmallThreads, 2)
     for (int p = 0; p < 4; ++p) {
         if (!s_active[p]) continue;
         uint32_t* region = regions + static_cast<uint64_t>(p) * region_words;
-        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0>(smem, s_src[p], s_dst[p], n, 8 * p,
+        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0>(smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p,
                                                                s_base + p * 256, region + 32, region, use_tma, 0,
                                                                neg1, first, parity);
         first = false;
@@ -869,6 +889,66 @@ int launch_small_sort(const uint32_t* in, uint32_t* out, uint64_t n, const Radix
                                     args, smem, stream) != cudaSuccess)
         return -1;
     return 1;
+}
+
+// ---------------------------------------------------------------------------
+// PR round fused with its exchange (launch_onesweep_peer, see radix.cuh).
+// ---------------------------------------------------------------------------
+template <int BITS, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
+    onesweep_peer_kernel(const uint32_t* __restrict__ src, uint32_t len, int shift,
+                         const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+                         uint32_t* __restrict__ tile_counter, int use_tma, int32_t neg1,
+                         const __grid_constant__ PeerTable tab, int p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t parity = 0;
+    onesweep_tiles<BITS, THREADS, ITEMS, false, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
+                                                              status, tile_counter, use_tma, 0, neg1, true, parity);
+    __threadfence_system(); // peer stores performed before the round's barrier
+}
+
+template <int BITS, int THREADS, int ITEMS>
+int launch_onesweep_peer_cfg(const uint32_t* block, uint32_t len, int shift, const uint64_t* digit_base,
+                             uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream) {
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, false>;
+    auto kern = onesweep_peer_kernel<BITS, THREADS, ITEMS>;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, L::bytes);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int sms = kSmCountB200, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    constexpr int RADIX = 1 << BITS;
+    const uint32_t tiles = (len + L::TILE - 1) / L::TILE;
+    const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
+    if (cudaMemsetAsync(status, 0, (32 + static_cast<uint64_t>(tiles) * RADIX) * sizeof(uint32_t), stream) !=
+        cudaSuccess)
+        return -1;
+    const bool tma = (reinterpret_cast<uintptr_t>(block) & 15) == 0;
+    TimedScope ts(3 /*BSG_K_PR*/, stream);
+    kern<<<grid, THREADS, L::bytes, stream>>>(block, len, shift, digit_base, status + 32, status, tma ? 1 : 0, -1,
+                                              tab, p);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
+                         uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream) {
+    if (len == 0) return 0;
+    if (len > kChunkKeys) return -1;
+    const uint32_t n = static_cast<uint32_t>(len);
+    switch (bits) {
+    case 1: return launch_onesweep_peer_cfg<1, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
+    case 2: return launch_onesweep_peer_cfg<2, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
+    case 4: return launch_onesweep_peer_cfg<4, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
+    case 8:
+        if (len > (uint64_t{1} << 23))
+            return launch_onesweep_peer_cfg<8, 1024, 24>(block, n, shift, digit_base, status, tab, p, stream);
+        return launch_onesweep_peer_cfg<8, 512, 16>(block, n, shift, digit_base, status, tab, p, stream);
+    default: return -1;
+    }
 }
 
 uint64_t onesweep_status_words(uint64_t n) {

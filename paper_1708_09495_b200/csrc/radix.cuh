@@ -51,4 +51,19 @@ int launch_count_pass(const uint32_t* in, uint32_t* out, uint64_t n, int bits, i
 int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uint64_t* counts,
                         uint32_t* scratch32, cudaStream_t stream);
 
+// Next-round blocks of all PR workers as seen from this process (own block
+// local, others CUDA-IPC mapped over NVLink) and their Partition offsets.
+constexpr int kPeerMax = 64;
+struct PeerTable {
+    uint32_t* blocks[kPeerMax];
+    uint64_t offset[kPeerMax + 1]; // Partition(n, p).offset_of(w); offset[p] = n
+};
+
+// One PR round fused with its exchange (r <= 2^8): a one-sweep pass over the
+// worker's block whose digit bases are the global positions of the block's
+// first key per digit (digit_base, device [radix]); every key is stored at
+// its final position in its owner's block.  len <= kChunkKeys.
+int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
+                         uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream);
+
 } // namespace bsg

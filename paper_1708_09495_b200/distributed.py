@@ -16,6 +16,13 @@ The block a rank holds after round k is bit-identical to worker `rank`'s
 block in run_parallel_radix with plan.rounds = k.  The only host round trip
 per round is the 2p split sizes NCCL's all-to-all-v needs on the host.
 
+With ``exchange="peer"`` the all-to-all-v and the rebuild
+are one kernel: every rank maps the next-round blocks of all ranks into its
+address space (CUDA IPC, NVLink) and stores each key of its sorted block
+straight at its final position in the owner's block; a barrier (a 1-element
+NCCL all-reduce) closes the round.  No send/receive buffers, no host round
+trip for split sizes.
+
 `parallel_radix_sort_single_exchange` is variant B of SURVEY §8(e) (the
 BASELINE config-5 formulation: one exchange, then a local sort).
 
@@ -84,6 +91,20 @@ class CudaStepOps:
                                              _lib.MEM_DEVICE, self._stream()), "local sort")
         return out
 
+    def peer_scatter(self, sorted_: torch.Tensor, counts_all: torch.Tensor, n: int, p: int, me: int, rnd: int,
+                     bits: int, peer_ptrs) -> None:
+        arr = (ctypes.c_void_p * p)(*peer_ptrs)
+        _lib.check(self.L.bsg_pr_peer_scatter(self.ctx.handle, sorted_.data_ptr(), sorted_.numel(),
+                                              counts_all.data_ptr(), n, p, me, rnd, bits, arr, self._stream()),
+                   "pr peer scatter")
+
+    def fused_round(self, block: torch.Tensor, counts_all: torch.Tensor, n: int, p: int, me: int, rnd: int,
+                    bits: int, peer_ptrs) -> None:
+        """Local stable pass + exchange + rebuild as one pass (r <= 2^8)."""
+        arr = (ctypes.c_void_p * p)(*peer_ptrs)
+        _lib.check(self.L.bsg_pr_fused_round(self.ctx.handle, block.data_ptr(), block.numel(), counts_all.data_ptr(),
+                                             n, p, me, rnd, bits, arr, self._stream()), "pr fused round")
+
     def rebuild(self, recv: torch.Tensor, recv_counts_dev: torch.Tensor, p: int, rnd: int, bits: int,
                 delta: torch.Tensor, out_len: int) -> torch.Tensor:
         block = torch.empty(out_len, dtype=torch.int32, device=self.device)
@@ -93,8 +114,48 @@ class CudaStepOps:
         return block
 
 
+class PeerBlocks:
+    """Two ping-pong next-round blocks per rank, mapped into every rank
+    (CUDA IPC handles exchanged with all_gather_object; torch's own
+    reduce_tensor/rebuild carries the allocation offset).  Round k's peer
+    scatter writes buffer k % 2 of every owner; the owner last read that
+    buffer in round k - 1, which the previous round's barrier closed."""
+
+    def __init__(self, n_total: int, group=None, device: Optional[torch.device] = None):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.p = dist.get_world_size(group)
+        self.me = dist.get_rank(group)
+        self.n_total = n_total
+        self.group = group
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        size = partition_size_of(n_total, self.p, self.me)
+        self.size = size
+        self.local = [torch.empty(max(size, 1), dtype=torch.int32, device=self.device) for _ in range(2)]
+        gathered: List = [None] * self.p
+        if self.p > 1:  # nothing to map for a single rank
+            mine = [reduce_tensor(t) for t in self.local]
+            dist.all_gather_object(gathered, mine, group=group)
+        self.mapped = [[None] * self.p for _ in range(2)]
+        for w in range(self.p):
+            for b in range(2):
+                if w == self.me:
+                    self.mapped[b][w] = self.local[b]
+                else:
+                    fn, args = gathered[w][b]
+                    self.mapped[b][w] = fn(*args)
+        self.ptrs = [[t.data_ptr() for t in self.mapped[b]] for b in range(2)]
+        self._token = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    def barrier(self) -> None:
+        """Round barrier on the device stream: every rank's scatter kernel has
+        completed (and fenced its peer stores) before any rank continues."""
+        dist.all_reduce(self._token, group=self.group)
+
+
 def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rounds: Optional[int] = None,
-                        group=None, ops=None, a2a_events: Optional[list] = None) -> torch.Tensor:
+                        group=None, ops=None, a2a_events: Optional[list] = None, exchange: str = "nccl",
+                        peer: Optional[PeerBlocks] = None) -> torch.Tensor:
     """Sorts the globally block-distributed array (rank w holds the keys at
     Partition(n_total, p).offset_of(w) .. +size_of(w), radix.hpp:207-229).
     Returns this rank's block of the sorted array (int32 bit patterns of the
@@ -113,6 +174,10 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
         ops = CudaStepOps(block.device)
     all_rounds = 32 // bits
     rounds = all_rounds if rounds is None else max(0, min(int(rounds), all_rounds))
+    if exchange == "peer":
+        return _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_events, peer)
+    if exchange != "nccl":
+        raise ValueError(f"exchange must be 'nccl' or 'peer', not {exchange!r}")
     for rnd in range(rounds):
         counts = ops.count(block, rnd, bits)
         counts_all = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
@@ -129,6 +194,32 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
             a2a_events.append((e0, e1))
         block = ops.rebuild(recv_buf, recv_dev, p, rnd, bits, delta, partition_size_of(n_total, p, me))
     return block
+
+
+def _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_events, peer):
+    p = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    if peer is None:
+        peer = PeerBlocks(n_total, group, block.device)
+    if peer.n_total != n_total or peer.p != p:
+        raise ValueError("PeerBlocks were mapped for a different (n, p)")
+    size = partition_size_of(n_total, p, me)
+    for rnd in range(rounds):
+        counts = ops.count(block, rnd, bits)
+        counts_all = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
+        dist.all_gather_into_tensor(counts_all, counts, group=group)
+        b = rnd % 2
+        if a2a_events is not None and block.is_cuda:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        # the round's local pass stores straight into the owners' blocks
+        ops.fused_round(block, counts_all, n_total, p, me, rnd, bits, peer.ptrs[b])
+        peer.barrier()
+        if a2a_events is not None and block.is_cuda:
+            e1.record()
+            a2a_events.append((e0, e1))
+        block = peer.local[b][:size]
+    return block.clone()
 
 
 def digit_cuts(global_counts, p: int):

@@ -115,6 +115,15 @@ def test_distributed_nccl_world1(cuda, bsg, orc):
                 out = D.parallel_radix_sort(blk, keys.size, radix=radix, rounds=rounds)
                 exp, _ = orc.parallel_radix(keys, 1, radix, -1 if rounds is None else rounds)
                 np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), exp)
+        # exchange + rebuild as one peer-store kernel (IPC-mapped
+        # next-round blocks; with one rank every store is local)
+        peer = D.PeerBlocks(keys.size)
+        for radix in (256, 65536):
+            for rounds in (1, None):
+                blk = torch.from_numpy(keys.view(np.int32)).cuda()
+                out = D.parallel_radix_sort(blk, keys.size, radix=radix, rounds=rounds, exchange="peer", peer=peer)
+                exp, _ = orc.parallel_radix(keys, 1, radix, -1 if rounds is None else rounds)
+                np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), exp)
     finally:
         dist.destroy_process_group()
 
@@ -130,3 +139,47 @@ def test_large_blocks_per_round(cuda, bsg, orc, p):
             exp, est = orc.parallel_radix(keys, p, radix, k)
             np.testing.assert_array_equal(res.output, exp)
             assert res.stats == est
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+def test_peer_scatter_logical_workers(cuda, bsg, orc, p):
+    """bsg_pr_peer_scatter with p logical workers in one process (all
+    next-round blocks local): every round's concatenated blocks equal
+    run_parallel_radix with plan.rounds = k (radix.hpp:371-414)."""
+    torch = cuda
+    import ctypes
+    from paper_1708_09495_b200 import distributed as D
+
+    ops = D.CudaStepOps(torch.device("cuda", 0))
+    n = 100003 if p != 2 else (1 << 21) + 5  # p = 2: multi-tile blocks
+    keys = orc.generate_uniform_keys(n, 40 + p) % np.uint32(1 << 30)
+    sizes = [D.partition_size_of(n, p, w) for w in range(p)]
+    offs = [D.partition_offset_of(n, p, w) for w in range(p)]
+    for radix in (256, 65536):
+        bits = radix.bit_length() - 1
+        blocks = [torch.from_numpy(keys[offs[w]:offs[w] + sizes[w]].view(np.int32)).cuda() for w in range(p)]
+        for rnd in range(32 // bits):
+            counts_all = torch.cat([ops.count(b, rnd, bits) for b in blocks])
+            exp, _ = orc.parallel_radix(keys, p, radix, rnd + 1)
+            # (a) local pass, then the peer-store exchange kernel
+            nxt = [torch.empty(max(sz, 1), dtype=torch.int32, device="cuda") for sz in sizes]
+            ptrs = [t.data_ptr() for t in nxt]
+            for me in range(p):
+                ops.peer_scatter(ops.local_sort(blocks[me], rnd, bits), counts_all, n, p, me, rnd, bits, ptrs)
+            np.testing.assert_array_equal(torch.cat([nxt[w][:sizes[w]] for w in range(p)]).cpu().numpy()
+                                          .view(np.uint32), exp)
+            # (b) the whole round as one pass writing into the owners' blocks
+            fused = [torch.empty(max(sz, 1), dtype=torch.int32, device="cuda") for sz in sizes]
+            fptrs = [t.data_ptr() for t in fused]
+            for me in range(p):
+                ops.fused_round(blocks[me], counts_all, n, p, me, rnd, bits, fptrs)
+            blocks = [fused[w][:sizes[w]] for w in range(p)]
+            np.testing.assert_array_equal(torch.cat(blocks).cpu().numpy().view(np.uint32), exp)
+    L = bsg._lib.lib()
+    arr = (ctypes.c_void_p * 2)(0, 0)
+    ctx = bsg._lib.context(0)
+    # size mismatch and bad worker index fail loudly
+    assert L.bsg_pr_peer_scatter(ctx.handle, 0, 5, 0, n, 2, 0, 0, 8, arr, None) != 0
+    assert L.bsg_pr_peer_scatter(ctx.handle, 0, 0, 0, n, 2, 2, 0, 8, arr, None) != 0
+    assert L.bsg_pr_fused_round(ctx.handle, 0, 5, 0, n, 2, 0, 0, 8, arr, None) != 0
+    assert L.bsg_pr_fused_round(ctx.handle, 0, 0, 0, n, 2, 0, 9, 8, arr, None) != 0
