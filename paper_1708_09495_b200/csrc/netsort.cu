@@ -44,7 +44,8 @@ constexpr uint32_t kPad = 0xFFFFFFFFu;
 // for x * d < 2^32 (indices and divisors here are < 2^16).
 struct FastDiv {
     uint32_t d, m;
-    __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv), m(dv > 1 ? 0xFFFFFFFFu / dv + 1u : 0u) {}
+    FastDiv() = default;
+    __host__ __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv), m(dv > 1 ? 0xFFFFFFFFu / dv + 1u : 0u) {}
     __device__ __forceinline__ uint32_t div(uint32_t x) const { return d > 1 ? __umulhi(x, m) : x; }
 };
 
@@ -227,10 +228,16 @@ __device__ __forceinline__ int oet_partner(int r, int i, int p, bool& keep_low) 
 // THREADS x MINB: 256 x 5 for padded arrays <= 8192 keys (several CTAs per
 // SM), 1024 x 1 above, where the two shared-memory copies allow one CTA per
 // SM (keeps 32 warps resident instead of 8).
+// Launch-uniform divisors with their multipliers precomputed on the host.
+struct NetDivs {
+    FastDiv P, pcb, cb, pcbm, cbm, len;
+};
+
 template <int kNetThreads, int MINB>
 __global__ void __launch_bounds__(kNetThreads, MINB)
     block_network_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t num_arrays,
-                         uint32_t len, int p, uint32_t L, int network, int run_stages, int full, int apc) {
+                         uint32_t len, int p, uint32_t L, int network, int run_stages, int full, int apc,
+                         const NetDivs dv) {
     extern __shared__ __align__(16) uint32_t net_smem[];
     const uint32_t P = L * static_cast<uint32_t>(p);
     const uint32_t padded = pad(static_cast<uint32_t>(apc) * P) + 1;
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
 
     // prepare_blocks: load + pad (netsort.hpp:131-139)
     const uint32_t tot = static_cast<uint32_t>(na) * P;
-    const FastDiv divP(P);
+    const FastDiv& divP = dv.P;
     for (uint32_t idx = tid; idx < tot; idx += kNetThreads) {
         const uint32_t a = divP.div(idx), e = idx - a * P;
         bufA[pad(idx)] = e < len ? __ldg(in + (array0 + a) * len + e) : kPad;
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
     constexpr int kSK = 2 * kNK;
     const uint32_t cb = (L + kSK - 1) / kSK; // sort chunks per block
     const uint32_t items = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cb;
-    const FastDiv div_pcb(static_cast<uint32_t>(p) * cb), div_cb(cb);
+    const FastDiv &div_pcb = dv.pcb, &div_cb = dv.cb;
     for (uint32_t it = tid; it < items; it += kNetThreads) {
         const uint32_t a = div_pcb.div(it), rem = it - a * p * cb;
         const uint32_t w = div_cb.div(rem), c = rem - w * cb;
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
     constexpr int kSK = kNK;
     const uint32_t cb = (L + kSK - 1) / kSK; // sort chunks per block
     const uint32_t items = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cb;
-    const FastDiv div_pcb(static_cast<uint32_t>(p) * cb), div_cb(cb);
+    const FastDiv &div_pcb = dv.pcb, &div_cb = dv.cb;
     for (uint32_t it = tid; it < items; it += kNetThreads) {
         const uint32_t a = div_pcb.div(it), rem = it - a * p * cb;
         const uint32_t w = div_cb.div(rem), c = rem - w * cb;
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
     uint32_t* dst = bufB;
     const uint32_t cbm = (L + kMK - 1) / kMK; // merge chunks per block
     const uint32_t mitems = static_cast<uint32_t>(na) * static_cast<uint32_t>(p) * cbm;
-    const FastDiv div_pcbm(static_cast<uint32_t>(p) * cbm), div_cbm(cbm);
+    const FastDiv &div_pcbm = dv.pcbm, &div_cbm = dv.cbm;
     for (uint32_t width = kSK; width < L; width *= 2) {
         for (uint32_t it = tid; it < mitems; it += kNetThreads) {
             const uint32_t a = div_pcbm.div(it), rem = it - a * p * cbm;
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
 
     // concatenate (+ strip the pad when the network ran to completion)
     if (full) {
-        const FastDiv div_len(len);
+        const FastDiv& div_len = dv.len;
         for (uint32_t idx = tid; idx < static_cast<uint32_t>(na) * len; idx += kNetThreads) {
             const uint32_t a = div_len.div(idx), e = idx - a * len;
             out[(array0 + a) * len + e] = src[pad(a * P + e)];
@@ -459,13 +466,24 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     (void)attr;
     const uint64_t resident = static_cast<uint64_t>(apc) * P;
     const bool big = resident > 8192;
+    NetDivs dv;
+    {
+        constexpr uint32_t sk = BSG_NET_SORT32 ? 2 * kNK : kNK; // register-sort chunk (kernel: kSK)
+        const uint32_t cb = (L + sk - 1) / sk, cbm = (L + kMK - 1) / kMK;
+        dv.P = FastDiv(P);
+        dv.pcb = FastDiv(static_cast<uint32_t>(p) * cb);
+        dv.cb = FastDiv(cb);
+        dv.pcbm = FastDiv(static_cast<uint32_t>(p) * cbm);
+        dv.cbm = FastDiv(cbm);
+        dv.len = FastDiv(len);
+    }
     TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
     if (!big)
         block_network_kernel<256, BSG_NET_MINB><<<static_cast<unsigned>(grid), 256, smem, stream>>>(
-            in, out, num_arrays, len, p, L, network, run_stages, full ? 1 : 0, apc);
+            in, out, num_arrays, len, p, L, network, run_stages, full ? 1 : 0, apc, dv);
     else
         block_network_kernel<1024, 1><<<static_cast<unsigned>(grid), 1024, smem, stream>>>(
-            in, out, num_arrays, len, p, L, network, run_stages, full ? 1 : 0, apc);
+            in, out, num_arrays, len, p, L, network, run_stages, full ? 1 : 0, apc, dv);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
