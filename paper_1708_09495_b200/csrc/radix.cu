@@ -41,6 +41,20 @@ namespace {
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
+
+// Look-back status word: 2-bit flag (aggregate / inclusive) + count.  32-bit
+// words (30-bit counts) while a pass covers <= 2^29 keys; 64-bit words
+// (62-bit counts) above, so one pass is always one look-back domain.
+template <bool WIDE>
+struct StatusWord {
+    using T = uint32_t;
+    static constexpr T AGG = 1u << 30, INC = 2u << 30, VAL = (1u << 30) - 1;
+};
+template <>
+struct StatusWord<true> {
+    using T = unsigned long long;
+    static constexpr T AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
+};
 constexpr int kScanThreads = 256;
 
 // ---------------------------------------------------------------------------
@@ -303,7 +317,7 @@ struct PeerSink {
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK, typename Sink = PlainSink>
 __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const uint32_t* __restrict__ src,
-                                               Sink dst, uint32_t chunk_n, int shift,
+                                               Sink dst, uint64_t chunk_n, int shift,
                                                const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                                                uint32_t* __restrict__ tile_counter, int use_tma, int dbg,
                                                int32_t neg1, bool init_bars, uint32_t& bar_parity) {
@@ -323,7 +337,10 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
 
-    const uint32_t ntiles = (chunk_n + TILE - 1) / TILE;
+    const uint32_t ntiles = static_cast<uint32_t>((chunk_n + TILE - 1) / TILE);
+    using SW = StatusWord<WIDE>;
+    using Stat = typename SW::T;
+    Stat* __restrict__ stat = reinterpret_cast<Stat*>(status);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -332,8 +349,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
     auto issue = [&](uint32_t tile, int b) {
         if (tile >= ntiles) return;
-        const uint32_t start = tile * TILE;
-        const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - start);
+        const uint64_t start = static_cast<uint64_t>(tile) * TILE;
+        const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), chunk_n - start));
         const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&s_bar[b], vec * 4);
@@ -365,8 +382,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             s_tile[cur ^ 1] = nxt;
             issue(nxt, cur ^ 1);
         }
-        const uint32_t tile_start = tile * TILE;
-        const uint32_t valid = min(static_cast<uint32_t>(TILE), chunk_n - tile_start);
+        const uint64_t tile_start = static_cast<uint64_t>(tile) * TILE;
+        const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), chunk_n - tile_start));
         const bool full = valid == TILE;
         uint32_t* buf = s_in + cur * TILE;
         // non-TMA body / unaligned tail straight from global
@@ -460,9 +477,9 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 run2 += c2;
             }
             const uint32_t lo = run2 & 0xFFFFu, hi = run2 >> 16;
-            const uint32_t flag = tile == 0 ? kFlagInc : kFlagAgg;
-            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + 2 * tid], flag | lo);
-            st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + 2 * tid + 1], flag | hi);
+            const Stat flag = tile == 0 ? SW::INC : SW::AGG;
+            st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + 2 * tid], flag | static_cast<Stat>(lo));
+            st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + 2 * tid + 1], flag | static_cast<Stat>(hi));
         }
         constexpr int SCAN_WARPS = (PAIRS + 31) / 32;
         uint32_t pair_incl = 0, pair_sum = 0;
@@ -506,27 +523,27 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         // one coalesced 128-byte request per predecessor per warp)
         if (tid < RADIX) {
             constexpr int LB_WIN = BSG_LB_WIN;
-            uint32_t prefix = 0;
+            Stat prefix = 0;
             if (tile > 0 && !(dbg & 1)) {
                 int64_t t = static_cast<int64_t>(tile) - 1;
                 while (true) {
                     if ((dbg & 8) && tid == 0) atomicAdd(&g_phase_cycles[7], 1ull);
-                    uint32_t sv[LB_WIN];
+                    Stat sv[LB_WIN];
 #pragma unroll
                     for (int j = 0; j < LB_WIN; ++j)
-                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&status[static_cast<uint64_t>(t - j) * RADIX + tid])
-                                             : kFlagInc;
+                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&stat[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                             : SW::INC;
                     int used = 0;
                     bool done = false, stop = false;
 #pragma unroll
                     for (int j = 0; j < LB_WIN; ++j) {
                         if (!stop) {
-                            if ((sv[j] & ~kValMask) == 0) {
+                            if ((sv[j] & ~SW::VAL) == 0) {
                                 stop = true;
                             } else {
-                                prefix += sv[j] & kValMask;
+                                prefix += sv[j] & SW::VAL;
                                 ++used;
-                                if (sv[j] & kFlagInc) done = stop = true;
+                                if (sv[j] & SW::INC) done = stop = true;
                             }
                         }
                     }
@@ -535,7 +552,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 }
             }
             if (tile > 0)
-                st_relaxed_gpu(&status[static_cast<uint64_t>(tile) * RADIX + tid], kFlagInc | (prefix + tile_cnt));
+                st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + tid],
+                               SW::INC | (prefix + static_cast<Stat>(tile_cnt)));
             s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
         }
         __syncthreads();
@@ -564,7 +582,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
-    onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint32_t chunk_n,
+    onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint64_t chunk_n,
                     int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                     uint32_t* __restrict__ tile_counter, int use_tma, int dbg, int32_t neg1) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -621,28 +639,16 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
-    // status layout per chunk: [counter (32 words)] [tiles * RADIX]
-    const uint64_t words_per_chunk = 32 + ((kChunkKeys + kMinTile - 1) / kMinTile) * RADIX;
-    int launches = 0;
-    const int dbg = onesweep_dbg();
-    for (uint64_t c = 0; c < chunks; ++c) {
-        const uint64_t off = c * kChunkKeys;
-        const uint32_t len = static_cast<uint32_t>(std::min<uint64_t>(kChunkKeys, n - off));
-        const uint32_t tiles = (len + L::TILE - 1) / L::TILE;
-        const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
-        uint32_t* st = status + c * words_per_chunk;
-        const uint64_t* base = base_for_pass + c * static_cast<uint64_t>(passes_stride) * RADIX;
-        // clear exactly the counter + status words this launch uses
-        if (cudaMemsetAsync(st, 0, (32 + static_cast<uint64_t>(tiles) * RADIX) * sizeof(uint32_t), stream) !=
-            cudaSuccess)
-            return -1;
-        TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
-        kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, off, len, shift, base, st + 32, st, use_tma ? 1 : 0, dbg,
-                                                   -1);
-        ++launches;
-    }
-    return launches;
+    // one look-back domain per pass: [tile counter (32 words)] [tiles * RADIX status words]
+    const uint32_t tiles = static_cast<uint32_t>((n + L::TILE - 1) / L::TILE);
+    const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
+    const uint64_t stat_words = static_cast<uint64_t>(tiles) * RADIX * (WIDE ? 2 : 1);
+    (void)passes_stride; // digit bases: chunk row 0 of [chunk][pass][radix] = global starts
+    if (cudaMemsetAsync(status, 0, (32 + stat_words) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
+    kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, 0, n, shift, base_for_pass, status + 32, status,
+                                               use_tma ? 1 : 0, onesweep_dbg(), -1);
+    return 1;
 }
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
@@ -665,8 +671,8 @@ int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, c
 template <int BITS>
 int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                          int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
-    const bool wide = n > 0xFFFFFFFFull;
-    if (wide) // n > 2^32: 24-key rows, the large-n configuration
+    const bool wide = n > kChunkKeys;
+    if (wide) // n > 2^29: 64-bit status words and positions, 24-key rows
         return launch_onesweep_cfg<BITS, 1024, 24, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                         stream, use_tma);
     if constexpr (BITS != 8)
@@ -704,10 +710,9 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
 template <int BITS>
 uint64_t status_words_for(uint64_t n) {
     constexpr int RADIX = 1 << BITS;
-    const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
-    const uint64_t per_chunk = 32 + ((kChunkKeys + kMinTile - 1) / kMinTile) * RADIX;
-    if (chunks <= 1) return 32 + ((n + kMinTile - 1) / kMinTile) * RADIX;
-    return chunks * per_chunk;
+    if (n > kChunkKeys) // WIDE: 1024 x 24 tiles, 64-bit status words
+        return 32 + ((n + 24575) / 24576) * RADIX * 2;
+    return 32 + ((n + kMinTile - 1) / kMinTile) * RADIX;
 }
 
 

@@ -211,3 +211,54 @@ def test_small_n_both_paths(cuda, bsg, orc, small):
         np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32), np.sort(keys))
     finally:
         L.bsg_debug_set_small_sort(prev)
+
+
+def _chunked_properties(torch, inp, out, step=1 << 27):
+    """Sortedness (incl. across chunk seams) and permutation checksums
+    (sum, sum of squares mod p) without n-sized int64 temporaries."""
+    n = inp.numel()
+    m = 1000003
+    s_in = s_out = q_in = q_out = 0
+    prev_last = None
+    for a in range(0, n, step):
+        x = inp[a:a + step].to(torch.int64) & 0xFFFFFFFF
+        y = out[a:a + step].to(torch.int64) & 0xFFFFFFFF
+        assert bool((y[1:] >= y[:-1]).all())
+        if prev_last is not None:
+            assert int(y[0]) >= prev_last
+        prev_last = int(y[-1])
+        s_in += int(x.sum()); s_out += int(y.sum())
+        q_in += int(((x % m) * (x % m) % m).sum()); q_out += int(((y % m) * (y % m) % m).sum())
+        del x, y
+    assert s_in == s_out and q_in == q_out
+
+
+@pytest.mark.parametrize("n", [(1 << 29) + 12345, (1 << 32) + 777])
+def test_multi_chunk_and_wide_positions(cuda, bsg, n):
+    """n > 2^29: several look-back chunks per pass; n > 2^32: 64-bit positions
+    (WIDE one-sweep).  ~48 GiB of device buffers at the larger size."""
+    torch = cuda
+    free, _ = torch.cuda.mem_get_info()
+    if free < 14 * n:
+        pytest.skip("not enough device memory")
+    g = torch.Generator(device="cuda").manual_seed(n)
+    inp = torch.randint(-2**31, 2**31, (n,), dtype=torch.int32, device="cuda", generator=g)
+    inp[:1000] = 7  # ties across the first tiles
+    out = torch.empty_like(inp)
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.bsg_radix_sort_u32(ctx.handle, inp.data_ptr(), out.data_ptr(), n, 8, 1, st) == 0
+    torch.cuda.synchronize()
+    _chunked_properties(torch, inp, out)
+    # one stable pass at the top digit: a count-sort round over all chunks
+    assert L.bsg_count_sort_round_u32(ctx.handle, inp.data_ptr(), out.data_ptr(), n, 3, 8, 1, st) == 0
+    torch.cuda.synchronize()
+    step = 1 << 27
+    prev = -1
+    for a in range(0, n, step):
+        d = (out[a:a + step].to(torch.int64) & 0xFFFFFFFF) >> 24
+        assert bool((d[1:] >= d[:-1]).all()) and int(d[0]) >= prev
+        prev = int(d[-1])
+    del inp, out
+    torch.cuda.empty_cache()
