@@ -405,6 +405,41 @@ __global__ void pr_fused_base_kernel(const uint64_t* __restrict__ dstart, const 
     if (d < radix) base[d] = dstart[d] + static_cast<uint64_t>(before_me[d]);
 }
 
+// In-process fused round: base[v][d] = digit_start[d] + sum_{u<v} cnt(u,d),
+// in place over the column-prefix table.
+__global__ void pr_add_dstart_kernel(int64_t* __restrict__ before, const uint64_t* __restrict__ dstart, int p,
+                                     int radix) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < static_cast<uint64_t>(p) * radix) before[i] += static_cast<int64_t>(dstart[i % radix]);
+}
+
+// RunStats send counts from the count matrix: worker v's digit-d run
+// [base[v][d], + cnt(v,d)) split over the partitions it overlaps.
+__global__ void __launch_bounds__(kSendThreads)
+    pr_send_from_counts_kernel(const uint64_t* __restrict__ counts, const int64_t* __restrict__ base, uint64_t n,
+                               int p, int radix, uint64_t* __restrict__ send) {
+    extern __shared__ unsigned long long s_cnt2[]; // p entries
+    const int v = blockIdx.y;
+    for (int w = threadIdx.x; w < p; w += kSendThreads) s_cnt2[w] = 0;
+    __syncthreads();
+    const int d = blockIdx.x * kSendThreads + threadIdx.x;
+    if (d < radix) {
+        const uint64_t cv = counts[static_cast<uint64_t>(v) * radix + d];
+        if (cv) {
+            const uint64_t np = static_cast<uint64_t>(base[static_cast<uint64_t>(v) * radix + d]);
+            const int w0 = part_owner(n, p, np), w1 = part_owner(n, p, np + cv - 1);
+            for (int w = w0; w <= w1; ++w) {
+                const uint64_t lo = part_offset(n, p, w);
+                const uint64_t o = overlap(np, np + cv, lo, lo + part_size(n, p, w));
+                if (o) atomicAdd(&s_cnt2[w], static_cast<unsigned long long>(o));
+            }
+        }
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < p; w += kSendThreads)
+        if (s_cnt2[w]) atomicAdd(reinterpret_cast<unsigned long long*>(send + static_cast<uint64_t>(v) * p + w), s_cnt2[w]);
+}
+
 } // namespace
 
 int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int bits, uint64_t* counts,
@@ -507,7 +542,61 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         return true;
     };
     const uint64_t max_len = n / p + (n % p ? 1 : 0);
-    for (int round = 0; round < rounds && n; ++round) {
+    // r <= 2^8: each worker's whole round is ONE one-sweep pass whose digit
+    // bases are the global positions of its block's first key per digit
+    // (the same fused round as bsg_pr_fused_round, all blocks local)
+    const bool fused = bits <= 8 && max_len <= kChunkKeys;
+    uint32_t* cur = A;
+    uint32_t* nxt = S;
+    for (int round = 0; round < rounds && n && fused; ++round) {
+        const int shift = round * bits;
+        uint64_t* counts = starts; // [p][radix]
+        int64_t* base = gd;        // [p][radix]
+        for (int w = 0; w < p; ++w) {
+            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
+            if (!add(launch_pr_count(ctx, cur + off, sz, round, bits, counts + static_cast<uint64_t>(w) * radix,
+                                     stream)))
+                return cuda_fail(cudaGetLastError(), "pr count");
+        }
+        {
+            TimedScope ts(3 /*BSG_K_PR*/, stream);
+            const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+            pr_plan_col_kernel<<<chunks, kDigChunk, 0, stream>>>(counts, p, radix, base, coltot, colchunk);
+            pr_digit_start_kernel<<<chunks, kDigChunk, 0, stream>>>(coltot, colchunk, radix, dstart);
+            const uint64_t pr = static_cast<uint64_t>(p) * radix;
+            pr_add_dstart_kernel<<<static_cast<unsigned>((pr + 255) / 256), 256, 0, stream>>>(base, dstart, p, radix);
+            launches += 3;
+        }
+        PeerTable tab{};
+        tab.blocks[0] = nxt;
+        tab.offset[0] = 0;
+        tab.offset[1] = n;
+        for (int w = 0; w < p; ++w) {
+            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
+            if (sz == 0) continue;
+            if (!add(launch_onesweep_peer(cur + off, sz, bits, shift,
+                                          reinterpret_cast<const uint64_t*>(base + static_cast<uint64_t>(w) * radix),
+                                          ctx->status.as<uint32_t>(), tab, 1, stream)))
+                return cuda_fail(cudaGetLastError(), "pr fused pass");
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
+        if (stats) {
+            if ((e = cudaMemsetAsync(send, 0, pp * 8, stream)) != cudaSuccess) return cuda_fail(e, "pr stats");
+            pr_send_from_counts_kernel<<<dim3((radix + kSendThreads - 1) / kSendThreads, p), kSendThreads, p * 8,
+                                         stream>>>(counts, base, n, p, radix, send);
+            ++launches;
+            if ((e = cudaMemcpyAsync(h_send.data(), send, pp * 8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess ||
+                (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+                return cuda_fail(e, "pr stats");
+            uint64_t nz = 0;
+            for (uint64_t i = 0; i < pp; ++i) nz += h_send[i] ? 1 : 0;
+            st.messages_sent += pp + nz;
+            st.words_sent += pp * static_cast<uint64_t>(radix) + n;
+        }
+        std::swap(cur, nxt);
+    }
+    if (fused) A = cur;
+    for (int round = 0; round < rounds && n && !fused; ++round) {
         const int shift = round * bits;
         // local stable pass of every worker (sort_and_scatter's count_sort_round)
         for (int w = 0; w < p; ++w) {
