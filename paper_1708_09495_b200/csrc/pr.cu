@@ -34,6 +34,12 @@ namespace bsg {
 
 namespace {
 
+// Binds the context's kernel timer to this thread for one C-ABI call.
+struct TimerBinding {
+    explicit TimerBinding(KTimer* t) { tl_timer = t; }
+    ~TimerBinding() { tl_timer = nullptr; }
+};
+
 constexpr int kPlanThreads = 256;
 
 __device__ __forceinline__ uint64_t part_size(uint64_t n, int p, int w) {
@@ -727,17 +733,14 @@ extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_
     if (!peer_blocks || !counts_all || (len && !sorted)) return fail(BSG_EINVAL, "null pointer");
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dev(ctx->device);
-    tl_timer = &ctx->timer;
+    TimerBinding bind(&ctx->timer);
     const int radix = 1 << radix_log2;
     const int chunks = (radix + kDigChunk - 1) / kDigChunk;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // scratch: before/delta [p][r] (int64), coltot [r], dstart [r], colchunk [chunks], gd [r]
     const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks;
     cudaError_t e = ctx->pr_delta.ensure(words * 8);
-    if (e != cudaSuccess) {
-        tl_timer = nullptr;
-        return cuda_fail(e, "peer scatter workspace");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "peer scatter workspace");
     int64_t* before = ctx->pr_delta.as<int64_t>();
     uint64_t* coltot = reinterpret_cast<uint64_t*>(before + static_cast<uint64_t>(p) * radix);
     uint64_t* dstart = coltot + radix;
@@ -745,10 +748,7 @@ extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_
     uint64_t* colchunk = reinterpret_cast<uint64_t*>(gd + radix);
     PeerTable tab{};
     for (int w = 0; w < p; ++w) {
-        if (!peer_blocks[w] && bsg_partition_size_of(n, p, w)) {
-            tl_timer = nullptr;
-            return fail(BSG_EINVAL, "peer scatter: null peer block");
-        }
+        if (!peer_blocks[w] && bsg_partition_size_of(n, p, w)) return fail(BSG_EINVAL, "peer scatter: null peer block");
         tab.blocks[w] = peer_blocks[w];
         tab.offset[w] = bsg_partition_offset_of(n, p, w);
     }
@@ -768,9 +768,7 @@ extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_
             ctx->launches += 1;
         }
     }
-    e = cudaPeekAtLastError();
-    tl_timer = nullptr;
-    if (e != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer scatter launch");
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer scatter launch");
     return BSG_OK;
 }
 
@@ -802,10 +800,7 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dev(ctx->device);
-    tl_timer = &ctx->timer;
-    struct Reset {
-        ~Reset() { tl_timer = nullptr; }
-    } reset;
+    TimerBinding bind(&ctx->timer);
     const int radix = 1 << radix_log2;
     const int chunks = (radix + kDigChunk - 1) / kDigChunk;
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -726,7 +726,10 @@ uint64_t status_words_for(uint64_t n) {
 // Workspace (zeroed by one memset): hist[4][256] | barrier word (+31 pad) |
 // 4 x per-pass look-back regions [tile counter (+31)][tiles][256].
 // ---------------------------------------------------------------------------
-constexpr int kSmallThreads = 512, kSmallItems = 16;
+#ifndef BSG_SMALL_THREADS
+#define BSG_SMALL_THREADS 512
+#endif
+constexpr int kSmallThreads = BSG_SMALL_THREADS, kSmallItems = 16;
 constexpr uint64_t kSmallMaxKeys = uint64_t{1} << 21;
 constexpr int kSmallHistCopies = 4;
 
@@ -748,7 +751,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSmallThreads, 2)
+__global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
     small_sort_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t* __restrict__ tmp,
                       uint32_t n, uint32_t* __restrict__ ws, uint32_t region_words, int use_tma, int32_t neg1) {
     using L = OnesweepSmem<8, kSmallThreads, kSmallItems, false>;
