@@ -96,6 +96,9 @@ int bsg_ctx_get_timing(bsg_ctx* ctx, int kernel_class, double* total_ms, uint64_
 /* ---- host-side helpers (no GPU needed) -------------------------------- */
 /* core.hpp:93-99 generate_uniform_keys: mt19937_64(seed), low 32 bits. */
 int bsg_generate_uniform_u32(uint32_t* out, uint64_t n, uint64_t seed);
+/* Draws [offset, offset + n) of the same stream (random access by
+ * jump-ahead: x^offset mod the generator's characteristic polynomial). */
+int bsg_generate_uniform_at_u32(uint32_t* out, uint64_t n, uint64_t seed, uint64_t offset);
 /* bench.hpp:77-88 derive_seed (splitmix64). */
 uint64_t bsg_derive_seed(uint64_t seed, int32_t rep);
 /* core.hpp:60-64 digit_bits + radix.hpp:143-151 checked_digit_bits:
@@ -231,6 +234,13 @@ int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t len,
                        const uint64_t* counts_all, uint64_t n, int p, int me,
                        int round, int radix_log2, uint32_t* const* peer_blocks,
                        void* stream);
+
+/* core.hpp:93-99 generate_uniform_keys on the GPU: the same n keys,
+ * bit-identical, written to device memory (`out`) on `stream`.  Segments of
+ * the stream start from jump-ahead states; the first call per process
+ * derives the generator's characteristic polynomial (host, ~0.1 s). */
+int bsg_generate_uniform_device_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n,
+                                    uint64_t seed, void* stream);
 
 #ifdef __cplusplus
 }

@@ -9,13 +9,14 @@ from . import _lib
 from ._lib import BspError, Context, DeviceError, LibraryNotBuilt, RunStats
 from .bspsort import sort_instance
 from .core import (Algorithm, Key, SortInstance, algorithm_from_name, algorithm_name, derive_seed, digit_bits,
-                   generate_skewed_keys, generate_uniform_keys, is_power_of_two, key_bits, log2_exact,
+                   generate_skewed_keys, generate_uniform_keys, generate_uniform_keys_at,
+                   generate_uniform_keys_device, is_power_of_two, key_bits, log2_exact,
                    verify_sorted_permutation)
 from . import netsort, radix
 
 __all__ = [
     "Algorithm", "BspError", "Context", "DeviceError", "Key", "LibraryNotBuilt", "RunStats", "SortInstance",
     "algorithm_from_name", "algorithm_name", "derive_seed", "digit_bits", "generate_skewed_keys",
-    "generate_uniform_keys", "is_power_of_two", "key_bits", "log2_exact", "netsort", "radix", "sort_instance",
+    "generate_uniform_keys", "generate_uniform_keys_at", "generate_uniform_keys_device", "is_power_of_two", "key_bits", "log2_exact", "netsort", "radix", "sort_instance",
     "verify_sorted_permutation",
 ]

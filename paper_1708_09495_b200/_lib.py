@@ -64,6 +64,8 @@ SIGNATURES = {
     "bsg_ctx_set_timing": (_i, [_vp, _i]),
     "bsg_ctx_get_timing": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "bsg_generate_uniform_u32": (_i, [_u32p, _u64, _u64]),
+    "bsg_generate_uniform_at_u32": (_i, [_u32p, _u64, _u64, _u64]),
+    "bsg_generate_uniform_device_u32": (_i, [_vp, _u32p, _u64, _u64, _vp]),
     "bsg_derive_seed": (ctypes.c_uint64, [_u64, ctypes.c_int32]),
     "bsg_checked_digit_bits": (_i, [_u64]),
     "bsg_generate_skewed_u32": (_i, [_u32p, _u64, _u64, _i, ctypes.c_double]),

@@ -97,6 +97,29 @@ def generate_uniform_keys(n: int, seed: int) -> np.ndarray:
     return out
 
 
+def generate_uniform_keys_at(n: int, seed: int, offset: int) -> np.ndarray:
+    """Draws [offset, offset + n) of generate_uniform_keys(., seed)'s stream
+    (jump-ahead; no need to generate the prefix)."""
+    out = np.empty(int(n), dtype=np.uint32)
+    _lib.check(_lib.lib().bsg_generate_uniform_at_u32(_ptr(out), int(n), int(seed) & (2**64 - 1), int(offset)),
+               "generate_uniform_keys_at")
+    return out
+
+
+def generate_uniform_keys_device(n: int, seed: int, device: int = 0):
+    """generate_uniform_keys on the GPU: a torch.uint32 CUDA tensor holding the
+    same n keys, bit for bit (segment starts by jump-ahead)."""
+    import torch
+
+    out = torch.empty(int(n), dtype=torch.int32, device=torch.device("cuda", device))
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().bsg_generate_uniform_device_u32(ctx.handle, out.data_ptr(), int(n),
+                                                          int(seed) & (2**64 - 1),
+                                                          torch.cuda.current_stream(out.device).cuda_stream),
+               "generate_uniform_keys_device")
+    return out.view(torch.uint32)
+
+
 SKEW_NARROW16, SKEW_ZIPF, SKEW_ALL_EQUAL = 0, 1, 2
 
 

@@ -127,7 +127,7 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
         CallGuard g(ctx);
         for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
                           &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
-                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32})
+                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->mt_ws})
             b->release();
     }
     delete ctx;

@@ -54,6 +54,7 @@ struct bsg_ctx {
     bsg::DevBuf stage_in, stage_out, stage_b;
     bsg::DevBuf pr_counts, pr_sorted, pr_recv, pr_block, pr_misc, pr_delta;
     bsg::DevBuf net_sched, cnt32;
+    bsg::DevBuf mt_ws; // device generator: segment start windows + jump polynomials
 
     // Ensures the radix workspace for n keys and returns a view of it.
     int radix_ws(uint64_t n, bsg::RadixWorkspace* ws);

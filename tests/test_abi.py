@@ -124,3 +124,22 @@ def test_verify_sorted_permutation(bsg):
     assert not v(u([1, 2]), u([2, 1]))
     assert not v(u([1, 1, 2]), u([1, 2, 2]))
     assert not v(u([1]), u([]))
+
+
+@pytest.mark.parametrize("seed", [1, 5489, 0, 2**64 - 1])
+def test_generate_uniform_random_access(seed):
+    """bsg_generate_uniform_at_u32 (jump-ahead by x^offset mod the MT19937-64
+    characteristic polynomial) equals slices of generate_uniform_keys
+    (core.hpp:93-99), across the first-twist boundaries and deep offsets."""
+    import numpy as np
+    from paper_1708_09495_b200 import _lib
+
+    L = _lib.lib()
+    n = 300000
+    full = np.empty(n, np.uint32)
+    assert L.bsg_generate_uniform_u32(full.ctypes.data, n, seed) == 0
+    for off in (0, 1, 155, 156, 311, 312, 313, 623, 624, 625, 4096, 99991, 299000):
+        m = min(1000, n - off)
+        part = np.empty(m, np.uint32)
+        assert L.bsg_generate_uniform_at_u32(part.ctypes.data, m, seed, off) == 0
+        np.testing.assert_array_equal(part, full[off:off + m])

@@ -262,3 +262,18 @@ def test_multi_chunk_and_wide_positions(cuda, bsg, n):
         prev = int(d[-1])
     del inp, out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [1, 311, 312, 313, 100003, (1 << 18) + 1, (1 << 20) + 7, 3 << 20])
+def test_device_generator_matches_host_stream(cuda, bsg, n):
+    """generate_uniform_keys on the GPU (segment starts by jump-ahead) is the
+    host stream bit for bit; n > 2^18 spans several segments."""
+    torch = cuda
+    L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    for seed in (bsg.derive_seed(1, 0), 7):
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        assert L.bsg_generate_uniform_device_u32(ctx.handle, out.data_ptr(), n, seed, st) == 0
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), bsg.generate_uniform_keys(n, seed))
