@@ -287,11 +287,10 @@ def run_single(args):
     # Every step still copies its own input in and its result out.
     import threading
 
-    ctx2 = _lib.Context(0)
-    s2 = torch.cuda.Stream()
-    h_in2 = torch.from_numpy(keys.view(np.int32)).pin_memory()
-    h_out2 = torch.empty_like(h_in2).pin_memory()
-    lanes = [(ctx, stream, h_in, h_out), (ctx2, s2, h_in2, h_out2)]
+    lanes = [(ctx, stream, h_in, h_out)]
+    for _ in range(args.e2e_inflight - 1):
+        lanes.append((_lib.Context(0), torch.cuda.Stream(), torch.from_numpy(keys.view(np.int32)).pin_memory(),
+                      torch.empty_like(h_in).pin_memory()))
 
     def lane_step(c, st, hi, ho):
         _lib.check(L.bsg_radix_sort_u32(c.handle, hi.data_ptr(), ho.data_ptr(), n, 8, _lib.MEM_HOST, st.cuda_stream))
@@ -299,37 +298,40 @@ def run_single(args):
     for lane in lanes:  # warm both contexts (workspace + staging allocation)
         lane_step(*lane)
     torch.cuda.synchronize()
-    kp = 2 * ke
+    nl = len(lanes)
+    kp = nl * ke
     start = torch.cuda.Event(enable_timing=True)
     ends = [torch.cuda.Event(enable_timing=True) for _ in lanes]
     start.record(stream)
-    s2.wait_event(start)
+    for _, st_, _, _ in lanes[1:]:
+        st_.wait_event(start)
 
     def worker(i):
         c, st, hi, ho = lanes[i]
-        for _ in range(kp // 2):
+        for _ in range(kp // nl):
             lane_step(c, st, hi, ho)
         ends[i].record(st)
 
-    ths = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(nl)]
     for t in ths:
         t.start()
     for t in ths:
         t.join()
     torch.cuda.synchronize()
     e2e_ms = max(start.elapsed_time(e) for e in ends) / kp
-    ok_e2e = ok_e2e and bool(np.array_equal(h_out2.numpy().view(np.uint32)[:: max(1, n // 4096)],
-                                            d_out.cpu().numpy().view(np.uint32)[:: max(1, n // 4096)]))
-    del ctx2
+    ref_s = d_out.cpu().numpy().view(np.uint32)[:: max(1, n // 4096)]
+    for _, _, _, ho in lanes[1:]:
+        ok_e2e = ok_e2e and bool(np.array_equal(ho.numpy().view(np.uint32)[:: max(1, n // 4096)], ref_s))
+    del lanes
 
     line = {
         "metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic (reference generator, seeded)", "config": _config(1),
         "e2e": {"value": n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
-                "ms_per_step": e2e_ms, "in_flight": 2,
-                "path": "bsg_radix_sort_u32(BSG_MEM_HOST) from pinned host memory; two host threads, each with "
-                        "its own context/stream, so one step's D2H overlaps the next step's H2D",
+                "ms_per_step": e2e_ms, "in_flight": args.e2e_inflight,
+                "path": "bsg_radix_sort_u32(BSG_MEM_HOST) from pinned host memory; host threads, each with "
+                        "its own context/stream, so one step's D2H overlaps another step's H2D",
                 "serial_value": n / (e2e_serial_ms / 1e3), "serial_ms_per_step": e2e_serial_ms},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -472,6 +474,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
     ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-inflight", type=int, default=3,
+                    help="sorts in flight in the e2e measurement (host threads, one context/stream each)")
     ap.add_argument("--pr-variant", choices=["A", "B", "P"], default="P",
                     help="multi-GPU algorithm: A = per-round PR4 (4 NCCL exchanges), B = single exchange, "
                          "P = per-round PR4 with the exchange + rebuild as one peer-store kernel over NVLink")
