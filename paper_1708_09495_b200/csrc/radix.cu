@@ -32,7 +32,7 @@
 #include "timer.cuh"
 
 #ifndef BSG_LB_WIN
-#define BSG_LB_WIN 16
+#define BSG_LB_WIN 12
 #endif
 namespace bsg {
 
