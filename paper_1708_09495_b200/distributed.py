@@ -148,9 +148,32 @@ class PeerBlocks:
         self._token = torch.zeros(1, dtype=torch.float32, device=self.device)
 
     def barrier(self) -> None:
-        """Round barrier on the device stream: every rank's scatter kernel has
-        completed (and fenced its peer stores) before any rank continues."""
-        dist.all_reduce(self._token, group=self.group)
+        """Round barrier: every rank's scatter kernel has completed (and fenced
+        its peer stores) before any rank continues.  NCCL: a 1-element
+        all-reduce ordered on the device stream; other backends (gloo, e.g.
+        two processes sharing one GPU in tests): host sync + barrier."""
+        if _is_nccl(self.group):
+            dist.all_reduce(self._token, group=self.group)
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
+
+
+def _is_nccl(group) -> bool:
+    return dist.get_backend(group) == "nccl"
+
+
+def _all_gather_counts(counts: torch.Tensor, p: int, group) -> torch.Tensor:
+    """The count exchange of radix.hpp:386-388 as one all-gather (device
+    buffers with NCCL; host-staged with other backends)."""
+    if _is_nccl(group) or not counts.is_cuda:
+        out = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
+        dist.all_gather_into_tensor(out, counts, group=group)
+        return out
+    host = counts.cpu()
+    parts = [torch.empty_like(host) for _ in range(p)]
+    dist.all_gather(parts, host, group=group)
+    return torch.cat(parts).to(counts.device)
 
 
 def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rounds: Optional[int] = None,
@@ -206,8 +229,7 @@ def _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_even
     size = partition_size_of(n_total, p, me)
     for rnd in range(rounds):
         counts = ops.count(block, rnd, bits)
-        counts_all = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
-        dist.all_gather_into_tensor(counts_all, counts, group=group)
+        counts_all = _all_gather_counts(counts, p, group)
         b = rnd % 2
         if a2a_events is not None and block.is_cuda:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
