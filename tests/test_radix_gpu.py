@@ -72,7 +72,7 @@ def test_serial_radix_sort_grid(cuda, bsg, orc, n):
     inputs = [orc.generate_uniform_keys(n, s) for s in (11, 22, 33)] + [adversarial(k, n) for k in range(3)]
     for keys in inputs:
         expect = np.sort(keys)
-        for radix in (256, 65536, 2):
+        for radix in (256, 65536, 2, 4, 16):
             np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, radix), expect)
 
 
@@ -277,3 +277,28 @@ def test_device_generator_matches_host_stream(cuda, bsg, n):
         assert L.bsg_generate_uniform_device_u32(ctx.handle, out.data_ptr(), n, seed, st) == 0
         torch.cuda.synchronize()
         np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), bsg.generate_uniform_keys(n, seed))
+
+
+def test_in_place_calls(cuda, bsg, orc):
+    """in == out device pointers: count-sort round, block networks and the
+    in-process parallel radix sort."""
+    torch = cuda
+    L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    for n in (1000, 70001, (1 << 21) + 3, 3 << 22):
+        keys = orc.generate_uniform_keys(n, n + 1)
+        t = torch.from_numpy(keys.view(np.int32)).cuda()
+        assert L.bsg_count_sort_round_u32(ctx.handle, t.data_ptr(), t.data_ptr(), n, 1, 8, 1, st) == 0
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32), orc.count_sort_round(keys, 1, 256))
+        t = torch.from_numpy(keys.view(np.int32)).cuda()
+        assert L.bsg_parallel_radix_sort_u32(ctx.handle, t.data_ptr(), t.data_ptr(), n, 3, 8, -1, None, 1, st) == 0
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32), np.sort(keys))
+    arrs = orc.generate_uniform_keys(64 * 4096, 3).reshape(64, 4096)
+    t = torch.from_numpy(arrs.reshape(-1).view(np.int32)).cuda()
+    assert L.bsg_block_network_batched_u32(ctx.handle, 0, t.data_ptr(), t.data_ptr(), 64, 4096, 8, -1, None, 1,
+                                           st) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32).reshape(64, 4096), np.sort(arrs, axis=1))
