@@ -208,6 +208,12 @@ int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len,
                    const uint64_t* recv_counts, int p, int round, int radix_log2,
                    const int64_t* rebuild_delta, uint32_t* block, void* stream);
 
+/* Enables direct loads/stores from the context's device to every other
+ * device that supports peer access (NVLink / NVSwitch), for the peer-memory
+ * PR exchange.  Idempotent; devices without peer access are skipped.
+ * *enabled (optional) receives the number of peers now accessible. */
+int bsg_ctx_enable_peer_access(bsg_ctx* ctx, int* enabled);
+
 /* Fused exchange + rebuild over peer memory (NVLink): replaces the
  * all-to-all-v of sort_and_scatter (radix.hpp:275-290) and gather_slices
  * (radix.hpp:295-333) for one round of worker `me`.  `sorted` is me's block

@@ -86,6 +86,7 @@ SIGNATURES = {
     "bsg_pr_local_sort": (_i, [_vp, _u32p, _u32p, _u64, _i, _i, _vp]),
     "bsg_pr_plan_host": (_i, [_vp, _u64, _i, _i, _i, _vp, _vp, _vp]),
     "bsg_pr_rebuild": (_i, [_vp, _u32p, _u64, _vp, _i, _i, _i, _vp, _u32p, _vp]),
+    "bsg_ctx_enable_peer_access": (_i, [_vp, ctypes.POINTER(_i)]),
     "bsg_pr_peer_scatter": (_i, [_vp, _u32p, _u64, _vp, _u64, _i, _i, _i, _i, ctypes.POINTER(_vp), _vp]),
     "bsg_pr_fused_round": (_i, [_vp, _u32p, _u64, _vp, _u64, _i, _i, _i, _i, ctypes.POINTER(_vp), _vp]),
 }

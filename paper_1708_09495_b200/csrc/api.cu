@@ -408,6 +408,28 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
     return BSG_OK;
 }
 
+int bsg_ctx_enable_peer_access(bsg_ctx* ctx, int* enabled) {
+    if (int rc = check_ctx(ctx)) return rc;
+    CallGuard g(ctx);
+    int count = 0, ok = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    for (int d = 0; d < count; ++d) {
+        if (d == ctx->device) continue;
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, ctx->device, d) != cudaSuccess || !can) continue;
+        e = cudaDeviceEnablePeerAccess(d, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+            cudaGetLastError(); // clear the sticky-free status of this benign error
+            e = cudaSuccess;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        ++ok;
+    }
+    if (enabled) *enabled = ok;
+    return BSG_OK;
+}
+
 int bsg_pr_local_sort(bsg_ctx* ctx, const uint32_t* block, uint32_t* sorted, uint64_t len, int round, int radix_log2,
                       void* stream) {
     return bsg_count_sort_round_u32(ctx, block, sorted, len, round, radix_log2, BSG_MEM_DEVICE, stream);

@@ -133,6 +133,11 @@ class PeerBlocks:
         self.size = size
         self.local = [torch.empty(max(size, 1), dtype=torch.int32, device=self.device) for _ in range(2)]
         gathered: List = [None] * self.p
+        if self.p > 1:
+            # kernels on this device store into blocks that live on the other
+            # ranks' devices: enable peer access (NVLink) from this device
+            ctx = _lib.context(self.device.index or 0)
+            _lib.check(_lib.lib().bsg_ctx_enable_peer_access(ctx.handle, None), "enable peer access")
         if self.p > 1:  # nothing to map for a single rank
             mine = [reduce_tensor(t) for t in self.local]
             dist.all_gather_object(gathered, mine, group=group)
