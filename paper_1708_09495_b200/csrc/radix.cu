@@ -425,7 +425,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             constexpr int PB = ITEMS % 8 == 0 ? 8 : ITEMS;
 #pragma unroll
             for (int i0 = 0; i0 < ITEMS; i0 += PB) {
-                uint32_t peers[PB];
+                uint32_t peers[PB], dgt[PB];
 #pragma unroll
                 for (int ii = 0; ii < PB; ++ii) {
                     const int i = i0 + ii;
@@ -433,6 +433,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                     const bool ok = FULL || idx < valid;
                     const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
                                           : static_cast<uint32_t>(RADIX);
+                    dgt[ii] = d;
                     if (dbg & 2) peers[ii] = 1u << lane;
                     else if (RANK == 1) peers[ii] = __match_any_sync(0xffffffffu, d);
                     else peers[ii] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
@@ -442,12 +443,12 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                     const int i = i0 + ii;
                     const uint32_t idx = wbase + i * 32 + lane;
                     const bool ok = FULL || idx < valid;
-                    const uint32_t d =
-                        ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift)) : 0u;
+                    const uint32_t d = ok ? dgt[ii] : 0u;
                     const uint32_t before = ok ? wc[d] : 0u;
                     const bool leader = (peers[ii] & gt) == 0u; // highest peer: no peer above it
-                    if (leader && ok) wc[d] = static_cast<uint16_t>(before + __popc(peers[ii]));
                     const uint32_t r = before + __popc(peers[ii] & lt);
+                    // the highest peer's rank is before + (group size - 1)
+                    if (leader && ok) wc[d] = static_cast<uint16_t>(r + 1);
                     __syncwarp();
                     if (i & 1) packed[i >> 1] = __byte_perm(packed[i >> 1], r, 0x5410);
                     else packed[i >> 1] = r;
