@@ -422,7 +422,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             // batch), then the per-warp running counts of the batch, item by
             // item (input order): every peer reads the same counter (a
             // broadcast), the highest peer alone stores the advanced count.
-            constexpr int PB = ITEMS % 8 == 0 ? 8 : ITEMS;
+            constexpr int PB = ITEMS % 4 == 0 ? 4 : ITEMS;
 #pragma unroll
             for (int i0 = 0; i0 < ITEMS; i0 += PB) {
                 uint32_t peers[PB], dgt[PB];
