@@ -509,12 +509,22 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         phase(3);
 
         // ---- stage the tile in digit order (in place: keys are in registers)
+        if (dbg & 16) {
+            // timing experiment only: skip staging
+        } else if (full) { // every item valid: no per-item guards
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const uint32_t idx = wbase + i * 32 + lane;
-            if ((full || idx < valid) && !(dbg & 16)) {
+            for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
                 buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t idx = wbase + i * 32 + lane;
+                if (idx < valid) {
+                    const uint32_t r = (packed[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+                    buf[wc[digit_of_key<BITS>(keys[i], shift)] + r] = keys[i];
+                }
             }
         }
 
