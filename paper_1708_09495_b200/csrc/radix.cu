@@ -34,6 +34,9 @@
 #ifndef BSG_LB_WIN
 #define BSG_LB_WIN 12
 #endif
+#ifndef BSG_LB_WIN_SMALL
+#define BSG_LB_WIN_SMALL 4
+#endif
 namespace bsg {
 
 namespace {
@@ -315,7 +318,16 @@ struct PeerSink {
     }
 };
 
-template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK, typename Sink = PlainSink>
+// Look-back window (predecessors per round trip), measured per configuration:
+// 1024-thread CTAs (one per SM) 12; 512-thread CTAs (two per SM, twice the
+// tiles in flight) 4 -- a wider window costs more than the extra round trips.
+template <int THREADS>
+constexpr int default_lb_window() {
+    return THREADS <= 512 ? BSG_LB_WIN_SMALL : BSG_LB_WIN;
+}
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK, typename Sink = PlainSink,
+          int LBW = default_lb_window<THREADS>()>
 __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const uint32_t* __restrict__ src,
                                                Sink dst, uint64_t chunk_n, int shift,
                                                const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
@@ -533,7 +545,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         // (each warp's load covers 32 consecutive digits of one predecessor:
         // one coalesced 128-byte request per predecessor per warp)
         if (tid < RADIX) {
-            constexpr int LB_WIN = BSG_LB_WIN;
+            constexpr int LB_WIN = LBW;
             Stat prefix = 0;
             if (tile > 0 && !(dbg & 1)) {
                 int64_t t = static_cast<int64_t>(tile) - 1;
@@ -683,16 +695,17 @@ template <int BITS>
 int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                          int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
     const bool wide = n > kChunkKeys;
-    if (wide) // n > 2^29: 64-bit status words and positions, 24-key rows
-        return launch_onesweep_cfg<BITS, 1024, 24, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+    if (wide) // n > 2^29: 64-bit status words and positions, the large-n rows
+        return launch_onesweep_cfg<BITS, 512, 24, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                         stream, use_tma);
     if constexpr (BITS != 8)
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     int cfg = onesweep_cfg();
     // measured on B200 (profiles/r01_onesweep_cfg_sweep.txt): 512x16 up to
-    // 2^21 keys, 1024x16 up to 2^23, 1024x24 (24576-key tiles) beyond
-    if (cfg == 0) cfg = n <= (uint64_t{1} << 21) ? 1 : (n <= (uint64_t{1} << 23) ? 2 : 4);
+    // 2^21 keys (only when the fused small-n sort is off), 1024x16 up to 2^23,
+    // 512x24 beyond (12288-key tiles, two CTAs per SM, 4-wide look-back)
+    if (cfg == 0) cfg = n <= (uint64_t{1} << 21) ? 1 : (n <= (uint64_t{1} << 23) ? 2 : 6);
     switch (cfg) {
     case 3: // 256 x 16: 4096-key tiles so small inputs still fill 148 SMs
         return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
@@ -721,8 +734,8 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
 template <int BITS>
 uint64_t status_words_for(uint64_t n) {
     constexpr int RADIX = 1 << BITS;
-    if (n > kChunkKeys) // WIDE: 1024 x 24 tiles, 64-bit status words
-        return 32 + ((n + 24575) / 24576) * RADIX * 2;
+    if (n > kChunkKeys) // WIDE: 512 x 24 tiles, 64-bit status words
+        return 32 + ((n + 12287) / 12288) * RADIX * 2;
     return 32 + ((n + kMinTile - 1) / kMinTile) * RADIX;
 }
 
@@ -845,7 +858,9 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
     for (int p = 0; p < 4; ++p) {
         if (!s_active[p]) continue;
         uint32_t* region = regions + static_cast<uint64_t>(p) * region_words;
-        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0>(smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p,
+        // all tiles are in flight at once here: the wide window
+        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0, PlainSink, BSG_LB_WIN>(
+            smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p,
                                                                s_base + p * 256, region + 32, region, use_tma, 0,
                                                                neg1, first, parity);
         first = false;
@@ -964,7 +979,7 @@ int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shif
     case 4: return launch_onesweep_peer_cfg<4, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
     case 8:
         if (len > (uint64_t{1} << 23))
-            return launch_onesweep_peer_cfg<8, 1024, 24>(block, n, shift, digit_base, status, tab, p, stream);
+            return launch_onesweep_peer_cfg<8, 512, 24>(block, n, shift, digit_base, status, tab, p, stream);
         return launch_onesweep_peer_cfg<8, 512, 16>(block, n, shift, digit_base, status, tab, p, stream);
     default: return -1;
     }
