@@ -587,7 +587,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         if (dbg & 4) {
             // timing experiment only: skip the write-out
         } else if (full) {
-#pragma unroll 4
+#pragma unroll
             for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = j * THREADS + tid;
                 const uint32_t key = buf[i];
