@@ -76,7 +76,7 @@ constexpr int kMaxP = 1024;
 
 __global__ void __launch_bounds__(kRebuildThreads)
     pr_rebuild_kernel(const uint32_t* __restrict__ recv, uint64_t recv_len, int p,
-                      const uint64_t* __restrict__ recv_counts, const uint32_t* const* __restrict__ src_ptrs,
+                      const uint64_t* __restrict__ recv_counts,
                       uint32_t mask, int shift, int radix, const int64_t* __restrict__ delta,
                       uint32_t* __restrict__ block) {
     __shared__ uint64_t s_off[kMaxP + 1];
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kRebuildThreads)
             else hi = mid - 1;
         }
         const int v = lo;
-        const uint32_t key = src_ptrs ? src_ptrs[v][j - s_off[v]] : recv[j];
+        const uint32_t key = recv[j];
         const uint32_t d = (key >> shift) & mask;
         block[static_cast<uint64_t>(delta[static_cast<uint64_t>(v) * radix + d] + static_cast<int64_t>(j))] = key;
     }
@@ -505,7 +505,7 @@ int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shi
     const uint64_t want = (recv_len + kRebuildThreads * 8 - 1) / (kRebuildThreads * 8);
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
     TimedScope ts(3 /*BSG_K_PR*/, stream);
-    pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(recv, recv_len, p, recv_counts, nullptr, (1u << bits) - 1u,
+    pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(recv, recv_len, p, recv_counts, (1u << bits) - 1u,
                                                            shift, 1 << bits, rebuild_delta, block);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
