@@ -298,6 +298,12 @@ struct OnesweepSmem {
 // first key of the chunk.  `bar_parity` carries the two mbarriers' phase
 // parities across calls (the fused small-n sort runs several passes in one
 // launch); `init_bars` initialises them on the first call.
+// Keys before the first 16-byte boundary at p (at most 3, at most valid).
+__device__ __forceinline__ uint32_t head_words(const uint32_t* p, uint32_t valid) {
+    const uint32_t hw = (4u - static_cast<uint32_t>((reinterpret_cast<uintptr_t>(p) >> 2) & 3u)) & 3u;
+    return hw < valid ? hw : valid;
+}
+
 // Output sinks of the write-out: one array, or the owners' blocks of a PR round.
 struct PlainSink {
     uint32_t* __restrict__ dst;
@@ -363,10 +369,13 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         if (tile >= ntiles) return;
         const uint64_t start = static_cast<uint64_t>(tile) * TILE;
         const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), chunk_n - start));
-        const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
+        // TMA moves the tile's 16-byte-aligned body; the <= 3 head and <= 3
+        // tail keys are read with plain loads by the ranking threads
+        const uint32_t hw = head_words(src + start, valid);
+        const uint32_t body = use_tma ? ((valid - hw) & ~3u) : 0u;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&s_bar[b], vec * 4);
-        if (vec) tma_bulk_g2s(s_in + b * TILE, src + start, vec * 4, &s_bar[b]);
+        mbar_arrive_expect_tx(&s_bar[b], body * 4);
+        if (body) tma_bulk_g2s(s_in + b * TILE, src + start + hw, body * 4, &s_bar[b]);
     };
 
     if (tid == 0) {
@@ -399,7 +408,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         const bool full = valid == TILE;
         uint32_t* buf = s_in + cur * TILE;
         // non-TMA body / unaligned tail straight from global
-        const uint32_t vec = use_tma ? (valid & ~3u) : 0u;
+        const uint32_t hw = head_words(src + tile_start, valid);
+        const uint32_t body = use_tma ? ((valid - hw) & ~3u) : 0u;
         long long t_ph = (dbg & 8) ? clock64() : 0;
         auto phase = [&](int ph) {
             if ((dbg & 8) && tid == 0) {
@@ -419,15 +429,19 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         uint16_t* wc = s_wcnt + warp * RADIX;
         uint32_t keys[ITEMS];
         uint32_t packed[ITEMS / 2];
-        auto rank_items = [&](auto full_tag) {
+        auto rank_items = [&](auto full_tag, auto aligned_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
+            constexpr bool ALIGNED = decltype(aligned_tag)::value;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const uint32_t idx = wbase + i * 32 + lane;
-                if (FULL) { // whole tile delivered by TMA
+                const uint32_t rel = idx - hw; // wraps for head keys
+                if (FULL && ALIGNED) { // whole tile delivered by TMA
                     keys[i] = buf[idx];
+                } else if (FULL) {
+                    keys[i] = rel < body ? buf[rel] : __ldg(src + tile_start + idx);
                 } else {
-                    keys[i] = idx < valid ? (idx < vec ? buf[idx] : __ldg(src + tile_start + idx)) : 0u;
+                    keys[i] = idx < valid ? (rel < body ? buf[rel] : __ldg(src + tile_start + idx)) : 0u;
                 }
             }
             // multisplit masks in batches of PB items (independent inside a
@@ -469,8 +483,9 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         };
         // full TMA tiles rank straight from shared memory; partial tiles and
         // misaligned (non-TMA) bodies take the guarded path
-        if (full && vec == static_cast<uint32_t>(TILE)) rank_items(std::true_type{});
-        else rank_items(std::false_type{});
+        if (full && hw == 0 && body == static_cast<uint32_t>(TILE)) rank_items(std::true_type{}, std::true_type{});
+        else if (full) rank_items(std::true_type{}, std::false_type{});
+        else rank_items(std::false_type{}, std::false_type{});
         phase(1);
         __syncthreads();
         phase(2);
@@ -961,7 +976,7 @@ int launch_onesweep_peer_cfg(const uint32_t* block, uint32_t len, int shift, con
     if (cudaMemsetAsync(status, 0, (32 + static_cast<uint64_t>(tiles) * RADIX) * sizeof(uint32_t), stream) !=
         cudaSuccess)
         return -1;
-    const bool tma = (reinterpret_cast<uintptr_t>(block) & 15) == 0;
+    const bool tma = true; // per-tile aligned bodies (head/tail keys via plain loads)
     TimedScope ts(3 /*BSG_K_PR*/, stream);
     kern<<<grid, THREADS, L::bytes, stream>>>(block, len, shift, digit_base, status + 32, status, tma ? 1 : 0, -1,
                                               tab, p);
@@ -998,8 +1013,7 @@ int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const Radi
     const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
     int launches = 0;
     {
-        const bool tma = allow_tma && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
-                                        reinterpret_cast<uintptr_t>(ws.tmp)) & 15) == 0;
+        const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
         const int l = launch_small_sort(in, out, n, ws, stream, tma);
         if (l != 0) return l;
     }
@@ -1014,8 +1028,7 @@ int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const Radi
     scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), PASSES, RADIX, n, ws.base,
                                                      ws.plan, in, out, ws.tmp, 1);
     ++launches;
-    const bool tma = allow_tma && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
-                                    reinterpret_cast<uintptr_t>(ws.tmp)) & 15) == 0;
+    const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
     for (int p = 0; p < PASSES && n; ++p) {
         const int l = launch_onesweep_pass<8>(ws.plan, p, n, 8 * p, ws.base + p * RADIX, PASSES, ws.status, stream, tma);
         if (l < 0) return -1;
@@ -1051,8 +1064,7 @@ int launch_count_pass(const uint32_t* in, uint32_t* out, uint64_t n, int bits, i
     scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), 1, radix, n, ws.base, ws.plan,
                                                      in, out, ws.tmp, 1);
     ++launches;
-    const bool tma = allow_tma && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
-                                    reinterpret_cast<uintptr_t>(ws.tmp)) & 15) == 0;
+    const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
     if (n) {
         uint64_t sw = 0;
         switch (bits) {
