@@ -411,6 +411,64 @@ __global__ void pr_fused_base_kernel(const uint64_t* __restrict__ dstart, const 
     if (d < radix) base[d] = dstart[d] + static_cast<uint64_t>(before_me[d]);
 }
 
+// count_digits of every worker block in one launch (grid.y = worker).
+// Lane-private shared counters (counter c of lane l at word c*32 + l: a
+// warp's 32 increments never share a bank, as in K1), 4 loads in flight per
+// thread; one global atomic per (CTA, digit).  counts must be zero on entry.
+constexpr int kSegCountThreads = 512;
+template <int RADIX>
+__global__ void __launch_bounds__(kSegCountThreads)
+    pr_seg_count_kernel(const uint32_t* __restrict__ keys, uint64_t n, int p, int shift,
+                        unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t h[RADIX * 32];
+    for (int i = threadIdx.x; i < RADIX * 32; i += kSegCountThreads) h[i] = 0;
+    __syncthreads();
+    const int w = blockIdx.y;
+    const uint64_t off = part_offset(n, p, w), len = part_size(n, p, w);
+    uint32_t* mine = h + (threadIdx.x & 31);
+    const uint32_t* blk = keys + off;
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * kSegCountThreads;
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * kSegCountThreads + threadIdx.x;
+    for (; i + 3 * step < len; i += 4 * step) {
+        const uint32_t k0 = __ldg(blk + i), k1 = __ldg(blk + i + step), k2 = __ldg(blk + i + 2 * step),
+                       k3 = __ldg(blk + i + 3 * step);
+        atomicAdd(mine + ((k0 >> shift) & (RADIX - 1)) * 32, 1u);
+        atomicAdd(mine + ((k1 >> shift) & (RADIX - 1)) * 32, 1u);
+        atomicAdd(mine + ((k2 >> shift) & (RADIX - 1)) * 32, 1u);
+        atomicAdd(mine + ((k3 >> shift) & (RADIX - 1)) * 32, 1u);
+    }
+    for (; i < len; i += step) atomicAdd(mine + ((__ldg(blk + i) >> shift) & (RADIX - 1)) * 32, 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < RADIX; d += kSegCountThreads) {
+        uint32_t c = 0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) c += h[d * 32 + ((l + d) & 31)]; // rotated: no bank conflicts
+        if (c) atomicAdd(&counts[static_cast<uint64_t>(w) * RADIX + d], static_cast<unsigned long long>(c));
+    }
+}
+
+int launch_pr_seg_count(const uint32_t* keys, uint64_t n, int p, int bits, int shift, uint64_t* counts,
+                        cudaStream_t stream) {
+    const int radix = 1 << bits;
+    if (cudaMemsetAsync(counts, 0, static_cast<uint64_t>(p) * radix * sizeof(uint64_t), stream) != cudaSuccess)
+        return -1;
+    if (n == 0) return 0;
+    const uint64_t per = n / static_cast<uint64_t>(p) + 1;
+    const uint64_t want = (per + kSegCountThreads * 32 - 1) / (kSegCountThreads * 32);
+    const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(want, std::max<uint64_t>(1, kSmCountB200 * 4 / static_cast<uint64_t>(p)))));
+    auto* c = reinterpret_cast<unsigned long long*>(counts);
+    const dim3 grid(gx, static_cast<unsigned>(p));
+    switch (bits) {
+    case 1: pr_seg_count_kernel<2><<<grid, kSegCountThreads, 0, stream>>>(keys, n, p, shift, c); break;
+    case 2: pr_seg_count_kernel<4><<<grid, kSegCountThreads, 0, stream>>>(keys, n, p, shift, c); break;
+    case 4: pr_seg_count_kernel<16><<<grid, kSegCountThreads, 0, stream>>>(keys, n, p, shift, c); break;
+    case 8: pr_seg_count_kernel<256><<<grid, kSegCountThreads, 0, stream>>>(keys, n, p, shift, c); break;
+    default: return -1;
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 // In-process fused round: base[v][d] = digit_start[d] + sum_{u<v} cnt(u,d),
 // in place over the column-prefix table.
 __global__ void pr_add_dstart_kernel(int64_t* __restrict__ before, const uint64_t* __restrict__ dstart, int p,
@@ -552,18 +610,17 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     // bases are the global positions of its block's first key per digit
     // (the same fused round as bsg_pr_fused_round, all blocks local)
     const bool fused = bits <= 8 && max_len <= kChunkKeys;
+    if (fused && (e = ctx->status.ensure(onesweep_seg_status_words(n, p) * sizeof(uint32_t))) != cudaSuccess)
+        return cuda_fail(e, "pr workspace");
     uint32_t* cur = A;
     uint32_t* nxt = S;
     for (int round = 0; round < rounds && n && fused; ++round) {
         const int shift = round * bits;
         uint64_t* counts = starts; // [p][radix]
         int64_t* base = gd;        // [p][radix]
-        for (int w = 0; w < p; ++w) {
-            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
-            if (!add(launch_pr_count(ctx, cur + off, sz, round, bits, counts + static_cast<uint64_t>(w) * radix,
-                                     stream)))
-                return cuda_fail(cudaGetLastError(), "pr count");
-        }
+        // count_digits of every worker (radix.hpp:238-243), one launch
+        if (!add(launch_pr_seg_count(cur, n, p, bits, shift, counts, stream)))
+            return cuda_fail(cudaGetLastError(), "pr count");
         {
             TimedScope ts(3 /*BSG_K_PR*/, stream);
             const int chunks = (radix + kDigChunk - 1) / kDigChunk;
@@ -573,18 +630,11 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             pr_add_dstart_kernel<<<static_cast<unsigned>((pr + 255) / 256), 256, 0, stream>>>(base, dstart, p, radix);
             launches += 3;
         }
-        PeerTable tab{};
-        tab.blocks[0] = nxt;
-        tab.offset[0] = 0;
-        tab.offset[1] = n;
-        for (int w = 0; w < p; ++w) {
-            const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
-            if (sz == 0) continue;
-            if (!add(launch_onesweep_peer(cur + off, sz, bits, shift,
-                                          reinterpret_cast<const uint64_t*>(base + static_cast<uint64_t>(w) * radix),
-                                          ctx->status.as<uint32_t>(), tab, 1, stream)))
-                return cuda_fail(cudaGetLastError(), "pr fused pass");
-        }
+        // every worker's local stable pass, stored at the global positions
+        // (sort_and_scatter + exchange + gather_slices), one segmented launch
+        if (!add(launch_onesweep_seg(cur, nxt, n, p, bits, shift, reinterpret_cast<const uint64_t*>(base),
+                                     ctx->status.as<uint32_t>(), stream)))
+            return cuda_fail(cudaGetLastError(), "pr fused pass");
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
         if (stats) {
             if ((e = cudaMemsetAsync(send, 0, pp * 8, stream)) != cudaSuccess) return cuda_fail(e, "pr stats");

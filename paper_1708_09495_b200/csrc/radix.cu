@@ -298,6 +298,37 @@ struct OnesweepSmem {
 // first key of the chunk.  `bar_parity` carries the two mbarriers' phase
 // parities across calls (the fused small-n sort runs several passes in one
 // launch); `init_bars` initialises them on the first call.
+// Segmented pass (the p worker blocks of an in-process PR round in ONE
+// launch): segment w = Partition(n, p) block w, nbig blocks of small+1 keys
+// then p-nbig of small keys; each segment is its own look-back domain with
+// its own digit bases (base table [p][radix]).  tiles are numbered segment
+// by segment, so tile -> (segment, start) is a closed form.
+struct SegDesc {
+    uint64_t small;       // n / p
+    uint32_t p, nbig;     // nbig = n % p
+    uint32_t tiles_big;   // ceil((small + 1) / TILE)
+    uint32_t tiles_small; // ceil(small / TILE)
+};
+struct SegTile {
+    uint32_t seg, first; // segment and its first tile id
+    uint64_t start, end; // key range of the segment
+};
+template <int TILE>
+__device__ __forceinline__ SegTile seg_of_tile(const SegDesc& sd, uint32_t tile) {
+    SegTile r;
+    const uint32_t big_tiles = sd.nbig * sd.tiles_big;
+    if (tile < big_tiles) {
+        r.seg = tile / sd.tiles_big;
+        r.first = r.seg * sd.tiles_big;
+    } else {
+        r.seg = sd.nbig + (sd.tiles_small ? (tile - big_tiles) / sd.tiles_small : 0u);
+        r.first = big_tiles + (r.seg - sd.nbig) * sd.tiles_small;
+    }
+    r.start = static_cast<uint64_t>(r.seg) * sd.small + (r.seg < sd.nbig ? r.seg : sd.nbig);
+    r.end = r.start + sd.small + (r.seg < sd.nbig ? 1 : 0);
+    return r;
+}
+
 // Keys before the first 16-byte boundary at p (at most 3, at most valid).
 __device__ __forceinline__ uint32_t head_words(const uint32_t* p, uint32_t valid) {
     const uint32_t hw = (4u - static_cast<uint32_t>((reinterpret_cast<uintptr_t>(p) >> 2) & 3u)) & 3u;
@@ -333,12 +364,13 @@ constexpr int default_lb_window() {
 }
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK, typename Sink = PlainSink,
-          int LBW = default_lb_window<THREADS>()>
+          int LBW = default_lb_window<THREADS>(), bool SEG = false>
 __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const uint32_t* __restrict__ src,
                                                Sink dst, uint64_t chunk_n, int shift,
                                                const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                                                uint32_t* __restrict__ tile_counter, int use_tma, int dbg,
-                                               int32_t neg1, bool init_bars, uint32_t& bar_parity) {
+                                               int32_t neg1, bool init_bars, uint32_t& bar_parity,
+                                               const SegDesc sd = SegDesc{}) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     using Off = typename L::Off;
     constexpr int RADIX = L::RADIX;
@@ -355,7 +387,23 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
 
-    const uint32_t ntiles = static_cast<uint32_t>((chunk_n + TILE - 1) / TILE);
+    const uint32_t ntiles = SEG ? sd.nbig * sd.tiles_big + (sd.p - sd.nbig) * sd.tiles_small
+                                : static_cast<uint32_t>((chunk_n + TILE - 1) / TILE);
+    // tile -> key range [start, start+valid), look-back floor, digit-base row
+    auto tile_range = [&](uint32_t tile, uint64_t& start, uint32_t& valid, uint32_t& first, uint32_t& seg) {
+        if constexpr (SEG) {
+            const SegTile st = seg_of_tile<TILE>(sd, tile);
+            start = st.start + static_cast<uint64_t>(tile - st.first) * TILE;
+            valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), st.end - start));
+            first = st.first;
+            seg = st.seg;
+        } else {
+            start = static_cast<uint64_t>(tile) * TILE;
+            valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), chunk_n - start));
+            first = 0;
+            seg = 0;
+        }
+    };
     using SW = StatusWord<WIDE>;
     using Stat = typename SW::T;
     Stat* __restrict__ stat = reinterpret_cast<Stat*>(status);
@@ -367,8 +415,9 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
     auto issue = [&](uint32_t tile, int b) {
         if (tile >= ntiles) return;
-        const uint64_t start = static_cast<uint64_t>(tile) * TILE;
-        const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), chunk_n - start));
+        uint64_t start;
+        uint32_t valid, first_unused, seg_unused;
+        tile_range(tile, start, valid, first_unused, seg_unused);
         // TMA moves the tile's 16-byte-aligned body; the <= 3 head and <= 3
         // tail keys are read with plain loads by the ranking threads
         const uint32_t hw = head_words(src + start, valid);
@@ -403,8 +452,9 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             s_tile[cur ^ 1] = nxt;
             issue(nxt, cur ^ 1);
         }
-        const uint64_t tile_start = static_cast<uint64_t>(tile) * TILE;
-        const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), chunk_n - tile_start));
+        uint64_t tile_start;
+        uint32_t valid, tfirst, seg;
+        tile_range(tile, tile_start, valid, tfirst, seg);
         const bool full = valid == TILE;
         uint32_t* buf = s_in + cur * TILE;
         // non-TMA body / unaligned tail straight from global
@@ -505,7 +555,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 run2 += c2;
             }
             const uint32_t lo = run2 & 0xFFFFu, hi = run2 >> 16;
-            const Stat flag = tile == 0 ? SW::INC : SW::AGG;
+            const Stat flag = tile == tfirst ? SW::INC : SW::AGG;
             st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + 2 * tid], flag | static_cast<Stat>(lo));
             st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + 2 * tid + 1], flag | static_cast<Stat>(hi));
         }
@@ -562,14 +612,15 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         if (tid < RADIX) {
             constexpr int LB_WIN = LBW;
             Stat prefix = 0;
-            if (tile > 0 && !(dbg & 1)) {
+            if (tile > tfirst && !(dbg & 1)) {
                 int64_t t = static_cast<int64_t>(tile) - 1;
                 while (true) {
                     if ((dbg & 8) && tid == 0) atomicAdd(&g_phase_cycles[7], 1ull);
                     Stat sv[LB_WIN];
 #pragma unroll
                     for (int j = 0; j < LB_WIN; ++j)
-                        sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&stat[static_cast<uint64_t>(t - j) * RADIX + tid])
+                        sv[j] = (t - j >= static_cast<int64_t>(tfirst))
+                                    ? ld_relaxed_gpu(&stat[static_cast<uint64_t>(t - j) * RADIX + tid])
                                              : SW::INC;
                     int used = 0;
                     bool done = false, stop = false;
@@ -589,10 +640,11 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                     t -= used;
                 }
             }
-            if (tile > 0)
+            if (tile > tfirst)
                 st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + tid],
                                SW::INC | (prefix + static_cast<Stat>(tile_cnt)));
-            s_delta[tid] = static_cast<Off>(digit_base[tid] + prefix - s_excl[tid]);
+            s_delta[tid] = static_cast<Off>(digit_base[static_cast<uint64_t>(seg) * RADIX + tid] + prefix -
+                                            s_excl[tid]);
         }
         __syncthreads();
 
@@ -998,6 +1050,72 @@ int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shif
         return launch_onesweep_peer_cfg<8, 512, 16>(block, n, shift, digit_base, status, tab, p, stream);
     default: return -1;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Segmented pass: all worker blocks of an in-process PR round in one launch.
+// ---------------------------------------------------------------------------
+template <int BITS, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
+    onesweep_seg_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, const SegDesc sd, int shift,
+                        const uint64_t* __restrict__ base_table, uint32_t* __restrict__ status,
+                        uint32_t* __restrict__ tile_counter, int32_t neg1) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t parity = 0;
+    onesweep_tiles<BITS, THREADS, ITEMS, false, 0, PlainSink, default_lb_window<THREADS>(), true>(
+        smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
+}
+
+template <int BITS, int THREADS, int ITEMS>
+int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int shift,
+                            const uint64_t* base_table, uint32_t* status, cudaStream_t stream) {
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, false>;
+    constexpr int RADIX = 1 << BITS;
+    auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS>;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, L::bytes);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int sms = kSmCountB200, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    SegDesc sd;
+    sd.small = n / static_cast<uint64_t>(p);
+    sd.p = static_cast<uint32_t>(p);
+    sd.nbig = static_cast<uint32_t>(n % static_cast<uint64_t>(p));
+    sd.tiles_big = static_cast<uint32_t>((sd.small + 1 + L::TILE - 1) / L::TILE);
+    sd.tiles_small = static_cast<uint32_t>((sd.small + L::TILE - 1) / L::TILE);
+    const uint64_t tiles = static_cast<uint64_t>(sd.nbig) * sd.tiles_big +
+                           static_cast<uint64_t>(sd.p - sd.nbig) * sd.tiles_small;
+    if (tiles == 0) return 0;
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * per_sm));
+    if (cudaMemsetAsync(status, 0, (32 + tiles * RADIX) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
+    kern<<<grid, THREADS, L::bytes, stream>>>(src, dst, sd, shift, base_table, status + 32, status, -1);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
+                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream) {
+    if (n == 0) return 0;
+    if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys) return -1;
+    switch (bits) {
+    case 1: return launch_onesweep_seg_cfg<1, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
+    case 2: return launch_onesweep_seg_cfg<2, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
+    case 4: return launch_onesweep_seg_cfg<4, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
+    case 8:
+        if (n > (uint64_t{1} << 23))
+            return launch_onesweep_seg_cfg<8, 512, 24>(src, dst, n, p, shift, base_table, status, stream);
+        return launch_onesweep_seg_cfg<8, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
+    default: return -1;
+    }
+}
+
+uint64_t onesweep_seg_status_words(uint64_t n, int p) {
+    // 8192-key tiles at the smallest: one extra partial tile per segment
+    return 32 + (n / 8192 + static_cast<uint64_t>(p) + 1) * 256;
 }
 
 uint64_t onesweep_status_words(uint64_t n) {

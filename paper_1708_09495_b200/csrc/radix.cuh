@@ -63,6 +63,14 @@ struct PeerTable {
 // worker's block whose digit bases are the global positions of the block's
 // first key per digit (digit_base, device [radix]); every key is stored at
 // its final position in its owner's block.  len <= kChunkKeys.
+// The stable pass of all p worker blocks (Partition(n, p)) of an in-process
+// PR round in ONE launch: key i of block w with digit d goes to
+// base_table[w][d] + (its rank among block w's digit-d keys).  Returns
+// launches (0 or 1) or -1.
+int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
+                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream);
+uint64_t onesweep_seg_status_words(uint64_t n, int p);
+
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
                          uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream);
 
