@@ -34,6 +34,15 @@
 #ifndef BSG_LB_WIN
 #define BSG_LB_WIN 12
 #endif
+#ifndef BSG_CLAIM_AT
+#define BSG_CLAIM_AT 0 // where a one-sweep CTA claims its next tile: 0 loop top, 1 after staging, 2 after look-back
+#endif
+#ifndef BSG_OS_DBG_MASK
+#define BSG_OS_DBG_MASK 0 // development builds: -DBSG_OS_DBG_MASK=31 enables the BSG_OS_DBG timing switches
+#endif
+#ifndef BSG_LB_FIRST
+#define BSG_LB_FIRST 0 // wider first look-back round (predecessors), 0 = same as the window
+#endif
 #ifndef BSG_LB_WIN_SMALL
 #define BSG_LB_WIN_SMALL 4
 #endif
@@ -271,6 +280,10 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
 // Phase-cycle instrumentation (dbg bit 8): thread 0 of every CTA accumulates
 // clock64 deltas per phase.  Development aid only.
 __device__ unsigned long long g_phase_cycles[8];
+#ifndef BSG_LB_STATS
+#define BSG_LB_STATS 0 // development: look-back round/predecessor/stall counts (g_lb_stats)
+#endif
+__device__ unsigned long long g_lb_stats[4]; // rounds, predecessors consumed, unpublished stops, tiles
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 struct OnesweepSmem {
@@ -373,6 +386,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                                                const SegDesc sd = SegDesc{}) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     using Off = typename L::Off;
+    dbg &= BSG_OS_DBG_MASK; // timing switches exist only in development builds
     constexpr int RADIX = L::RADIX;
     constexpr int WARPS = L::WARPS;
     constexpr int TILE = L::TILE;
@@ -441,17 +455,23 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
 
     const uint32_t lt = lanemask_lt();
     const uint32_t gt = ~(lt | (1u << lane));
+    uint32_t lbs_rounds = 0, lbs_used = 0, lbs_stops = 0, lbs_tiles = 0;
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
     for (uint32_t k = 0;; ++k) {
         const int cur = k & 1;
         __syncthreads(); // s_tile[cur] visible; previous tile's buffer/counters free
         const uint32_t tile = s_tile[cur];
         if (tile >= ntiles) break;
-        if (tid == 0) {
-            const uint32_t nxt = atomicAdd(tile_counter, 1u);
-            s_tile[cur ^ 1] = nxt;
-            issue(nxt, cur ^ 1);
-        }
+        // claim the next tile and start its TMA load (buffer cur^1 is free:
+        // its tile was written out before the barrier above)
+        auto claim_next = [&]() {
+            if (tid == 0) {
+                const uint32_t nxt = atomicAdd(tile_counter, 1u);
+                s_tile[cur ^ 1] = nxt;
+                issue(nxt, cur ^ 1);
+            }
+        };
+        if (BSG_CLAIM_AT == 0) claim_next();
         uint64_t tile_start;
         uint32_t valid, tfirst, seg;
         tile_range(tile, tile_start, valid, tfirst, seg);
@@ -605,41 +625,53 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             }
         }
 
+        if (BSG_CLAIM_AT == 1) claim_next();
         phase(4);
         // ---- decoupled look-back: LB_WIN predecessors per round trip ------
         // (each warp's load covers 32 consecutive digits of one predecessor:
         // one coalesced 128-byte request per predecessor per warp)
         if (tid < RADIX) {
             constexpr int LB_WIN = LBW;
+            constexpr int LB_FIRST = BSG_LB_FIRST > LBW ? BSG_LB_FIRST : LBW;
             Stat prefix = 0;
-            if (tile > tfirst && !(dbg & 1)) {
-                int64_t t = static_cast<int64_t>(tile) - 1;
-                while (true) {
-                    if ((dbg & 8) && tid == 0) atomicAdd(&g_phase_cycles[7], 1ull);
-                    Stat sv[LB_WIN];
+            // one round trip: W predecessors from t down; consumes the
+            // published ones up to the first inclusive (done) or unpublished
+            auto lb_round = [&](auto wtag, int64_t& t, bool& done) {
+                constexpr int W = decltype(wtag)::value;
+                Stat sv[W];
 #pragma unroll
-                    for (int j = 0; j < LB_WIN; ++j)
-                        sv[j] = (t - j >= static_cast<int64_t>(tfirst))
-                                    ? ld_relaxed_gpu(&stat[static_cast<uint64_t>(t - j) * RADIX + tid])
-                                             : SW::INC;
-                    int used = 0;
-                    bool done = false, stop = false;
+                for (int j = 0; j < W; ++j)
+                    sv[j] = (t - j >= static_cast<int64_t>(tfirst))
+                                ? ld_relaxed_gpu(&stat[static_cast<uint64_t>(t - j) * RADIX + tid])
+                                : SW::INC;
+                int used = 0;
+                bool stop = false;
 #pragma unroll
-                    for (int j = 0; j < LB_WIN; ++j) {
-                        if (!stop) {
-                            if ((sv[j] & ~SW::VAL) == 0) {
-                                stop = true;
-                            } else {
-                                prefix += sv[j] & SW::VAL;
-                                ++used;
-                                if (sv[j] & SW::INC) done = stop = true;
-                            }
+                for (int j = 0; j < W; ++j) {
+                    if (!stop) {
+                        if ((sv[j] & ~SW::VAL) == 0) {
+                            stop = true;
+                        } else {
+                            prefix += sv[j] & SW::VAL;
+                            ++used;
+                            if (sv[j] & SW::INC) done = stop = true;
                         }
                     }
-                    if (done) break;
-                    t -= used;
                 }
+                if (BSG_LB_STATS) {
+                    ++lbs_rounds;
+                    lbs_used += used;
+                    lbs_stops += (!done && used < W) ? 1 : 0;
+                }
+                t -= used;
+            };
+            if (tile > tfirst && !(dbg & 1)) {
+                int64_t t = static_cast<int64_t>(tile) - 1;
+                bool done = false;
+                if constexpr (LB_FIRST > LB_WIN) lb_round(std::integral_constant<int, LB_FIRST>{}, t, done);
+                while (!done) lb_round(std::integral_constant<int, LB_WIN>{}, t, done);
             }
+            if (BSG_LB_STATS) ++lbs_tiles;
             if (tile > tfirst)
                 st_relaxed_gpu(&stat[static_cast<uint64_t>(tile) * RADIX + tid],
                                SW::INC | (prefix + static_cast<Stat>(tile_cnt)));
@@ -648,6 +680,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         }
         __syncthreads();
 
+        if (BSG_CLAIM_AT == 2) claim_next();
         phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
         for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
@@ -668,10 +701,24 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         }
         phase(6);
     }
+    if (BSG_LB_STATS && tid < RADIX && lane == 0) {
+        atomicAdd(&g_lb_stats[0], static_cast<unsigned long long>(lbs_rounds));
+        atomicAdd(&g_lb_stats[1], static_cast<unsigned long long>(lbs_used));
+        atomicAdd(&g_lb_stats[2], static_cast<unsigned long long>(lbs_stops));
+        atomicAdd(&g_lb_stats[3], static_cast<unsigned long long>(lbs_tiles));
+    }
+}
+
+#ifndef BSG_OS_MINB16
+#define BSG_OS_MINB16 2
+#endif
+template <int THREADS, int ITEMS>
+constexpr int onesweep_min_blocks() {
+    return THREADS <= 512 ? (ITEMS <= 16 ? BSG_OS_MINB16 : 2) : 1;
 }
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK>
-__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
+__global__ void __launch_bounds__(THREADS, (onesweep_min_blocks<THREADS, ITEMS>()))
     onesweep_kernel(const PassPlan* __restrict__ plan, int pass, uint64_t chunk_off, uint64_t chunk_n,
                     int shift, const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                     uint32_t* __restrict__ tile_counter, int use_tma, int dbg, int32_t neg1) {
@@ -1264,6 +1311,15 @@ extern "C" int bsg_debug_set_small_sort(int on) {
 
 // Development aid: reads (and optionally clears) the one-sweep phase-cycle
 // accumulators filled when BSG_OS_DBG has bit 8 set.
+extern "C" int bsg_debug_lb_stats(unsigned long long* out4, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out4, bsg::g_lb_stats, sizeof(unsigned long long) * 4);
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        e = cudaMemcpyToSymbol(bsg::g_lb_stats, z, sizeof(z));
+    }
+    return e == cudaSuccess ? 0 : 3;
+}
+
 extern "C" int bsg_debug_phase_cycles(unsigned long long* out8, int reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out8, bsg::g_phase_cycles, sizeof(unsigned long long) * 8);
     if (e == cudaSuccess && reset) {
