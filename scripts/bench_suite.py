@@ -115,11 +115,16 @@ def c2(args, ref, ctx, sort_dev, emit):
             os_ms, os_n = ctx.kernel_time(_lib.K_ONESWEEP)
             ctx.set_timing(False)
             ok = bool(torch.equal(out.to(torch.int64) & 0xFFFFFFFF, torch.sort(t.to(torch.int64) & 0xFFFFFFFF).values))
-            passes = os_n / 7  # 7 timed sorts incl. warm-up
+            sorts = os_n / 4  # every sort launches the four 8-bit passes (identity ones exit at once)
+            # identity passes (one digit value over all keys) are skipped: the
+            # roofline is taken over the executed passes only
+            skipped = [p for p in range(4) if int(((keys >> (8 * p)) & 255).min()) == int(((keys >> (8 * p)) & 255).max())]
+            passes = 4 - len(skipped)
             row = {"row": f"{'C2' if name == 'uniform' else 'C3'} {name} r=2^{bits}", "n": n, "gpu_ms": ms,
-                   "gpu_keys_per_s": n / ms * 1e3, "executed_passes_per_sort": passes, "verified": ok}
-            if os_n:
-                per = os_ms / os_n
+                   "gpu_keys_per_s": n / ms * 1e3, "executed_passes_per_sort": passes,
+                   "skipped_identity_passes": skipped, "verified": ok}
+            if os_n and passes:
+                per = os_ms / (sorts * passes)
                 row.update({"onesweep_ms_per_pass": per, "pass_GBps": 8 * n / per / 1e6,
                             "pass_frac_of_measured_hbm": 8 * n / per / 1e6 / PEAK})
             if ref is not None:
