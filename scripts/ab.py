@@ -36,7 +36,11 @@ for rnd in range(int(os.environ.get("AB_ROUNDS", "3"))):
         env = dict(os.environ, REPO=repo, BSG_LIB=os.path.abspath(lib))
         if cfg:
             env["BSG_OS_CFG"] = cfg
-        p = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+        try:
+            p = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True,
+                               timeout=float(os.environ.get("AB_TIMEOUT", "120")))
+        except subprocess.TimeoutExpired:
+            print(rnd, spec, "TIMEOUT", flush=True); continue
         line = [l for l in p.stdout.splitlines() if l.startswith("RESULT")]
         if not line:
             print(spec, "FAILED", p.stderr[-2000:]); continue

@@ -1,1 +1,1 @@
-AB_ROUNDS=2 timeout 1000 python scripts/ab.py paper_1708_09495_b200/libbsg.so:6 paper_1708_09495_b200/libbsg.so:4 paper_1708_09495_b200/libbsg.so:2 paper_1708_09495_b200/libbsg.so:5 build/var/lw8/libbsg.so:4 build/var/lw4/libbsg.so:4 build/var/lw8/libbsg.so:2 | grep SUMMARY
+AB_ROUNDS=3 timeout 1000 python scripts/ab.py paper_1708_09495_b200/libbsg.so build/var/m4/libbsg.so:7 build/var/m3/libbsg.so:7 build/var/m4w8/libbsg.so:7 build/var/m4w2/libbsg.so:7 | grep SUMMARY
