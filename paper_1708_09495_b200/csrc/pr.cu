@@ -469,6 +469,22 @@ int launch_pr_seg_count(const uint32_t* keys, uint64_t n, int p, int bits, int s
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// Segment-local digit bases of an 8-bit sub-pass: base[w][d] = offset_of(w) +
+// sum_{d'<d} cnt(w, d'), so a segmented one-sweep pass sorts every worker's
+// block in place (the two byte sub-passes of an r = 2^16 local pass).
+__global__ void __launch_bounds__(256)
+    pr_local_base_kernel(const uint64_t* __restrict__ counts, uint64_t n, int p, int64_t* __restrict__ base) {
+    __shared__ uint64_t s_w[8];
+    const int w = blockIdx.x, d = threadIdx.x, lane = d & 31, wp = d >> 5;
+    const uint64_t c = counts[static_cast<uint64_t>(w) * 256 + d];
+    const uint64_t incl = warp_inclusive_scan(c);
+    if (lane == 31) s_w[wp] = incl;
+    __syncthreads();
+    uint64_t excl = incl - c;
+    for (int j = 0; j < wp; ++j) excl += s_w[j];
+    base[static_cast<uint64_t>(w) * 256 + d] = static_cast<int64_t>(part_offset(n, p, w) + excl);
+}
+
 // In-process fused round: base[v][d] = digit_start[d] + sum_{u<v} cnt(u,d),
 // in place over the column-prefix table.
 __global__ void pr_add_dstart_kernel(int64_t* __restrict__ before, const uint64_t* __restrict__ dstart, int p,
@@ -652,12 +668,17 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         std::swap(cur, nxt);
     }
     if (fused) A = cur;
+    // r = 2^16: the workers' local passes as segmented byte sub-passes
+    const bool seg16 = !fused && bits == 16 && max_len <= kChunkKeys;
+    if (seg16 && (e = ctx->status.ensure(onesweep_seg_status_words(n, p) * sizeof(uint32_t))) != cudaSuccess)
+        return cuda_fail(e, "pr workspace");
     for (int round = 0; round < rounds && n && !fused; ++round) {
         const int shift = round * bits;
         // local stable pass of every worker (sort_and_scatter's count_sort_round)
         for (int w = 0; w < p; ++w) {
             const uint64_t off = bsg_partition_offset_of(n, p, w), sz = bsg_partition_size_of(n, p, w);
             if (sz == 0) continue;
+            if (seg16) break; // all workers' local passes at once below
             if (bits <= 8) {
                 if (!add(launch_count_pass(A + off, S + off, sz, bits, shift, ws, stream, true)))
                     return cuda_fail(cudaGetLastError(), "pr local pass");
@@ -667,6 +688,28 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
                     !add(launch_count_pass(mid, S + off, sz, 8, shift + 8, ws, stream, true)))
                     return cuda_fail(cudaGetLastError(), "pr local pass");
             }
+        }
+        if (seg16) {
+            // r = 2^16 local pass of every worker as two segmented one-sweep
+            // byte sub-passes (each block sorted in place, stably: low byte,
+            // then high byte); a block holds the same keys before and after
+            // the first sub-pass, so both byte histograms come from A
+            uint64_t* cA = starts;
+            uint64_t* cB = starts + static_cast<uint64_t>(p) * 256;
+            int64_t* bA = gd;
+            int64_t* bB = gd + static_cast<uint64_t>(p) * 256;
+            uint32_t* mid = ctx->stage_b.as<uint32_t>();
+            if (!add(launch_pr_seg_count(A, n, p, 8, shift, cA, stream)) ||
+                !add(launch_pr_seg_count(A, n, p, 8, shift + 8, cB, stream)))
+                return cuda_fail(cudaGetLastError(), "pr local count");
+            pr_local_base_kernel<<<p, 256, 0, stream>>>(cA, n, p, bA);
+            pr_local_base_kernel<<<p, 256, 0, stream>>>(cB, n, p, bB);
+            launches += 2;
+            if (!add(launch_onesweep_seg(A, mid, n, p, 8, shift, reinterpret_cast<const uint64_t*>(bA),
+                                         ctx->status.as<uint32_t>(), stream)) ||
+                !add(launch_onesweep_seg(mid, S, n, p, 8, shift + 8, reinterpret_cast<const uint64_t*>(bB),
+                                         ctx->status.as<uint32_t>(), stream)))
+                return cuda_fail(cudaGetLastError(), "pr local pass");
         }
         {
             TimedScope ts(3 /*BSG_K_PR*/, stream);
