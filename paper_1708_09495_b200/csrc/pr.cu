@@ -625,7 +625,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     // r <= 2^8: each worker's whole round is ONE one-sweep pass whose digit
     // bases are the global positions of its block's first key per digit
     // (the same fused round as bsg_pr_fused_round, all blocks local)
-    const bool fused = bits <= 8 && max_len <= kChunkKeys;
+    const bool fused = bits == 8 || (bits < 8 && max_len <= kChunkKeys); // 8-bit: 64-bit rows above 2^29
     if (fused && (e = ctx->status.ensure(onesweep_seg_status_words(n, p) * sizeof(uint32_t))) != cudaSuccess)
         return cuda_fail(e, "pr workspace");
     uint32_t* cur = A;
@@ -669,7 +669,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     }
     if (fused) A = cur;
     // r = 2^16: the workers' local passes as segmented byte sub-passes
-    const bool seg16 = !fused && bits == 16 && max_len <= kChunkKeys;
+    const bool seg16 = !fused && bits == 16;
     if (seg16 && (e = ctx->status.ensure(onesweep_seg_status_words(n, p) * sizeof(uint32_t))) != cudaSuccess)
         return cuda_fail(e, "pr workspace");
     for (int round = 0; round < rounds && n && !fused; ++round) {

@@ -1113,23 +1113,25 @@ int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shif
 // ---------------------------------------------------------------------------
 // Segmented pass: all worker blocks of an in-process PR round in one launch.
 // ---------------------------------------------------------------------------
-template <int BITS, int THREADS, int ITEMS>
+// WIDE: 64-bit status words and positions (segments above 2^29 keys or
+// arrays above 2^32 keys, e.g. BASELINE config 5's n = 2^33 with p <= 8).
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_seg_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, const SegDesc sd, int shift,
                         const uint64_t* __restrict__ base_table, uint32_t* __restrict__ status,
                         uint32_t* __restrict__ tile_counter, int32_t neg1) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, false, 0, PlainSink, default_lb_window<THREADS>(), true>(
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PlainSink, default_lb_window<THREADS>(), true>(
         smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
 }
 
-template <int BITS, int THREADS, int ITEMS>
+template <int BITS, int THREADS, int ITEMS, bool WIDE = false>
 int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int shift,
                             const uint64_t* base_table, uint32_t* status, cudaStream_t stream) {
-    using L = OnesweepSmem<BITS, THREADS, ITEMS, false>;
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
-    auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS>;
+    auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS, WIDE>;
     static int per_sm = 0;
     if (per_sm == 0) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
@@ -1149,7 +1151,8 @@ int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int 
                            static_cast<uint64_t>(sd.p - sd.nbig) * sd.tiles_small;
     if (tiles == 0) return 0;
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * per_sm));
-    if (cudaMemsetAsync(status, 0, (32 + tiles * RADIX) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    if (cudaMemsetAsync(status, 0, (32 + tiles * RADIX * (WIDE ? 2 : 1)) * sizeof(uint32_t), stream) != cudaSuccess)
+        return -1;
     TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
     kern<<<grid, THREADS, L::bytes, stream>>>(src, dst, sd, shift, base_table, status + 32, status, -1);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
@@ -1158,7 +1161,11 @@ int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int 
 int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
                         const uint64_t* base_table, uint32_t* status, cudaStream_t stream) {
     if (n == 0) return 0;
-    if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys) return -1;
+    if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys || n > 0xFFFFFFFFull) {
+        // 64-bit status words and positions
+        if (bits != 8) return -1;
+        return launch_onesweep_seg_cfg<8, 512, 24, true>(src, dst, n, p, shift, base_table, status, stream);
+    }
     switch (bits) {
     case 1: return launch_onesweep_seg_cfg<1, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
     case 2: return launch_onesweep_seg_cfg<2, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
@@ -1173,7 +1180,8 @@ int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, i
 
 uint64_t onesweep_seg_status_words(uint64_t n, int p) {
     // 8192-key tiles at the smallest: one extra partial tile per segment
-    return 32 + (n / 8192 + static_cast<uint64_t>(p) + 1) * 256;
+    // (64-bit words for the large segments of the WIDE rows)
+    return 32 + (n / 8192 + static_cast<uint64_t>(p) + 1) * 256 * 2;
 }
 
 uint64_t onesweep_status_words(uint64_t n) {

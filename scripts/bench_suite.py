@@ -53,7 +53,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--only", default="C1,C2,C4,PR", help="comma-separated sections: C1,C2,C4,PR")
+    ap.add_argument("--only", default="C1,C2,C4,PR,C5", help="comma-separated sections: C1,C2,C4,PR,C5")
     args = ap.parse_args()
     only = set(args.only.split(","))
     ref = maybe_reference()
@@ -77,6 +77,8 @@ def main():
         c4(args, ref, ctx, L, st, emit)
     if "PR" in only:
         pr_rows(args, ref, L, ctx, st, emit)
+    if "C5" in only and not args.quick:
+        c5_rows(args, ref, L, ctx, st, emit)
     if args.out:
         with open(args.out, "w") as f:
             json.dump({"host_threads": os.cpu_count(), "gpu": torch.cuda.get_device_name(0), "rows": rows,
@@ -192,6 +194,41 @@ def pr_rows(args, ref, L, ctx, st, emit):
                 tc, _ = ref.time_parallel_radix(keys, p, 1 << radix_log2)
                 row.update({"cpu_ref_ms": tc * 1e3, "cpu_threads": p, "speedup": tc * 1e3 / ms})
             emit(row)
+
+
+def c5_rows(args, ref, L, ctx, st, emit):
+    # ---- C5 at its full size on one GPU: p logical workers ---------------
+    # n = 2^33 keys of generate_uniform_keys(n, derive_seed(1, 0)), generated
+    # on the device (bit-identical stream); verified by sortedness + multiset
+    # checksums (tests/test_pr_gpu.py::test_c5_full_size_in_process)
+    n = 1 << 33
+    free, _ = torch.cuda.mem_get_info()
+    if free < 17 * n:
+        emit({"row": "C5 2^33 in-process", "skipped": f"needs ~{17 * n >> 30} GiB free, have {free >> 30}"})
+        return
+    t = bsg.generate_uniform_keys_device(n, bsg.derive_seed(1, 0)).view(torch.int32)
+    out = torch.empty_like(t)
+    for p in (2, 4, 8):
+        def runp():
+            _lib.check(L.bsg_parallel_radix_sort_u32(ctx.handle, t.data_ptr(), out.data_ptr(), n, p, 8, -1, None, 1,
+                                                     st))
+        ms = gpu_time(runp, reps=3, warm=1)
+        step = 1 << 27
+        ok = True
+        prev = -1
+        s_in = s_out = 0
+        for a in range(0, n, step):
+            y = out[a:a + step].to(torch.int64) & 0xFFFFFFFF
+            x = t[a:a + step].to(torch.int64) & 0xFFFFFFFF
+            ok = ok and bool((y[1:] >= y[:-1]).all()) and int(y[0]) >= prev
+            prev = int(y[-1])
+            s_in += int(x.sum()); s_out += int(y.sum())
+        emit({"row": f"C5 PR4 p={p} logical workers, 1 GPU, n=2^33", "n": n, "gpu_ms": ms,
+              "gpu_keys_per_s": n / ms * 1e3, "verified": ok and s_in == s_out,
+              "note": "one GPU stands in for the data flow only (no NVLink): blocks of n/p keys, every round a "
+                      "local pass + routing to the owners' blocks"})
+    del t, out
+    torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":

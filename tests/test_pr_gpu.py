@@ -183,3 +183,74 @@ def test_peer_scatter_logical_workers(cuda, bsg, orc, p):
     assert L.bsg_pr_peer_scatter(ctx.handle, 0, 0, 0, n, 2, 2, 0, 8, arr, None) != 0
     assert L.bsg_pr_fused_round(ctx.handle, 0, 5, 0, n, 2, 0, 0, 8, arr, None) != 0
     assert L.bsg_pr_fused_round(ctx.handle, 0, 0, 0, n, 2, 0, 9, 8, arr, None) != 0
+
+
+@pytest.mark.parametrize("p", [8])
+def test_c5_full_size_in_process(cuda, bsg, p):
+    """BASELINE config 5 at its full size on one GPU: n = 2^33 keys of
+    generate_uniform_keys(n, derive_seed(1, 0)) (generated on the device,
+    bit-identical to the host stream), PR4 with p logical workers
+    (block-distributed n/p: each block 2^30 keys).  At this size the CPU oracle
+    is replaced by size-independent properties: globally sorted concatenation
+    and multiset checksums (sum, sum of squares mod a prime) equal to the
+    input's.  ~128 GiB of device buffers."""
+    torch = cuda
+    from test_radix_gpu import _chunked_properties
+
+    n = 1 << 33
+    free, _ = torch.cuda.mem_get_info()
+    if free < 17 * n:
+        pytest.skip("not enough device memory")
+    keys = bsg.generate_uniform_keys_device(n, bsg.derive_seed(1, 0)).view(torch.int32)
+    # the device stream is the host generator's stream: spot-check a window
+    # far into it against the host random-access generator
+    off = n - 4099
+    exp = bsg.generate_uniform_keys_at(4096, bsg.derive_seed(1, 0), off)
+    np.testing.assert_array_equal(keys[off:off + 4096].cpu().numpy().view(np.uint32), exp)
+    out = torch.empty_like(keys)
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.bsg_parallel_radix_sort_u32(ctx.handle, keys.data_ptr(), out.data_ptr(), n, p, 8, -1, None, 1, st) == 0, \
+        bsg._lib.last_error()
+    torch.cuda.synchronize()
+    _chunked_properties(torch, keys, out)
+    del keys, out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("radix_log2", [8, 16])
+def test_large_segments_wide_rows(cuda, bsg, radix_log2):
+    """Worker blocks above 2^29 keys (p = 2, n = 2^31 + 12345): the segmented
+    one-sweep runs its 64-bit status/position rows.  After one round the
+    concatenated blocks equal one count_sort_round of the whole array
+    (radix.hpp:371-414 with plan.rounds = 1), and the full run equals the
+    serial sort; both compared on the device chunk by chunk."""
+    torch = cuda
+    n, p = (1 << 31) + 12345, 2
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 * n:
+        pytest.skip("not enough device memory")
+    keys = bsg.generate_uniform_keys_device(n, 77).view(torch.int32)
+    keys[:5000] = 12345  # ties across the first tiles of block 0
+    got = torch.empty_like(keys)
+    exp = torch.empty_like(keys)
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    step = 1 << 27
+
+    def same():
+        torch.cuda.synchronize()
+        return all(bool(torch.equal(got[a:a + step], exp[a:a + step])) for a in range(0, n, step))
+
+    assert L.bsg_parallel_radix_sort_u32(ctx.handle, keys.data_ptr(), got.data_ptr(), n, p, radix_log2, 1, None, 1,
+                                         st) == 0, bsg._lib.last_error()
+    assert L.bsg_count_sort_round_u32(ctx.handle, keys.data_ptr(), exp.data_ptr(), n, 0, radix_log2, 1, st) == 0
+    assert same()
+    assert L.bsg_parallel_radix_sort_u32(ctx.handle, keys.data_ptr(), got.data_ptr(), n, p, radix_log2, -1, None, 1,
+                                         st) == 0, bsg._lib.last_error()
+    assert L.bsg_radix_sort_u32(ctx.handle, keys.data_ptr(), exp.data_ptr(), n, radix_log2, 1, st) == 0
+    assert same()
+    del keys, got, exp
+    torch.cuda.empty_cache()
