@@ -876,7 +876,8 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     if (p < 1 || p > kPeerMax || me < 0 || me >= p) return fail(BSG_EINVAL, "fused round: worker index out of range");
     if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
     if (len != bsg_partition_size_of(n, p, me)) return fail(BSG_EINVAL, "fused round: block size != size_of(me)");
-    if (len > kChunkKeys) return fail(BSG_EINVAL, "fused round: block larger than 2^29 keys");
+    if (len > kChunkKeys && radix_log2 < 8)
+        return fail(BSG_EINVAL, "fused round: blocks above 2^29 keys need r >= 2^8");
     if (!peer_blocks || !counts_all || (len && !block)) return fail(BSG_EINVAL, "null pointer");
     if (radix_log2 == 16) {
         cudaError_t e;

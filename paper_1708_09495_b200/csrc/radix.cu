@@ -1053,24 +1053,24 @@ int launch_small_sort(const uint32_t* in, uint32_t* out, uint64_t n, const Radix
 // ---------------------------------------------------------------------------
 // PR round fused with its exchange (launch_onesweep_peer, see radix.cuh).
 // ---------------------------------------------------------------------------
-template <int BITS, int THREADS, int ITEMS>
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
-    onesweep_peer_kernel(const uint32_t* __restrict__ src, uint32_t len, int shift,
+    onesweep_peer_kernel(const uint32_t* __restrict__ src, uint64_t len, int shift,
                          const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                          uint32_t* __restrict__ tile_counter, int use_tma, int32_t neg1,
                          const __grid_constant__ PeerTable tab, int p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, false, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
                                                               status, tile_counter, use_tma, 0, neg1, true, parity);
     __threadfence_system(); // peer stores performed before the round's barrier
 }
 
-template <int BITS, int THREADS, int ITEMS>
-int launch_onesweep_peer_cfg(const uint32_t* block, uint32_t len, int shift, const uint64_t* digit_base,
+template <int BITS, int THREADS, int ITEMS, bool WIDE = false>
+int launch_onesweep_peer_cfg(const uint32_t* block, uint64_t len, int shift, const uint64_t* digit_base,
                              uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream) {
-    using L = OnesweepSmem<BITS, THREADS, ITEMS, false>;
-    auto kern = onesweep_peer_kernel<BITS, THREADS, ITEMS>;
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
+    auto kern = onesweep_peer_kernel<BITS, THREADS, ITEMS, WIDE>;
     static int per_sm = 0;
     if (per_sm == 0) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
@@ -1081,10 +1081,10 @@ int launch_onesweep_peer_cfg(const uint32_t* block, uint32_t len, int shift, con
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     constexpr int RADIX = 1 << BITS;
-    const uint32_t tiles = (len + L::TILE - 1) / L::TILE;
+    const uint32_t tiles = static_cast<uint32_t>((len + L::TILE - 1) / L::TILE);
     const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
-    if (cudaMemsetAsync(status, 0, (32 + static_cast<uint64_t>(tiles) * RADIX) * sizeof(uint32_t), stream) !=
-        cudaSuccess)
+    if (cudaMemsetAsync(status, 0, (32 + static_cast<uint64_t>(tiles) * RADIX * (WIDE ? 2 : 1)) * sizeof(uint32_t),
+                        stream) != cudaSuccess)
         return -1;
     const bool tma = true; // per-tile aligned bodies (head/tail keys via plain loads)
     TimedScope ts(3 /*BSG_K_PR*/, stream);
@@ -1096,7 +1096,10 @@ int launch_onesweep_peer_cfg(const uint32_t* block, uint32_t len, int shift, con
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
                          uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream) {
     if (len == 0) return 0;
-    if (len > kChunkKeys) return -1;
+    if (len > kChunkKeys) // 64-bit status words and positions (config 5: 2^30-2^32 keys per GPU)
+        return bits == 8 ? launch_onesweep_peer_cfg<8, 512, 24, true>(block, len, shift, digit_base, status, tab, p,
+                                                                        stream)
+                         : -1;
     const uint32_t n = static_cast<uint32_t>(len);
     switch (bits) {
     case 1: return launch_onesweep_peer_cfg<1, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);

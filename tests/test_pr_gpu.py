@@ -254,3 +254,40 @@ def test_large_segments_wide_rows(cuda, bsg, radix_log2):
     assert same()
     del keys, got, exp
     torch.cuda.empty_cache()
+
+
+def test_fused_round_large_blocks(cuda, bsg):
+    """bsg_pr_fused_round with blocks above 2^29 keys (config 5 puts 2^30-2^32
+    keys on each GPU): the 64-bit one-sweep rows store into the owners'
+    blocks.  Two logical workers in one process; one round on the input
+    equals one count_sort_round of the whole array (a PR round is a stable
+    count sort of the block concatenation, radix.hpp:371-414)."""
+    torch = cuda
+    from paper_1708_09495_b200 import distributed as D
+
+    n, p = (1 << 30) + 4101, 2
+    free, _ = torch.cuda.mem_get_info()
+    if free < 24 * n:
+        pytest.skip("not enough device memory")
+    ops = D.CudaStepOps(torch.device("cuda", 0))
+    keys = bsg.generate_uniform_keys_device(n, 99).view(torch.int32)
+    sizes = [D.partition_size_of(n, p, w) for w in range(p)]
+    offs = [D.partition_offset_of(n, p, w) for w in range(p)]
+    blocks = [keys[offs[w]:offs[w] + sizes[w]] for w in range(p)]
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    exp = torch.empty_like(keys)
+    for bits, rnd in ((8, 1), (16, 1)):
+        counts_all = torch.cat([ops.count(b, rnd, bits) for b in blocks])
+        nxt = [torch.empty(sz, dtype=torch.int32, device="cuda") for sz in sizes]
+        ptrs = [t.data_ptr() for t in nxt]
+        for me in range(p):
+            ops.fused_round(blocks[me], counts_all, n, p, me, rnd, bits, ptrs)
+        assert L.bsg_count_sort_round_u32(ctx.handle, keys.data_ptr(), exp.data_ptr(), n, rnd, bits, 1, st) == 0
+        torch.cuda.synchronize()
+        for w in range(p):
+            assert bool(torch.equal(nxt[w], exp[offs[w]:offs[w] + sizes[w]])), (bits, w)
+        del nxt
+    del keys, exp, blocks
+    torch.cuda.empty_cache()
