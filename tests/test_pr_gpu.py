@@ -291,3 +291,45 @@ def test_fused_round_large_blocks(cuda, bsg):
         del nxt
     del keys, exp, blocks
     torch.cuda.empty_cache()
+
+
+def test_distributed_world1_large_block(cuda, bsg):
+    """The multi-GPU orchestration (distributed.py) at a config-5 block size:
+    one rank holding 2^30 + 7 keys (every per-rank kernel past 2^29 keys runs
+    its 64-bit rows).  Variants A (NCCL all-to-all-v, r = 2^8 and 2^16), B
+    (single exchange) and P (peer-store rounds) all equal the serial sort."""
+    torch = cuda
+    import os
+    import torch.distributed as dist
+    from paper_1708_09495_b200 import distributed as D
+
+    n = (1 << 30) + 7
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 * n:
+        pytest.skip("not enough device memory")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29533"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        keys = bsg.generate_uniform_keys_device(n, 5).view(torch.int32)
+        exp = torch.empty_like(keys)
+        ctx = bsg._lib.context(0)
+        L = bsg._lib.lib()
+        st = torch.cuda.current_stream().cuda_stream
+        assert L.bsg_radix_sort_u32(ctx.handle, keys.data_ptr(), exp.data_ptr(), n, 8, 1, st) == 0
+        step = 1 << 27
+
+        def check(out):
+            torch.cuda.synchronize()
+            assert out.numel() == n
+            assert all(bool(torch.equal(out[a:a + step], exp[a:a + step])) for a in range(0, n, step))
+
+        for radix in (256, 65536):
+            check(D.parallel_radix_sort(keys.clone(), n, radix=radix))
+        check(D.parallel_radix_sort_single_exchange(keys.clone()))
+        peer = D.PeerBlocks(n)
+        check(D.parallel_radix_sort(keys.clone(), n, radix=256, exchange="peer", peer=peer))
+        del peer, keys, exp
+        torch.cuda.empty_cache()
+    finally:
+        dist.destroy_process_group()
