@@ -235,6 +235,8 @@ int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_t len,
  * count_sort_round + all-to-all-v + gather_slices fused.  counts_all is the
  * gathered p x r count matrix of this round (bsg_pr_count_digits on every
  * worker).  For r = 2^16 the call runs bsg_pr_local_sort + the peer scatter.
+ * Any block size at r >= 2^8 (blocks above 2^29 keys run 64-bit status words
+ * and positions); r < 2^8 needs len <= 2^29 (BSG_EINVAL otherwise).
  * Same ordering contract as bsg_pr_peer_scatter. */
 int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t len,
                        const uint64_t* counts_all, uint64_t n, int p, int me,
