@@ -517,6 +517,20 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                     keys[i] = idx < valid ? (rel < body ? buf[rel] : __ldg(src + tile_start + idx)) : 0u;
                 }
             }
+            if constexpr (RANK == 3) {
+                // count only: per-warp digit histogram by shared-memory
+                // reductions (16-bit halves of a word; counts < 2^16)
+                uint32_t* wc32w = reinterpret_cast<uint32_t*>(wc);
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const uint32_t idx = wbase + i * 32 + lane;
+                    if (FULL || idx < valid) {
+                        const uint32_t d = digit_of_key<BITS>(keys[i], shift);
+                        atomicAdd(wc32w + (d >> 1), 1u << ((d & 1u) * 16u));
+                    }
+                }
+                return;
+            }
             // multisplit masks in batches of PB items (independent inside a
             // batch), then the per-warp running counts of the batch, item by
             // item (input order): every peer reads the same counter (a
@@ -614,7 +628,43 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         phase(3);
 
         // ---- stage the tile in digit order (in place: keys are in registers)
-        if (dbg & 16) {
+        if constexpr (RANK == 3) {
+            // rank against the warp's final digit offsets (the counter rows
+            // now hold tile offset + warp prefix) and scatter at once
+            auto rank_stage = [&](auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                constexpr int PB = ITEMS % 4 == 0 ? 4 : ITEMS;
+#pragma unroll
+                for (int i0 = 0; i0 < ITEMS; i0 += PB) {
+                    uint32_t peers[PB], dgt[PB];
+#pragma unroll
+                    for (int ii = 0; ii < PB; ++ii) {
+                        const int i = i0 + ii;
+                        const uint32_t idx = wbase + i * 32 + lane;
+                        const bool ok = FULL || idx < valid;
+                        const uint32_t d = ok ? (BITS == 8 ? digit8_fma(keys[i], dmul) : digit_of_key<BITS>(keys[i], shift))
+                                              : static_cast<uint32_t>(RADIX);
+                        dgt[ii] = d;
+                        peers[ii] = peers_ballot<FULL ? BITS : BITS + 1>(d, neg1);
+                    }
+#pragma unroll
+                    for (int ii = 0; ii < PB; ++ii) {
+                        const int i = i0 + ii;
+                        const uint32_t idx = wbase + i * 32 + lane;
+                        const bool ok = FULL || idx < valid;
+                        const uint32_t d = ok ? dgt[ii] : 0u;
+                        const uint32_t before = ok ? wc[d] : 0u;
+                        const bool leader = (peers[ii] & gt) == 0u;
+                        const uint32_t r = before + __popc(peers[ii] & lt);
+                        if (leader && ok) wc[d] = static_cast<uint16_t>(r + 1);
+                        __syncwarp();
+                        if (ok) buf[r] = keys[i];
+                    }
+                }
+            };
+            if (full) rank_stage(std::true_type{});
+            else rank_stage(std::false_type{});
+        } else if (dbg & 16) {
             // timing experiment only: skip staging
         } else if (full) { // every item valid: no per-item guards
 #pragma unroll
@@ -802,17 +852,23 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
 template <int BITS, int THREADS, int ITEMS, bool WIDE>
 int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
-    // RANK 0 = ballot multisplit (default), 1 = match-any (~40 SM-cycles per warp-item on B200)
+    // RANK 3 = per-warp count by shared-memory reductions, then ballot-multisplit
+    // ranks against the final offsets with the scatter (default, BSG_OS_RANK=0);
+    // 0 = rank first, stage after the scan (BSG_OS_RANK=2, +3.4% per sort);
+    // 1 = match-any ranks (~40 SM-cycles per warp-item on B200)
     if constexpr (BITS == 8) {
         switch (onesweep_rank_mode()) {
         case 1:
             return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 1>(plan, pass, n, shift, base_for_pass,
                                                                         passes_stride, status, stream, use_tma);
+        case 2:
+            return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 0>(plan, pass, n, shift, base_for_pass,
+                                                                        passes_stride, status, stream, use_tma);
         default:
             break;
         }
     }
-    return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 0>(plan, pass, n, shift, base_for_pass, passes_stride,
+    return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 3>(plan, pass, n, shift, base_for_pass, passes_stride,
                                                                 status, stream, use_tma);
 }
 
@@ -984,7 +1040,7 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
         if (!s_active[p]) continue;
         uint32_t* region = regions + static_cast<uint64_t>(p) * region_words;
         // all tiles are in flight at once here: the wide window
-        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0, PlainSink, BSG_LB_WIN>(
+        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 3, PlainSink, BSG_LB_WIN>(
             smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p,
                                                                s_base + p * 256, region + 32, region, use_tma, 0,
                                                                neg1, first, parity);
@@ -1061,7 +1117,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                          const __grid_constant__ PeerTable tab, int p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
                                                               status, tile_counter, use_tma, 0, neg1, true, parity);
     __threadfence_system(); // peer stores performed before the round's barrier
 }
@@ -1125,7 +1181,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                         uint32_t* __restrict__ tile_counter, int32_t neg1) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PlainSink, default_lb_window<THREADS>(), true>(
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PlainSink, default_lb_window<THREADS>(), true>(
         smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
 }
 
