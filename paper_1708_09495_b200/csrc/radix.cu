@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kScanThreads)
                      const uint32_t* in, uint32_t* out, uint32_t* tmp, int allow_skip) {
     __shared__ uint64_t s_warp[kScanThreads / 32];
     __shared__ int s_active[kMaxPasses];
+    __shared__ int s_skew[kMaxPasses];
     const int d = threadIdx.x;
     const int lane = d & 31, warp = d >> 5;
     for (int p = 0; p < passes; ++p) {
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(kScanThreads)
         if (d < radix)
             for (int c = 0; c < chunks; ++c) total += hist[(static_cast<uint64_t>(c) * passes + p) * radix + d];
         const int ident = __syncthreads_or(d < radix && total == n);
+        const int skew = __syncthreads_or(d < radix && total * 16 > n);
         const uint64_t incl = warp_inclusive_scan(total);
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
@@ -177,7 +179,10 @@ __global__ void __launch_bounds__(kScanThreads)
                 run += hist[idx];
             }
         }
-        if (d == 0) s_active[p] = (n > 0) && !(allow_skip && ident);
+        if (d == 0) {
+            s_active[p] = (n > 0) && !(allow_skip && ident);
+            s_skew[p] = skew;
+        }
     }
     __syncthreads();
     if (d != 0) return;
@@ -188,6 +193,7 @@ __global__ void __launch_bounds__(kScanThreads)
         pl.src[p] = nullptr;
         pl.dst[p] = nullptr;
         pl.active[p] = p < passes ? s_active[p] : 0;
+        pl.skew[p] = p < passes ? s_skew[p] : 0;
     }
     pl.executed = m;
     if (m == 0) {
@@ -786,6 +792,17 @@ __global__ void __launch_bounds__(THREADS, (onesweep_min_blocks<THREADS, ITEMS>(
     extern __shared__ __align__(128) uint8_t smem[];
     if (!plan->active[pass]) return;
     uint32_t parity = 0;
+    if constexpr (RANK == 3) {
+        // skewed digit distribution (a digit holds > n/16 keys): the counting
+        // reductions would serialise on that digit's counter; rank first
+        // (warp-aggregated by the ballot multisplit) instead
+        if (plan->skew[pass]) {
+            onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0>(smem, plan->src[pass] + chunk_off,
+                                                          PlainSink{plan->dst[pass]}, chunk_n, shift, digit_base,
+                                                          status, tile_counter, use_tma, dbg, neg1, true, parity);
+            return;
+        }
+    }
     onesweep_tiles<BITS, THREADS, ITEMS, WIDE, RANK>(smem, plan->src[pass] + chunk_off, PlainSink{plan->dst[pass]}, chunk_n,
                                                      shift, digit_base, status, tile_counter, use_tma, dbg, neg1,
                                                      true, parity);
@@ -1040,7 +1057,7 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
         if (!s_active[p]) continue;
         uint32_t* region = regions + static_cast<uint64_t>(p) * region_words;
         // all tiles are in flight at once here: the wide window
-        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 3, PlainSink, BSG_LB_WIN>(
+        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0, PlainSink, BSG_LB_WIN>(
             smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p,
                                                                s_base + p * 256, region + 32, region, use_tma, 0,
                                                                neg1, first, parity);
@@ -1117,7 +1134,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                          const __grid_constant__ PeerTable tab, int p) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
                                                               status, tile_counter, use_tma, 0, neg1, true, parity);
     __threadfence_system(); // peer stores performed before the round's barrier
 }
@@ -1181,7 +1198,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
                         uint32_t* __restrict__ tile_counter, int32_t neg1) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PlainSink, default_lb_window<THREADS>(), true>(
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PlainSink, default_lb_window<THREADS>(), true>(
         smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
 }
 

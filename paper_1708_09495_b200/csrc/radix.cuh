@@ -14,6 +14,7 @@ struct PassPlan {
     const uint32_t* src[kMaxPasses];
     uint32_t* dst[kMaxPasses];
     int32_t active[kMaxPasses];
+    int32_t skew[kMaxPasses];  // a digit holds > n/16 keys: contention-free ranking path
     int32_t executed;          // number of active passes
     int32_t need_copy;         // result is not in `out` yet
     const uint32_t* final_buf; // buffer holding the result after the last pass
