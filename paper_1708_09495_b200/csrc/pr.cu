@@ -284,15 +284,21 @@ __global__ void __launch_bounds__(kSendThreads)
 //   adj:  pr_plan2_kernel rebases delta onto me's receive buffer.
 __global__ void __launch_bounds__(kDigChunk)
     pr_plan_col_kernel(const uint64_t* __restrict__ counts, int p, int radix, int64_t* __restrict__ delta,
-                       uint64_t* __restrict__ coltot, uint64_t* __restrict__ colchunk) {
+                       uint64_t* __restrict__ coltot, uint64_t* __restrict__ colchunk,
+                       uint32_t* __restrict__ skew = nullptr, uint64_t n = 0) {
     const int d = blockIdx.x * kDigChunk + threadIdx.x;
     uint64_t before = 0;
     if (d < radix) {
+        bool heavy = false;
         for (int v = 0; v < p; ++v) {
             delta[static_cast<uint64_t>(v) * radix + d] = static_cast<int64_t>(before);
-            before += counts[static_cast<uint64_t>(v) * radix + d];
+            const uint64_t c = counts[static_cast<uint64_t>(v) * radix + d];
+            before += c;
+            heavy = heavy || c * 16 > part_size(n, p, v);
         }
         coltot[d] = before;
+        // a digit holding > 1/16 of some block: that round's pass ranks first
+        if (skew && heavy) atomicOr(skew, 1u);
     }
     uint64_t ex;
     const uint64_t tot = chunk_excl_scan(before, ex);
@@ -473,10 +479,12 @@ int launch_pr_seg_count(const uint32_t* keys, uint64_t n, int p, int bits, int s
 // sum_{d'<d} cnt(w, d'), so a segmented one-sweep pass sorts every worker's
 // block in place (the two byte sub-passes of an r = 2^16 local pass).
 __global__ void __launch_bounds__(256)
-    pr_local_base_kernel(const uint64_t* __restrict__ counts, uint64_t n, int p, int64_t* __restrict__ base) {
+    pr_local_base_kernel(const uint64_t* __restrict__ counts, uint64_t n, int p, int64_t* __restrict__ base,
+                         uint32_t* __restrict__ skew) {
     __shared__ uint64_t s_w[8];
     const int w = blockIdx.x, d = threadIdx.x, lane = d & 31, wp = d >> 5;
     const uint64_t c = counts[static_cast<uint64_t>(w) * 256 + d];
+    if (c * 16 > part_size(n, p, w)) atomicOr(skew, 1u); // heavy byte: that sub-pass ranks first
     const uint64_t incl = warp_inclusive_scan(c);
     if (lane == 31) s_w[wp] = incl;
     __syncthreads();
@@ -596,7 +604,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     if ((e = ctx->pr_counts.ensure(static_cast<uint64_t>(p) * (radix + 1) * 8)) != cudaSuccess)
         return cuda_fail(e, "pr workspace");
     if ((e = ctx->pr_delta.ensure(static_cast<uint64_t>(p) * radix * 8)) != cudaSuccess) return cuda_fail(e, "pr workspace");
-    if ((e = ctx->pr_misc.ensure(pp * 8 + static_cast<uint64_t>(radix) * 16 + 64 * 8)) != cudaSuccess)
+    if ((e = ctx->pr_misc.ensure(pp * 8 + static_cast<uint64_t>(radix) * 16 + 128 * 8)) != cudaSuccess)
         return cuda_fail(e, "pr workspace");
     if (bits == 16 && (e = ctx->stage_b.ensure(std::max<uint64_t>(n, 4) * 4)) != cudaSuccess) return cuda_fail(e, "pr workspace");
     RadixWorkspace ws;
@@ -610,6 +618,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     uint64_t* coltot = send + pp;                      // [radix]
     uint64_t* dstart = coltot + radix;                 // [radix]
     uint64_t* colchunk = dstart + radix;               // [radix / kDigChunk]
+    uint32_t* skew = reinterpret_cast<uint32_t*>(colchunk + 64); // round's skew flag
 
     if (n && (e = cudaMemcpyAsync(A, in, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
         return cuda_fail(e, "pr copy in");
@@ -640,7 +649,9 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         {
             TimedScope ts(3 /*BSG_K_PR*/, stream);
             const int chunks = (radix + kDigChunk - 1) / kDigChunk;
-            pr_plan_col_kernel<<<chunks, kDigChunk, 0, stream>>>(counts, p, radix, base, coltot, colchunk);
+            if ((e = cudaMemsetAsync(skew, 0, sizeof(uint32_t), stream)) != cudaSuccess)
+                return cuda_fail(e, "pr plan");
+            pr_plan_col_kernel<<<chunks, kDigChunk, 0, stream>>>(counts, p, radix, base, coltot, colchunk, skew, n);
             pr_digit_start_kernel<<<chunks, kDigChunk, 0, stream>>>(coltot, colchunk, radix, dstart);
             const uint64_t pr = static_cast<uint64_t>(p) * radix;
             pr_add_dstart_kernel<<<static_cast<unsigned>((pr + 255) / 256), 256, 0, stream>>>(base, dstart, p, radix);
@@ -649,7 +660,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         // every worker's local stable pass, stored at the global positions
         // (sort_and_scatter + exchange + gather_slices), one segmented launch
         if (!add(launch_onesweep_seg(cur, nxt, n, p, bits, shift, reinterpret_cast<const uint64_t*>(base),
-                                     ctx->status.as<uint32_t>(), stream)))
+                                     ctx->status.as<uint32_t>(), stream, skew)))
             return cuda_fail(cudaGetLastError(), "pr fused pass");
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
         if (stats) {
@@ -702,13 +713,15 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             if (!add(launch_pr_seg_count(A, n, p, 8, shift, cA, stream)) ||
                 !add(launch_pr_seg_count(A, n, p, 8, shift + 8, cB, stream)))
                 return cuda_fail(cudaGetLastError(), "pr local count");
-            pr_local_base_kernel<<<p, 256, 0, stream>>>(cA, n, p, bA);
-            pr_local_base_kernel<<<p, 256, 0, stream>>>(cB, n, p, bB);
+            if ((e = cudaMemsetAsync(skew, 0, 2 * sizeof(uint32_t), stream)) != cudaSuccess)
+                return cuda_fail(e, "pr local count");
+            pr_local_base_kernel<<<p, 256, 0, stream>>>(cA, n, p, bA, skew);
+            pr_local_base_kernel<<<p, 256, 0, stream>>>(cB, n, p, bB, skew + 1);
             launches += 2;
             if (!add(launch_onesweep_seg(A, mid, n, p, 8, shift, reinterpret_cast<const uint64_t*>(bA),
-                                         ctx->status.as<uint32_t>(), stream)) ||
+                                         ctx->status.as<uint32_t>(), stream, skew)) ||
                 !add(launch_onesweep_seg(mid, S, n, p, 8, shift + 8, reinterpret_cast<const uint64_t*>(bB),
-                                         ctx->status.as<uint32_t>(), stream)))
+                                         ctx->status.as<uint32_t>(), stream, skew + 1)))
                 return cuda_fail(cudaGetLastError(), "pr local pass");
         }
         {

@@ -982,6 +982,7 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
     __shared__ const uint32_t* s_src[4];
     __shared__ uint32_t* s_dst[4];
     __shared__ int s_active[4];
+    __shared__ int s_skew[4];
     __shared__ const uint32_t* s_final;
     __shared__ int s_copy;
     __shared__ uint64_t s_warp[kSmallThreads / 32];
@@ -1020,13 +1021,17 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
     for (int p = 0; p < 4; ++p) {
         const uint32_t total = tid < 256 ? __ldcg(&g_hist[p * 256 + tid]) : 0u;
         const int ident = __syncthreads_or(tid < 256 && total == n);
+        const int skew = __syncthreads_or(tid < 256 && static_cast<uint64_t>(total) * 16 > n);
         const uint64_t incl = warp_inclusive_scan(static_cast<uint64_t>(total));
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
         uint64_t excl = incl - total;
         for (int w = 0; w < warp; ++w) excl += s_warp[w];
         if (tid < 256) s_base[p * 256 + tid] = excl;
-        if (tid == 0) s_active[p] = !ident;
+        if (tid == 0) {
+            s_active[p] = !ident;
+            s_skew[p] = skew;
+        }
         __syncthreads();
     }
     if (tid == 0) {
@@ -1056,11 +1061,16 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
     for (int p = 0; p < 4; ++p) {
         if (!s_active[p]) continue;
         uint32_t* region = regions + static_cast<uint64_t>(p) * region_words;
-        // all tiles are in flight at once here: the wide window
-        onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0, PlainSink, BSG_LB_WIN>(
-            smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p,
-                                                               s_base + p * 256, region + 32, region, use_tma, 0,
-                                                               neg1, first, parity);
+        // all tiles are in flight at once here: the wide window; count then
+        // rank unless a digit holds > n/16 keys (then rank first)
+        if (s_skew[p])
+            onesweep_tiles<8, kSmallThreads, kSmallItems, false, 0, PlainSink, BSG_LB_WIN>(
+                smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p, s_base + p * 256, region + 32, region, use_tma, 0,
+                neg1, first, parity);
+        else
+            onesweep_tiles<8, kSmallThreads, kSmallItems, false, 3, PlainSink, BSG_LB_WIN>(
+                smem, s_src[p], PlainSink{s_dst[p]}, n, 8 * p, s_base + p * 256, region + 32, region, use_tma, 0,
+                neg1, first, parity);
         first = false;
         bar_target += G;
         grid_barrier(g_bar, bar_target);
@@ -1195,16 +1205,22 @@ template <int BITS, int THREADS, int ITEMS, bool WIDE>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_seg_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, const SegDesc sd, int shift,
                         const uint64_t* __restrict__ base_table, uint32_t* __restrict__ status,
-                        uint32_t* __restrict__ tile_counter, int32_t neg1) {
+                        uint32_t* __restrict__ tile_counter, int32_t neg1, const uint32_t* __restrict__ skew) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PlainSink, default_lb_window<THREADS>(), true>(
-        smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
+    // count then rank unless the caller flags a heavy digit (or gives no flag)
+    if (BITS == 8 && skew && !*skew)
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PlainSink, default_lb_window<THREADS>(), true>(
+            smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
+    else
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PlainSink, default_lb_window<THREADS>(), true>(
+            smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
 }
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE = false>
 int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int shift,
-                            const uint64_t* base_table, uint32_t* status, cudaStream_t stream) {
+                            const uint64_t* base_table, uint32_t* status, cudaStream_t stream,
+                            const uint32_t* skew) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
     auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS, WIDE>;
@@ -1230,26 +1246,26 @@ int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int 
     if (cudaMemsetAsync(status, 0, (32 + tiles * RADIX * (WIDE ? 2 : 1)) * sizeof(uint32_t), stream) != cudaSuccess)
         return -1;
     TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
-    kern<<<grid, THREADS, L::bytes, stream>>>(src, dst, sd, shift, base_table, status + 32, status, -1);
+    kern<<<grid, THREADS, L::bytes, stream>>>(src, dst, sd, shift, base_table, status + 32, status, -1, skew);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
-                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream) {
+                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream, const uint32_t* skew) {
     if (n == 0) return 0;
     if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys || n > 0xFFFFFFFFull) {
         // 64-bit status words and positions
         if (bits != 8) return -1;
-        return launch_onesweep_seg_cfg<8, 512, 24, true>(src, dst, n, p, shift, base_table, status, stream);
+        return launch_onesweep_seg_cfg<8, 512, 24, true>(src, dst, n, p, shift, base_table, status, stream, skew);
     }
     switch (bits) {
-    case 1: return launch_onesweep_seg_cfg<1, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
-    case 2: return launch_onesweep_seg_cfg<2, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
-    case 4: return launch_onesweep_seg_cfg<4, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
+    case 1: return launch_onesweep_seg_cfg<1, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);
+    case 2: return launch_onesweep_seg_cfg<2, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);
+    case 4: return launch_onesweep_seg_cfg<4, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);
     case 8:
         if (n > (uint64_t{1} << 23))
-            return launch_onesweep_seg_cfg<8, 512, 24>(src, dst, n, p, shift, base_table, status, stream);
-        return launch_onesweep_seg_cfg<8, 512, 16>(src, dst, n, p, shift, base_table, status, stream);
+            return launch_onesweep_seg_cfg<8, 512, 24>(src, dst, n, p, shift, base_table, status, stream, skew);
+        return launch_onesweep_seg_cfg<8, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);
     default: return -1;
     }
 }

@@ -68,8 +68,11 @@ struct PeerTable {
 // PR round in ONE launch: key i of block w with digit d goes to
 // base_table[w][d] + (its rank among block w's digit-d keys).  Returns
 // launches (0 or 1) or -1.
+// skew: device flag (0 = no digit holds > 1/16 of a block: count-then-rank
+// path); nullptr = always rank first.
 int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
-                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream);
+                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream,
+                        const uint32_t* skew = nullptr);
 uint64_t onesweep_seg_status_words(uint64_t n, int p);
 
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
