@@ -911,7 +911,7 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     const int radix = 1 << radix_log2;
     const int chunks = (radix + kDigChunk - 1) / kDigChunk;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks;
+    const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks + 1; // + skew flag
     cudaError_t e = ctx->pr_delta.ensure(words * 8);
     if (e == cudaSuccess) e = ctx->status.ensure(onesweep_status_words(std::max<uint64_t>(len, 1)) * sizeof(uint32_t));
     if (e != cudaSuccess) return cuda_fail(e, "fused round workspace");
@@ -920,6 +920,7 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     uint64_t* dstart = coltot + radix;
     uint64_t* base = dstart + radix;
     uint64_t* colchunk = base + radix;
+    uint32_t* skew = reinterpret_cast<uint32_t*>(colchunk + chunks); // heavy-digit flag of this round
     PeerTable tab{};
     for (int w = 0; w < p; ++w) {
         if (!peer_blocks[w] && bsg_partition_size_of(n, p, w)) return fail(BSG_EINVAL, "fused round: null peer block");
@@ -929,14 +930,15 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     tab.offset[p] = n;
     {
         TimedScope ts(3 /*BSG_K_PR*/, st);
-        pr_plan_col_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all, p, radix, before, coltot, colchunk);
+        if ((e = cudaMemsetAsync(skew, 0, sizeof(uint32_t), st)) != cudaSuccess) return cuda_fail(e, "fused round plan");
+        pr_plan_col_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all, p, radix, before, coltot, colchunk, skew, n);
         pr_digit_start_kernel<<<chunks, kDigChunk, 0, st>>>(coltot, colchunk, radix, dstart);
         pr_fused_base_kernel<<<(radix + 255) / 256, 256, 0, st>>>(dstart, before + static_cast<uint64_t>(me) * radix,
                                                                  radix, base);
         ctx->launches += 3;
     }
     const int l = launch_onesweep_peer(block, len, radix_log2, round * radix_log2, base, ctx->status.as<uint32_t>(),
-                                       tab, p, st);
+                                       tab, p, st, skew);
     if (l < 0) return cuda_fail(cudaGetLastError(), "fused round launch");
     ctx->launches += static_cast<uint64_t>(l);
     if ((e = cudaPeekAtLastError()) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fused round launch");

@@ -1141,17 +1141,23 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_peer_kernel(const uint32_t* __restrict__ src, uint64_t len, int shift,
                          const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                          uint32_t* __restrict__ tile_counter, int use_tma, int32_t neg1,
-                         const __grid_constant__ PeerTable tab, int p) {
+                         const __grid_constant__ PeerTable tab, int p, const uint32_t* __restrict__ skew) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t parity = 0;
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
-                                                              status, tile_counter, use_tma, 0, neg1, true, parity);
+    // count then rank unless the round's count matrix has a heavy digit
+    if (BITS == 8 && skew && !*skew)
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
+                                                                  status, tile_counter, use_tma, 0, neg1, true, parity);
+    else
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PeerSink>(smem, src, PeerSink{&tab, p}, len, shift, digit_base,
+                                                                  status, tile_counter, use_tma, 0, neg1, true, parity);
     __threadfence_system(); // peer stores performed before the round's barrier
 }
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE = false>
 int launch_onesweep_peer_cfg(const uint32_t* block, uint64_t len, int shift, const uint64_t* digit_base,
-                             uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream) {
+                             uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream,
+                             const uint32_t* skew) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     auto kern = onesweep_peer_kernel<BITS, THREADS, ITEMS, WIDE>;
     static int per_sm = 0;
@@ -1172,26 +1178,26 @@ int launch_onesweep_peer_cfg(const uint32_t* block, uint64_t len, int shift, con
     const bool tma = true; // per-tile aligned bodies (head/tail keys via plain loads)
     TimedScope ts(3 /*BSG_K_PR*/, stream);
     kern<<<grid, THREADS, L::bytes, stream>>>(block, len, shift, digit_base, status + 32, status, tma ? 1 : 0, -1,
-                                              tab, p);
+                                              tab, p, skew);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
-                         uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream) {
+                         uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream, const uint32_t* skew) {
     if (len == 0) return 0;
     if (len > kChunkKeys) // 64-bit status words and positions (config 5: 2^30-2^32 keys per GPU)
         return bits == 8 ? launch_onesweep_peer_cfg<8, 512, 24, true>(block, len, shift, digit_base, status, tab, p,
-                                                                        stream)
+                                                                        stream, skew)
                          : -1;
     const uint32_t n = static_cast<uint32_t>(len);
     switch (bits) {
-    case 1: return launch_onesweep_peer_cfg<1, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
-    case 2: return launch_onesweep_peer_cfg<2, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
-    case 4: return launch_onesweep_peer_cfg<4, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream);
+    case 1: return launch_onesweep_peer_cfg<1, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream, skew);
+    case 2: return launch_onesweep_peer_cfg<2, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream, skew);
+    case 4: return launch_onesweep_peer_cfg<4, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream, skew);
     case 8:
         if (len > (uint64_t{1} << 23))
-            return launch_onesweep_peer_cfg<8, 512, 24>(block, n, shift, digit_base, status, tab, p, stream);
-        return launch_onesweep_peer_cfg<8, 512, 16>(block, n, shift, digit_base, status, tab, p, stream);
+            return launch_onesweep_peer_cfg<8, 512, 24>(block, n, shift, digit_base, status, tab, p, stream, skew);
+        return launch_onesweep_peer_cfg<8, 512, 16>(block, n, shift, digit_base, status, tab, p, stream, skew);
     default: return -1;
     }
 }
