@@ -43,6 +43,9 @@
 #ifndef BSG_SCAN_NBAR
 #define BSG_SCAN_NBAR 1 // named barrier among the scan warps instead of a CTA barrier (-0.6%)
 #endif
+#ifndef BSG_EARLY_COUNT
+#define BSG_EARLY_COUNT 1 // count-then-rank: the upper half of the warps counts the next tile during the look-back
+#endif
 #ifndef BSG_LB_FIRST
 #define BSG_LB_FIRST 0 // wider first look-back round (predecessors), 0 = same as the window
 #endif
@@ -466,6 +469,14 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     const uint32_t gt = ~(lt | (1u << lane));
     uint32_t lbs_rounds = 0, lbs_used = 0, lbs_stops = 0, lbs_tiles = 0;
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
+    uint32_t keys[ITEMS];
+    // Early count (count-then-rank only): while warps [0, WARPS/2) walk the
+    // look-back of tile k, warps [WARPS/2, WARPS) already load their keys of
+    // tile k+1 (TMA-delivered to the other buffer) and count them into their
+    // own (reset) counter rows; in iteration k+1 they skip the count phase.
+    constexpr bool EARLY = RANK == 3 && BSG_EARLY_COUNT && BITS == 8 && !WIDE && THREADS == 512 && ITEMS == 24 && !SEG;
+    const bool early_warp = EARLY && warp >= WARPS / 2;
+    bool have_next = false; // this warp's keys and counts of the current tile are in place
     for (uint32_t k = 0;; ++k) {
         const int cur = k & 1;
         __syncthreads(); // s_tile[cur] visible; previous tile's buffer/counters free
@@ -497,8 +508,11 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 t_ph = now;
             }
         };
-        mbar_wait_parity(&s_bar[cur], (bar_parity >> cur) & 1u);
-        bar_parity ^= 1u << cur;
+        const bool pre = early_warp && have_next; // keys + counts of this tile already in place
+        if (!pre) {
+            mbar_wait_parity(&s_bar[cur], (bar_parity >> cur) & 1u);
+            bar_parity ^= 1u << cur;
+        }
         phase(0);
 
         // ---- warp-local stable ranks + per-warp digit counts --------------
@@ -506,7 +520,6 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         // key w*32*ITEMS + i*32 + l: item-major, lane-minor = input order.
         const uint32_t wbase = warp * (32 * ITEMS);
         uint16_t* wc = s_wcnt + warp * RADIX;
-        uint32_t keys[ITEMS];
         uint32_t packed[ITEMS / 2];
         auto rank_items = [&](auto full_tag, auto aligned_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
@@ -576,9 +589,12 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         };
         // full TMA tiles rank straight from shared memory; partial tiles and
         // misaligned (non-TMA) bodies take the guarded path
-        if (full && hw == 0 && body == static_cast<uint32_t>(TILE)) rank_items(std::true_type{}, std::true_type{});
+        if (pre) {
+            // counted during the previous tile's look-back
+        } else if (full && hw == 0 && body == static_cast<uint32_t>(TILE)) rank_items(std::true_type{}, std::true_type{});
         else if (full) rank_items(std::true_type{}, std::false_type{});
         else rank_items(std::false_type{}, std::false_type{});
+        have_next = false;
         phase(1);
         __syncthreads();
         phase(2);
@@ -670,6 +686,38 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             };
             if (full) rank_stage(std::true_type{});
             else rank_stage(std::false_type{});
+            if (early_warp) {
+                const uint32_t nxt = s_tile[cur ^ 1];
+                if (nxt < ntiles) {
+                    uint64_t nstart;
+                    uint32_t nvalid, nfirst, nseg;
+                    tile_range(nxt, nstart, nvalid, nfirst, nseg);
+                    const uint32_t nhw = head_words(src + nstart, nvalid);
+                    const uint32_t nbody = use_tma ? ((nvalid - nhw) & ~3u) : 0u;
+                    // own counter row: this tile's ranks are done with it
+                    uint32_t* row = reinterpret_cast<uint32_t*>(wc);
+                    for (int i = lane; i < RADIX / 2; i += 32) row[i] = 0;
+                    __syncwarp();
+                    mbar_wait_parity(&s_bar[cur ^ 1], (bar_parity >> (cur ^ 1)) & 1u);
+                    bar_parity ^= 1u << (cur ^ 1);
+                    const uint32_t* nbuf = s_in + (cur ^ 1) * TILE;
+#pragma unroll
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const uint32_t idx = wbase + i * 32 + lane;
+                        const uint32_t rel = idx - nhw;
+                        keys[i] = idx < nvalid ? (rel < nbody ? nbuf[rel] : __ldg(src + nstart + idx)) : 0u;
+                    }
+#pragma unroll
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const uint32_t idx = wbase + i * 32 + lane;
+                        if (idx < nvalid) {
+                            const uint32_t d = digit_of_key<BITS>(keys[i], shift);
+                            atomicAdd(row + (d >> 1), 1u << ((d & 1u) * 16u));
+                        }
+                    }
+                    have_next = true;
+                }
+            }
         } else if (dbg & 16) {
             // timing experiment only: skip staging
         } else if (full) { // every item valid: no per-item guards
@@ -747,7 +795,12 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         if (BSG_CLAIM_AT == 2) claim_next();
         phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
-        for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
+        if (EARLY) {
+            if (!early_warp) // early warps hold the next tile's counts already
+                for (int i = lane; i < RADIX / 2; i += 32) reinterpret_cast<uint32_t*>(wc)[i] = 0;
+        } else {
+            for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t*>(s_wcnt)[i] = 0;
+        }
         if (dbg & 4) {
             // timing experiment only: skip the write-out
         } else if (full) {
@@ -795,7 +848,9 @@ __global__ void __launch_bounds__(THREADS, (onesweep_min_blocks<THREADS, ITEMS>(
     if constexpr (RANK == 3) {
         // skewed digit distribution (a digit holds > n/16 keys): the counting
         // reductions would serialise on that digit's counter; rank first
-        // (warp-aggregated by the ballot multisplit) instead
+        // (warp-aggregated by the ballot multisplit) instead.  (Two kernels
+        // launched back to back, one exiting at once, measured 1.6% slower:
+        // an empty 296-CTA launch per pass costs ~13 us.)
         if (plan->skew[pass]) {
             onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0>(smem, plan->src[pass] + chunk_off,
                                                           PlainSink{plan->dst[pass]}, chunk_n, shift, digit_base,
