@@ -955,10 +955,11 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     int cfg = onesweep_cfg();
-    // measured on B200 (profiles/r01_onesweep_cfg_sweep.txt): 512x16 up to
-    // 2^21 keys (only when the fused small-n sort is off), 1024x16 up to 2^23,
-    // 512x24 beyond (12288-key tiles, two CTAs per SM, 4-wide look-back)
-    if (cfg == 0) cfg = n <= (uint64_t{1} << 21) ? 1 : (n <= (uint64_t{1} << 23) ? 2 : 6);
+    // measured on B200 with the count-then-rank kernels
+    // (profiles/r01_onesweep_cfg_sweep.txt): 512x16 up to 2^25 keys (8192-key
+    // tiles, two CTAs per SM; 2^22-2^24: 7% faster than 1024x16), 512x24
+    // beyond (12288-key tiles, 4-wide look-back)
+    if (cfg == 0) cfg = n <= (uint64_t{1} << 25) ? 1 : 6;
     switch (cfg) {
     case 3: // 256 x 16: 4096-key tiles so small inputs still fill 148 SMs
         return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,

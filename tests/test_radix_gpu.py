@@ -182,8 +182,8 @@ def test_every_onesweep_configuration(cuda, bsg, orc, cfg):
 
 
 def test_auto_configuration_boundaries(cuda, bsg, orc):
-    """Sizes either side of the auto-selection thresholds (2^21, 2^23)."""
-    for n in ((1 << 21), (1 << 21) + 1, (1 << 23) + 1):
+    """Sizes either side of the auto-selection thresholds (2^21, 2^25)."""
+    for n in ((1 << 21), (1 << 21) + 1, (1 << 25), (1 << 25) + 1):
         keys = orc.generate_uniform_keys(n, n)
         np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), orc.serial_radix_sort(keys, 256))
 
