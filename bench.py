@@ -474,7 +474,7 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
     ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-inflight", type=int, default=3,
+    ap.add_argument("--e2e-inflight", type=int, default=4,
                     help="sorts in flight in the e2e measurement (host threads, one context/stream each)")
     ap.add_argument("--pr-variant", choices=["A", "B", "P"], default="P",
                     help="multi-GPU algorithm: A = per-round PR4 (4 NCCL exchanges), B = single exchange, "
