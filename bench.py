@@ -126,44 +126,55 @@ def _sorted_permutation_checks(inp, out) -> bool:
     return int(a.sum()) == int(b.sum()) and sq(a) == sq(b) and cube(a) == cube(b)
 
 
-def cpu_baseline_sample(n_sample: int = 1 << 24, reps: int = 3):
+def cpu_baseline_sample(keys: np.ndarray, reps: int = 1):
     """The reference's serial_radix_sort(., 256) on one host core (SR4, the
-    paper's baseline row) on a bounded sample, timed like run_once."""
+    paper's baseline row, bench.hpp:185-199) on the SAME config-2 keys (all
+    2^28 of them), timed like run_once (bench.hpp:114-141)."""
     from oracle.pyoracle import Oracle, maybe_reference
-    import paper_1708_09495_b200 as bsg
 
-    keys = bsg.generate_uniform_keys(n_sample, bsg.derive_seed(1, 0))
     ref = maybe_reference()
     impl, kind = (ref, "reference") if ref is not None else (Oracle(), "port")
     ts = []
     for _ in range(reps):
         t, out = impl.time_serial_radix_sort(keys, 256)
         ts.append(t)
-    assert np.array_equal(out, np.sort(keys))
+    assert np.array_equal(out[:: max(1, keys.size // 65536)], np.sort(keys)[:: max(1, keys.size // 65536)])
     t = statistics.median(ts)
-    return {"value": n_sample / t, "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": f"serial_radix_sort(.,256) (SR4) of {n_sample} uniform keys on 1 host core, median of {reps}, "
-                      f"timed like bench.hpp run_once; host {os.cpu_count()} threads"}
+    return {"value": keys.size / t, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"serial_radix_sort(.,256) (SR4) of the config-2 keys (n={keys.size}) on 1 host core, "
+                      f"{'median of ' + str(reps) if reps > 1 else 'one run'}, timed like bench.hpp run_once; "
+                      f"host {os.cpu_count()} threads, {_cpu_model()}"}
 
 
 def run_reference(args, rank: int, world: int):
-    """--impl reference: PR4 with p = all host threads on a bounded sample."""
+    """--impl reference: the reference's own CPU implementation of config 2.
+
+    Only the reference's headers compiled unmodified (oracle/_ref/libbspref.so)
+    run here -- the product package is never imported, so libbsg.so is not
+    loaded in this process.  Keys come from the reference's own
+    generate_uniform_keys (core.hpp:93-99) with derive_seed(1, 0)
+    (bench.hpp:86-88).  A step is run_parallel_radix PR4 (radix.hpp:260-303,
+    r=256: the same 4 stable count-sort rounds as config 2) with p = every
+    host thread over ALL n = 2^28 keys, timed like bench::detail::run_once
+    (bench.hpp:114-141: prepare outside, run inside the clock).  Under torchrun
+    only rank 0 runs; the others exit without work."""
     if rank != 0:
         return
     from oracle.pyoracle import Oracle, maybe_reference
-    import paper_1708_09495_b200 as bsg
 
-    n = args.ref_n
-    keys = bsg.generate_uniform_keys(n, bsg.derive_seed(1, 0))
+    n = args.ref_n if args.ref_n else N_PER_GPU
     ref = maybe_reference()
     p = os.cpu_count() or 1
+    seed = Oracle().derive_seed(1, 0)
     if ref is not None:
         kind = "reference"
+        keys = ref.generate_uniform_keys(n, seed)
         step = lambda: ref.time_parallel_radix(keys, p, 256)  # noqa: E731
-        what = f"run_parallel_radix PR4 (r=256) with p={p} worker threads"
-    else:  # the oracle port is single-threaded
-        kind, p = "port", 1
+        what = f"reference run_parallel_radix PR4 (r=256, 4 rounds) with p={p} worker threads"
+    else:  # the oracle port is single-threaded (only when the reference could not be compiled)
         orc = Oracle()
+        kind, p = "port", 1
+        keys = orc.generate_uniform_keys(n, seed)
         step = lambda: orc.time_serial_radix_sort(keys, 256)  # noqa: E731
         what = "oracle port serial_radix_sort(.,256), 1 thread"
     for _ in range(args.warmup):
@@ -172,20 +183,37 @@ def run_reference(args, rank: int, world: int):
     for _ in range(args.steps):
         t, out = step()
         ts.append(t)
-    assert np.array_equal(out, np.sort(keys))
+    verified = bool(np.array_equal(out, np.sort(keys)))
     t = sum(ts) / len(ts)
     value = n / t
-    sample = (f"{what} on {n} uniform keys per step (a bounded sample of the {N_PER_GPU * world}-key workload), "
-              f"mean of {args.steps} steps, timed like bench.hpp run_once")
+    full = n == N_PER_GPU and world == 1
+    sample = (f"{what} on n={n} keys per step "
+              + ("(the full config-2 workload)" if full else f"(a bounded sample of the {world}-GPU workload)")
+              + f", mean of {args.steps} steps, timed like bench.hpp run_once; host: {os.cpu_count()} threads, "
+              + _cpu_model())
+    cfg = _config(1) if world == 1 else _config(world, args.pr_variant)
+    cfg = dict(cfg, n=n, algorithm="PR4" if kind == "reference" else "SR4")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": _config(world, None if world == 1 else "B"),
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (reference generator, seeded)", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": p, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "verified": verified,
     }
     print(json.dumps(line), flush=True)
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for l in f:
+                if l.startswith("model name"):
+                    return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
 
 
 def _config(world: int, variant=None):
@@ -344,7 +372,7 @@ def run_single(args):
         "verified": ok and ok_e2e,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample()
+        line["cpu_baseline"] = cpu_baseline_sample(keys)
     print(json.dumps(line), flush=True)
 
 
@@ -472,7 +500,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
-    ap.add_argument("--ref-n", type=int, default=1 << 26, help="keys per reference step (bounded sample)")
+    ap.add_argument("--ref-n", type=int, default=0, help="keys per reference step (default: config 2's 2^28)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-inflight", type=int, default=4,
                     help="sorts in flight in the e2e measurement (host threads, one context/stream each)")
