@@ -19,7 +19,13 @@
  *    (pinned for full PCIe speed); the call copies in, sorts, copies out and
  *    synchronises `stream` before returning -- the reference's synchronous
  *    by-value semantics (radix.hpp:180, netsort.hpp:157).
- *  - in == out is allowed everywhere (in-place).
+ *  - in == out is allowed everywhere (in-place); partially overlapping device
+ *    inputs/outputs (e.g. merge_split's low == a, or a padded intermediate
+ *    network state written over its own input) are staged through the
+ *    context's workspace first, so any aliasing gives the non-aliased result.
+ *  - One context may be used from several streams: each call is ordered
+ *    after the context's previous call (an event on the previous stream), as
+ *    all calls share the context's device workspace.
  *  - Keys are uint32; counts and positions are 64-bit everywhere (n may
  *    exceed 2^32 on one GPU), fixing the reference's uint32 count blocks
  *    (radix.hpp:238-243) which wrap at 2^32 keys per worker.

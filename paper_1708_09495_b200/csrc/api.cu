@@ -84,6 +84,12 @@ int with_device_io(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n_i
     return BSG_OK;
 }
 
+bool ranges_overlap(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb) {
+    if (!na || !nb) return false;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+    return a0 < b0 + nb * 4 && b0 < a0 + na * 4;
+}
+
 int radix_bits_or_fail(int radix_log2) {
     if (radix_log2 != 1 && radix_log2 != 2 && radix_log2 != 4 && radix_log2 != 8 && radix_log2 != 16) {
         if (radix_log2 > 16 && radix_log2 <= 32 && 32 % radix_log2 == 0)
@@ -129,6 +135,7 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
                           &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
                           &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->mt_ws})
             b->release();
+        if (ctx->last_use) cudaEventDestroy(ctx->last_use);
     }
     delete ctx;
     return BSG_OK;
@@ -176,6 +183,7 @@ int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t
     if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
     CallGuard g(ctx);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
         RadixWorkspace ws;
         if (int rc = ctx->radix_ws(n, &ws)) return rc;
@@ -201,6 +209,7 @@ int bsg_count_sort_round_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
     CallGuard g(ctx);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
         RadixWorkspace ws;
         if (int rc = ctx->radix_ws(n, &ws)) return rc;
@@ -230,7 +239,22 @@ int bsg_merge_split_u32(bsg_ctx* ctx, const uint32_t* a, uint64_t na, const uint
     if (na + nb >= (uint64_t{1} << 31)) return fail(BSG_EINVAL, "merge_split: |a|+|b| must be < 2^31");
     CallGuard g(ctx);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     if (mem_kind == BSG_MEM_DEVICE) {
+        // merge_split_kernel reads a/b while other CTAs write low/high: when
+        // an output overlaps an input, stage the inputs through workspace
+        if (ranges_overlap(a, na, low, na) || ranges_overlap(a, na, high, nb) || ranges_overlap(b, nb, low, na) ||
+            ranges_overlap(b, nb, high, nb)) {
+            cudaError_t e = ctx->stage_b.ensure(std::max<uint64_t>(na + nb, 4) * 4);
+            if (e != cudaSuccess) return cuda_fail(e, "merge_split staging");
+            uint32_t* sa = ctx->stage_b.as<uint32_t>();
+            if (na && (e = cudaMemcpyAsync(sa, a, na * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+                return cuda_fail(e, "merge_split staging");
+            if (nb && (e = cudaMemcpyAsync(sa + na, b, nb * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+                return cuda_fail(e, "merge_split staging");
+            a = sa;
+            b = sa + na;
+        }
         const int l = launch_merge_split(a, na, b, nb, low, high, st);
         if (l < 0) return cuda_fail(cudaGetLastError(), "merge_split launch");
         ctx->launches += static_cast<uint64_t>(l);
@@ -285,10 +309,23 @@ int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in,
     }
     CallGuard g(ctx);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     const uint64_t n_in = num_arrays * len, n_out = num_arrays * out_per;
     return with_device_io(ctx, in, out, n_in, n_out, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
         if (num_arrays == 0 || len == 0) return BSG_OK;
         if (padded <= kNetMaxPadded) { // shared-memory resident arrays: one CTA per array
+            // one CTA reads array a and writes array a at the same stride: in
+            // place is safe; a different output stride (padded intermediate
+            // states) or a shifted overlap would overwrite arrays other CTAs
+            // have yet to read, so stage the input through workspace
+            if (ranges_overlap(d_in, n_in, d_out, n_out) && !(d_in == d_out && out_per == len)) {
+                cudaError_t e = ctx->stage_b.ensure(std::max<uint64_t>(n_in, 4) * 4);
+                if (e != cudaSuccess) return cuda_fail(e, "network staging");
+                if ((e = cudaMemcpyAsync(ctx->stage_b.as<uint32_t>(), d_in, n_in * 4, cudaMemcpyDeviceToDevice, s)) !=
+                    cudaSuccess)
+                    return cuda_fail(e, "network staging");
+                d_in = ctx->stage_b.as<uint32_t>();
+            }
             const int l = launch_block_network(network, d_in, d_out, num_arrays, len, p, run, full, s);
             if (l < 0) return cuda_fail(cudaGetLastError(), "block network launch");
             ctx->launches += static_cast<uint64_t>(l);
@@ -341,6 +378,7 @@ int bsg_parallel_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out,
     const int rounds = (rounds_limit >= 0 && rounds_limit < all_rounds) ? rounds_limit : all_rounds;
     CallGuard g(ctx);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
         return run_parallel_radix_local(ctx, d_in, d_out, n, p, radix_log2, rounds, stats, s);
     });
@@ -383,6 +421,7 @@ int bsg_pr_count_digits(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int r
     if (int rc = radix_bits_or_fail(radix_log2)) return rc;
     if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
     CallGuard g(ctx);
+    StreamOrder order(ctx, static_cast<cudaStream_t>(stream));
     const int l = launch_pr_count(ctx, block, len, round, radix_log2, counts, static_cast<cudaStream_t>(stream));
     if (l < 0) return cuda_fail(cudaGetLastError(), "count_digits launch");
     ctx->launches += static_cast<uint64_t>(l);
@@ -396,6 +435,7 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
     if (p < 1 || me < 0 || me >= p) return fail(BSG_EINVAL, "pr_plan: worker index out of range");
     (void)round;
     CallGuard g(ctx);
+    StreamOrder order(ctx, static_cast<cudaStream_t>(stream));
     // scratch for launch_pr_plan: split[p], coltot[r], dstart[r], colchunk[r/1024], rowchunk[p][r/1024]
     const uint64_t chunks = ((uint64_t{1} << radix_log2) + 1023) / 1024;
     cudaError_t e = ctx->pr_recv.ensure(
@@ -443,6 +483,7 @@ int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len, const 
     (void)recv_counts;
     (void)p;
     CallGuard g(ctx);
+    StreamOrder order(ctx, static_cast<cudaStream_t>(stream));
     const int l = launch_pr_rebuild(recv, recv_len, radix_log2, round * radix_log2, rebuild_delta, block,
                                     static_cast<cudaStream_t>(stream), recv_counts, p);
     if (l < 0) return cuda_fail(cudaGetLastError(), "rebuild launch");

@@ -8,6 +8,35 @@
 namespace bsg {
 
 constexpr int kSmCountB200 = 148;
+constexpr int kMaxDevices = 64;
+
+// Kernel attributes (max dynamic shared memory) are per device, so every
+// launcher caches "attribute set + resident CTAs per SM" per device ordinal:
+// a context on cuda:1 must not launch a >48 KB-smem kernel whose attribute
+// was only set on cuda:0.  Returns the CTAs per SM (>= 1) for the current
+// device.  Racing first calls from two host threads both set the same value.
+struct PerDeviceOccupancy {
+    int per_sm[kMaxDevices] = {};
+};
+template <typename K>
+inline int kernel_occupancy(PerDeviceOccupancy& cache, K kern, int threads, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& v = cache.per_sm[dev & (kMaxDevices - 1)];
+    if (v == 0) {
+        int per = 0;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem);
+        v = per < 1 ? -1 : per; // -1: does not fit (recorded so it is not re-queried)
+    }
+    return v;
+}
+inline int current_sm_count() {
+    int dev = 0, sms = kSmCountB200;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
 
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t l;

@@ -55,6 +55,13 @@ struct bsg_ctx {
     bsg::DevBuf pr_counts, pr_sorted, pr_recv, pr_block, pr_misc, pr_delta;
     bsg::DevBuf net_sched, cnt32;
     bsg::DevBuf mt_ws; // device generator: segment start windows + jump polynomials
+    // Cross-stream ordering of the shared workspace: every call records
+    // `last_use` on its stream; a call on a different stream first waits on
+    // it, so device-mode calls issued on two streams never run on the same
+    // scratch buffers at once (the mutex alone only serialises the host side).
+    cudaEvent_t last_use = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool used = false;
 
     // Ensures the radix workspace for n keys and returns a view of it.
     int radix_ws(uint64_t n, bsg::RadixWorkspace* ws);
@@ -74,6 +81,27 @@ struct DeviceGuard {
         int cur = -1;
         cudaGetDevice(&cur);
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// RAII: order this call's stream after the context's previous call (see
+// bsg_ctx::last_use).  Construct with the context mutex held and the
+// context's device current.
+struct StreamOrder {
+    bsg_ctx* c;
+    cudaStream_t s;
+    StreamOrder(bsg_ctx* ctx, cudaStream_t stream) : c(ctx), s(stream) {
+        if (c->used && c->last_stream != s) cudaStreamWaitEvent(s, c->last_use, 0);
+    }
+    ~StreamOrder() {
+        if (!c->last_use && cudaEventCreateWithFlags(&c->last_use, cudaEventDisableTiming) != cudaSuccess) {
+            c->last_use = nullptr;
+            return;
+        }
+        if (cudaEventRecord(c->last_use, s) == cudaSuccess) {
+            c->last_stream = s;
+            c->used = true;
+        }
     }
 };
 

@@ -348,6 +348,7 @@ int bsg_generate_uniform_device_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n, uin
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dev(ctx->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     const uint64_t words = S * NW + static_cast<uint64_t>(std::max(rounds, 1)) * PW;
     cudaError_t e = ctx->mt_ws.ensure(words * sizeof(uint64_t));
     if (e != cudaSuccess) return cuda_fail(e, "generator workspace");

@@ -456,14 +456,13 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     const size_t smem = 2ull * padded * sizeof(uint32_t);
     const uint64_t grid = (num_arrays + apc - 1) / apc;
     if (grid > 0x7FFFFFFFull) return -1;
-    static const bool attr = [] {
-        const int max_smem = static_cast<int>(2 * (kNetMaxPadded + kNetMaxPadded / 32 + 1) * sizeof(uint32_t));
-        cudaFuncSetAttribute(block_network_kernel<256, BSG_NET_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             max_smem);
-        cudaFuncSetAttribute(block_network_kernel<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-        return true;
-    }();
-    (void)attr;
+    {
+        // per device (kernel attributes do not carry over to other GPUs)
+        const size_t max_smem = 2 * (kNetMaxPadded + kNetMaxPadded / 32 + 1) * sizeof(uint32_t);
+        static PerDeviceOccupancy occ_small, occ_big;
+        kernel_occupancy(occ_small, block_network_kernel<256, BSG_NET_MINB>, 256, max_smem);
+        kernel_occupancy(occ_big, block_network_kernel<1024, 1>, 1024, max_smem);
+    }
     const uint64_t resident = static_cast<uint64_t>(apc) * P;
     const bool big = resident > 8192;
     NetDivs dv;

@@ -536,11 +536,8 @@ int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round
     if (bits == 16) {
         if (cudaMemsetAsync(counts, 0, radix * sizeof(uint64_t), stream) != cudaSuccess) return -1;
         if (len == 0) return 0;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(hist16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
-            attr = true;
-        }
+        static PerDeviceOccupancy occ; // attribute per device
+        kernel_occupancy(occ, hist16_kernel, kHist16Threads, 32768 * 4);
         const uint64_t want = (len + kHist16Threads * 16 - 1) / (kHist16Threads * 16);
         const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200)));
         hist16_kernel<<<grid, kHist16Threads, 32768 * 4, stream>>>(block, len, 16 * round,
@@ -843,6 +840,7 @@ extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_
     const int radix = 1 << radix_log2;
     const int chunks = (radix + kDigChunk - 1) / kDigChunk;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     // scratch: before/delta [p][r] (int64), coltot [r], dstart [r], colchunk [chunks], gd [r]
     const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks;
     cudaError_t e = ctx->pr_delta.ensure(words * 8);
@@ -889,8 +887,6 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     if (p < 1 || p > kPeerMax || me < 0 || me >= p) return fail(BSG_EINVAL, "fused round: worker index out of range");
     if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
     if (len != bsg_partition_size_of(n, p, me)) return fail(BSG_EINVAL, "fused round: block size != size_of(me)");
-    if (len > kChunkKeys && radix_log2 < 8)
-        return fail(BSG_EINVAL, "fused round: blocks above 2^29 keys need r >= 2^8");
     if (!peer_blocks || !counts_all || (len && !block)) return fail(BSG_EINVAL, "null pointer");
     if (radix_log2 == 16) {
         cudaError_t e;
@@ -911,6 +907,7 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     const int radix = 1 << radix_log2;
     const int chunks = (radix + kDigChunk - 1) / kDigChunk;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
     const uint64_t words = static_cast<uint64_t>(p) * radix + 3ull * radix + chunks + 1; // + skew flag
     cudaError_t e = ctx->pr_delta.ensure(words * 8);
     if (e == cudaSuccess) e = ctx->status.ensure(onesweep_status_words(std::max<uint64_t>(len, 1)) * sizeof(uint32_t));
@@ -938,7 +935,7 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
         ctx->launches += 3;
     }
     const int l = launch_onesweep_peer(block, len, radix_log2, round * radix_log2, base, ctx->status.as<uint32_t>(),
-                                       tab, p, st, skew);
+                                       tab, p, st, skew, n);
     if (l < 0) return cuda_fail(cudaGetLastError(), "fused round launch");
     ctx->launches += static_cast<uint64_t>(l);
     if ((e = cudaPeekAtLastError()) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fused round launch");

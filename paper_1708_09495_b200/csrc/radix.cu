@@ -135,16 +135,10 @@ __global__ void __launch_bounds__(kHist2Threads)
 template <int BITS, int NDIG>
 void launch_hist(const uint32_t* in, uint64_t n, int first_shift, uint32_t* hist, cudaStream_t stream) {
     constexpr size_t smem = sizeof(uint32_t) * NDIG * (1 << BITS) * 32;
-    static int per_sm = 0;
+    static PerDeviceOccupancy occ;
     auto kern = hist_kernel<BITS, NDIG>;
-    if (per_sm == 0) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHist2Threads, smem);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int sms = kSmCountB200, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = std::max(1, kernel_occupancy(occ, kern, kHist2Threads, smem));
+    const int sms = current_sm_count();
     const uint64_t want = (n / 4 + kHist2Threads - 1) / kHist2Threads;
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, sms * per_sm)));
     kern<<<grid, kHist2Threads, smem, stream>>>(in, n, first_shift, hist);
@@ -897,18 +891,9 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
     auto kern = onesweep_kernel<BITS, THREADS, ITEMS, WIDE, RANK>;
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, L::bytes);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int sms = kSmCountB200;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    static PerDeviceOccupancy occ;
+    const int per_sm = std::max(1, kernel_occupancy(occ, kern, THREADS, L::bytes));
+    const int sms = current_sm_count();
     // one look-back domain per pass: [tile counter (32 words)] [tiles * RADIX status words]
     const uint32_t tiles = static_cast<uint32_t>((n + L::TILE - 1) / L::TILE);
     const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
@@ -1152,15 +1137,9 @@ int launch_small_sort(const uint32_t* in, uint32_t* out, uint64_t n, const Radix
     if (n == 0 || n > kSmallMaxKeys || !small_sort_enabled()) return 0;
     using L = OnesweepSmem<8, kSmallThreads, kSmallItems, false>;
     const size_t smem = L::bytes + 4 * 256 * sizeof(uint64_t);
-    static int per_sm = -1;
-    static int sms = 0;
-    if (per_sm < 0) {
-        cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_sort_kernel, kSmallThreads, smem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    static PerDeviceOccupancy occ;
+    const int per_sm = kernel_occupancy(occ, small_sort_kernel, kSmallThreads, smem);
+    const int sms = current_sm_count();
     if (per_sm < 1) return 0;
     const uint64_t region = small_region_words(n);
     if (cudaMemsetAsync(ws.status, 0, small_ws_words(n) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
@@ -1216,15 +1195,9 @@ int launch_onesweep_peer_cfg(const uint32_t* block, uint64_t len, int shift, con
                              const uint32_t* skew) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     auto kern = onesweep_peer_kernel<BITS, THREADS, ITEMS, WIDE>;
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, L::bytes);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int sms = kSmCountB200, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static PerDeviceOccupancy occ;
+    const int per_sm = std::max(1, kernel_occupancy(occ, kern, THREADS, L::bytes));
+    const int sms = current_sm_count();
     constexpr int RADIX = 1 << BITS;
     const uint32_t tiles = static_cast<uint32_t>((len + L::TILE - 1) / L::TILE);
     const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms * per_sm));
@@ -1239,12 +1212,22 @@ int launch_onesweep_peer_cfg(const uint32_t* block, uint64_t len, int shift, con
 }
 
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
-                         uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream, const uint32_t* skew) {
+                         uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream, const uint32_t* skew,
+                         uint64_t n_total) {
     if (len == 0) return 0;
-    if (len > kChunkKeys) // 64-bit status words and positions (config 5: 2^30-2^32 keys per GPU)
-        return bits == 8 ? launch_onesweep_peer_cfg<8, 512, 24, true>(block, len, shift, digit_base, status, tab, p,
-                                                                        stream, skew)
-                         : -1;
+    // 64-bit status words and positions when the block exceeds a 30-bit
+    // look-back count (config 5: 2^30-2^32 keys per GPU) OR when the global
+    // positions the write-out computes (digit bases up to n_total) do not fit
+    // in 32 bits -- e.g. 2^28 keys per GPU at p >= 17, or 2^33 keys at p = 16.
+    if (len > kChunkKeys || n_total > 0xFFFFFFFFull) {
+        switch (bits) {
+        case 1: return launch_onesweep_peer_cfg<1, 512, 24, true>(block, len, shift, digit_base, status, tab, p, stream, skew);
+        case 2: return launch_onesweep_peer_cfg<2, 512, 24, true>(block, len, shift, digit_base, status, tab, p, stream, skew);
+        case 4: return launch_onesweep_peer_cfg<4, 512, 24, true>(block, len, shift, digit_base, status, tab, p, stream, skew);
+        case 8: return launch_onesweep_peer_cfg<8, 512, 24, true>(block, len, shift, digit_base, status, tab, p, stream, skew);
+        default: return -1;
+        }
+    }
     const uint32_t n = static_cast<uint32_t>(len);
     switch (bits) {
     case 1: return launch_onesweep_peer_cfg<1, 1024, 16>(block, n, shift, digit_base, status, tab, p, stream, skew);
@@ -1286,15 +1269,9 @@ int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int 
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
     auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS, WIDE>;
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::bytes));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, L::bytes);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int sms = kSmCountB200, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static PerDeviceOccupancy occ;
+    const int per_sm = std::max(1, kernel_occupancy(occ, kern, THREADS, L::bytes));
+    const int sms = current_sm_count();
     SegDesc sd;
     sd.small = n / static_cast<uint64_t>(p);
     sd.p = static_cast<uint32_t>(p);

@@ -77,6 +77,6 @@ uint64_t onesweep_seg_status_words(uint64_t n, int p);
 
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
                          uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream,
-                         const uint32_t* skew = nullptr);
+                         const uint32_t* skew, uint64_t n_total);
 
 } // namespace bsg

@@ -293,6 +293,47 @@ def test_fused_round_large_blocks(cuda, bsg):
     torch.cuda.empty_cache()
 
 
+def test_fused_round_global_positions_above_2_32(cuda, bsg):
+    """bsg_pr_fused_round where the BLOCKS are small (< 2^29 keys, the
+    32-bit look-back rows would do) but the global positions are not:
+    n = 2^32 + 2^20 + 7 keys over p = 17 logical workers (~2^28 keys per
+    block, the weak-scaled 2^28-per-GPU shape at p >= 17).  Digit bases of the
+    high digits exceed 2^32, so the write-out must run the 64-bit position rows
+    (a 32-bit position would wrap and store keys at the wrong owner/offset).
+    All workers' round-0 passes together equal one count_sort_round of the
+    whole array (radix.hpp:44-65; a PR round is a stable count sort of the
+    block concatenation, radix.hpp:260-303)."""
+    torch = cuda
+    from paper_1708_09495_b200 import distributed as D
+
+    n, p = (1 << 32) + (1 << 20) + 7, 17
+    free, _ = torch.cuda.mem_get_info()
+    if free < 18 * n:
+        pytest.skip("not enough device memory")
+    ops = D.CudaStepOps(torch.device("cuda", 0))
+    keys = bsg.generate_uniform_keys_device(n, 1234).view(torch.int32)
+    sizes = [D.partition_size_of(n, p, w) for w in range(p)]
+    offs = [D.partition_offset_of(n, p, w) for w in range(p)]
+    assert max(sizes) < (1 << 29)
+    blocks = [keys[offs[w]:offs[w] + sizes[w]] for w in range(p)]
+    counts_all = torch.cat([ops.count(b, 0, 8) for b in blocks])
+    nxt = torch.empty_like(keys)
+    ptrs = [nxt[offs[w]:].data_ptr() for w in range(p)]
+    for me in range(p):
+        ops.fused_round(blocks[me], counts_all, n, p, me, 0, 8, ptrs)
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    exp = torch.empty_like(keys)
+    assert L.bsg_count_sort_round_u32(ctx.handle, keys.data_ptr(), exp.data_ptr(), n, 0, 8, 1, st) == 0
+    torch.cuda.synchronize()
+    step = 1 << 28
+    for a in range(0, n, step):
+        assert bool(torch.equal(nxt[a:a + step], exp[a:a + step])), a
+    del keys, nxt, exp, blocks
+    torch.cuda.empty_cache()
+
+
 def test_distributed_world1_large_block(cuda, bsg):
     """The multi-GPU orchestration (distributed.py) at a config-5 block size:
     one rank holding 2^30 + 7 keys (every per-rank kernel past 2^29 keys runs

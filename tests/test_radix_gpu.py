@@ -302,3 +302,74 @@ def test_in_place_calls(cuda, bsg, orc):
                                            st) == 0
     torch.cuda.synchronize()
     np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32).reshape(64, 4096), np.sort(arrs, axis=1))
+
+
+def test_one_context_two_streams(cuda, bsg, orc):
+    """Device-mode calls on ONE context issued on two different streams share
+    the context's workspace (tmp / status / hist); the context orders each
+    call after the previous one (bsg_ctx::last_use), so back-to-back sorts on
+    two streams with no host sync in between both come out right."""
+    torch = cuda
+    ctx = bsg._lib.context(0)
+    L = bsg._lib.lib()
+    n = (1 << 24) + 3
+    a = torch.from_numpy(orc.generate_uniform_keys(n, 71).view(np.int32)).cuda()
+    b = torch.from_numpy(orc.generate_uniform_keys(n, 72).view(np.int32)).cuda()
+    oa, ob = torch.empty_like(a), torch.empty_like(b)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        assert L.bsg_radix_sort_u32(ctx.handle, a.data_ptr(), oa.data_ptr(), n, 8, 1, s1.cuda_stream) == 0
+        assert L.bsg_radix_sort_u32(ctx.handle, b.data_ptr(), ob.data_ptr(), n, 8, 1, s2.cuda_stream) == 0
+        assert L.bsg_count_sort_round_u32(ctx.handle, a.data_ptr(), oa.data_ptr(), n, 1, 8, 1, s1.cuda_stream) == 0
+        assert L.bsg_radix_sort_u32(ctx.handle, b.data_ptr(), ob.data_ptr(), n, 8, 1, s2.cuda_stream) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(oa.cpu().numpy().view(np.uint32),
+                                  orc.count_sort_round(a.cpu().numpy().view(np.uint32), 1, 256))
+    np.testing.assert_array_equal(ob.cpu().numpy().view(np.uint32), np.sort(b.cpu().numpy().view(np.uint32)))
+
+
+def test_aliased_outputs(cuda, bsg, orc):
+    """Partially aliased device arguments give the non-aliased result:
+    merge_split with low == a / high == b (netsort.hpp:30-51), and a
+    truncated network (padded intermediate state, out_per > len) written over
+    its own input."""
+    torch = cuda
+    L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    a = np.sort(orc.generate_uniform_keys(300001, 5))
+    b = np.sort(orc.generate_uniform_keys(200003, 6))
+    lo_e, hi_e = orc.merge_split(a, b)
+    ta = torch.from_numpy(a.view(np.int32)).cuda()
+    tb = torch.from_numpy(b.view(np.int32)).cuda()
+    assert L.bsg_merge_split_u32(ctx.handle, ta.data_ptr(), a.size, tb.data_ptr(), b.size, ta.data_ptr(),
+                                 tb.data_ptr(), 1, st) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ta.cpu().numpy().view(np.uint32), lo_e)
+    np.testing.assert_array_equal(tb.cpu().numpy().view(np.uint32), hi_e)
+    # swapped roles: low over b's storage is too small unless |a| == |b|
+    a2, b2 = a[:200003], b
+    lo_e, hi_e = orc.merge_split(a2, b2)
+    ta = torch.from_numpy(a2.view(np.int32)).cuda()
+    tb = torch.from_numpy(b2.view(np.int32)).cuda()
+    assert L.bsg_merge_split_u32(ctx.handle, ta.data_ptr(), a2.size, tb.data_ptr(), b2.size, tb.data_ptr(),
+                                 ta.data_ptr(), 1, st) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(tb.cpu().numpy().view(np.uint32), lo_e)
+    np.testing.assert_array_equal(ta.cpu().numpy().view(np.uint32), hi_e)
+    # truncated network, len not divisible by p: out_per = padded > len
+    num, ln, p = 97, 1001, 8
+    arrs = orc.generate_uniform_keys(num * ln, 9).reshape(num, ln)
+    Lb = (ln + p - 1) // p
+    buf = torch.zeros(num * Lb * p, dtype=torch.int32, device="cuda")
+    buf[:num * ln] = torch.from_numpy(arrs.reshape(-1).view(np.int32)).cuda()
+    for stages in (0, 2):
+        t = buf.clone()
+        assert L.bsg_block_network_batched_u32(ctx.handle, 0, t.data_ptr(), t.data_ptr(), num, ln, p, stages, None,
+                                               1, st) == 0
+        torch.cuda.synchronize()
+        got = t.cpu().numpy().view(np.uint32).reshape(num, Lb * p)
+        for i in (0, 1, 50, num - 1):
+            exp, _ = orc.block_network(0, arrs[i], p, stages)
+            np.testing.assert_array_equal(got[i], exp)
