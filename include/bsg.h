@@ -18,7 +18,7 @@
  *    default stream) and returns.  BSG_MEM_HOST: in/out are host pointers
  *    (pinned for full PCIe speed); the call copies in, sorts, copies out and
  *    synchronises `stream` before returning -- the reference's synchronous
- *    by-value semantics (radix.hpp:180, netsort.hpp:157).
+ *    by-value semantics (radix.hpp:69, netsort.hpp:157).
  *  - in == out is allowed everywhere (in-place); partially overlapping device
  *    inputs/outputs (e.g. merge_split's low == a, or a padded intermediate
  *    network state written over its own input) are staged through the
@@ -28,7 +28,7 @@
  *    all calls share the context's device workspace.
  *  - Keys are uint32; counts and positions are 64-bit everywhere (n may
  *    exceed 2^32 on one GPU), fixing the reference's uint32 count blocks
- *    (radix.hpp:238-243) which wrap at 2^32 keys per worker.
+ *    (radix.hpp:127-132) which wrap at 2^32 keys per worker.
  *  - There is no CPU fallback: without a usable GPU every compute entry point
  *    fails with BSG_ECUDA.
  */
@@ -107,7 +107,7 @@ int bsg_generate_uniform_u32(uint32_t* out, uint64_t n, uint64_t seed);
 int bsg_generate_uniform_at_u32(uint32_t* out, uint64_t n, uint64_t seed, uint64_t offset);
 /* bench.hpp:77-88 derive_seed (splitmix64). */
 uint64_t bsg_derive_seed(uint64_t seed, int32_t rep);
-/* core.hpp:60-64 digit_bits + radix.hpp:143-151 checked_digit_bits:
+/* core.hpp:60-64 digit_bits + radix.hpp:32-40 checked_digit_bits:
  * lg r for r in {2,4,16,256,65536}, else -1 (and sets the error message). */
 int bsg_checked_digit_bits(uint64_t radix);
 /* Builder-defined skewed inputs for config 3 (not in the
@@ -120,18 +120,18 @@ int bsg_generate_skewed_u32(uint32_t* out, uint64_t n, uint64_t seed, int kind, 
  * cap_stages are written). */
 int bsg_network_schedule(int network, int p, int32_t* partner, int32_t* keep_low, int cap_stages,
                          int* stages);
-/* radix.hpp:207-229 detail::Partition */
+/* radix.hpp:96-118 detail::Partition */
 uint64_t bsg_partition_size_of(uint64_t n, int p, int w);
 uint64_t bsg_partition_offset_of(uint64_t n, int p, int w);
 int bsg_partition_owner_of(uint64_t n, int p, uint64_t pos);
 
 /* ---- sorts ------------------------------------------------------------ */
-/* radix.hpp:180-201 serial_radix_sort(KeyArray, radix): 32/lg r stable
+/* radix.hpp:69-90 serial_radix_sort(KeyArray, radix): 32/lg r stable
  * count-sort rounds (SR4 when r = 256).  Output is ascending. */
 int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
                        int radix_log2, int mem_kind, void* stream);
 
-/* radix.hpp:155-176 count_sort_round(keys, round, radix): one stable pass
+/* radix.hpp:44-65 count_sort_round(keys, round, radix): one stable pass
  * over digit `round` (low digit first).  radix_log2 in {1,2,4,8,16}. */
 int bsg_count_sort_round_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
                              int round, int radix_log2, int mem_kind, void* stream);
@@ -154,7 +154,7 @@ int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in,
                                   uint64_t num_arrays, uint32_t len, int p, int stages_limit,
                                   bsg_run_stats* stats, int mem_kind, void* stream);
 
-/* radix.hpp:344-414 prepare_parallel_radix + run_parallel_radix (PR4 at
+/* radix.hpp:233-303 prepare_parallel_radix + run_parallel_radix (PR4 at
  * r=256, PR2 at r=65536) with p logical workers resident on the context's
  * GPU: per round a digit count per worker, the p x r count exchange, the
  * stable local pass, slice routing and the rebuild, all as kernels.
@@ -177,11 +177,11 @@ int bsg_sort_instance_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint6
  * with the collectives.  All pointers are device pointers, all calls are
  * asynchronous on `stream`.  Counts are uint64. */
 
-/* radix.hpp:238-243 count_digits: counts[d] = #{keys in block with digit d}. */
+/* radix.hpp:127-132 count_digits: counts[d] = #{keys in block with digit d}. */
 int bsg_pr_count_digits(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round,
                         int radix_log2, uint64_t* counts, void* stream);
 
-/* radix.hpp:248-290 digit_starts + the routing part of sort_and_scatter,
+/* radix.hpp:137-179 digit_starts + the routing part of sort_and_scatter,
  * from the gathered count matrix counts[v*r + d] (p x r, device):
  *   send_counts[w] = #keys worker `me` sends to worker w,
  *   recv_counts[v] = #keys worker `me` receives from worker v,
@@ -193,7 +193,7 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
                 int radix_log2, uint64_t* send_counts, uint64_t* recv_counts,
                 int64_t* rebuild_delta, void* stream);
 
-/* radix.hpp:262-290 sort_and_scatter's local stable count-sort: sorted =
+/* radix.hpp:151-179 sort_and_scatter's local stable count-sort: sorted =
  * count_sort_round(block, round, radix).  Because global positions increase
  * along the digit-sorted block, the slice for worker w is the contiguous
  * range [sum(send_counts[<w]), +send_counts[w]) of `sorted` -- no per-key
@@ -207,7 +207,7 @@ int bsg_pr_local_sort(bsg_ctx* ctx, const uint32_t* block, uint32_t* sorted, uin
 int bsg_pr_plan_host(const uint64_t* counts, uint64_t n, int p, int me, int radix_log2,
                      uint64_t* send_counts, uint64_t* recv_counts, int64_t* rebuild_delta);
 
-/* radix.hpp:295-333 gather_slices: rebuilds the block from the source-major
+/* radix.hpp:184-222 gather_slices: rebuilds the block from the source-major
  * receive buffer (recv_len keys) by scattering each key to
  * rebuild_delta[src*r + digit] + index. */
 int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len,
@@ -221,8 +221,8 @@ int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len,
 int bsg_ctx_enable_peer_access(bsg_ctx* ctx, int* enabled);
 
 /* Fused exchange + rebuild over peer memory (NVLink): replaces the
- * all-to-all-v of sort_and_scatter (radix.hpp:275-290) and gather_slices
- * (radix.hpp:295-333) for one round of worker `me`.  `sorted` is me's block
+ * all-to-all-v of sort_and_scatter (radix.hpp:164-179) and gather_slices
+ * (radix.hpp:184-222) for one round of worker `me`.  `sorted` is me's block
  * after its local stable pass (bsg_pr_local_sort), `counts_all` the gathered
  * p x r digit-count matrix (device).  Every key is stored directly at its
  * position in the next-round block of its owner: peer_blocks[w] (host array
@@ -235,7 +235,7 @@ int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_t len,
                         void* stream);
 
 /* One whole PR round of worker `me` as ONE pass (r <= 2^8): the local stable
- * pass of sort_and_scatter (radix.hpp:262-270) writes every key of `block`
+ * pass of sort_and_scatter (radix.hpp:151-159) writes every key of `block`
  * (me's current block, len = size_of(me)) directly at its final position in
  * its owner's next-round block (peer_blocks as in bsg_pr_peer_scatter), i.e.
  * count_sort_round + all-to-all-v + gather_slices fused.  counts_all is the

@@ -129,17 +129,17 @@ inline bool verify_sorted_permutation(const KeyArray& input, const KeyArray& out
 
 namespace radix {
 
-inline constexpr Key digit_of(Key key, int round, int bits) { // radix.hpp:139-141
+inline constexpr Key digit_of(Key key, int round, int bits) { // radix.hpp:28-30
     return (key >> (round * bits)) & ((std::uint64_t{1} << bits) - 1);
 }
 
-inline int checked_digit_bits(std::uint64_t radix) { // radix.hpp:143-151
+inline int checked_digit_bits(std::uint64_t radix) { // radix.hpp:32-40
     const int b = bsg_checked_digit_bits(radix);
     if (b < 0) throw std::invalid_argument(bsg_last_error());
     return b;
 }
 
-inline KeyArray count_sort_round(const KeyArray& keys, int round, std::uint64_t radix) { // radix.hpp:155-176
+inline KeyArray count_sort_round(const KeyArray& keys, int round, std::uint64_t radix) { // radix.hpp:44-65
     const int bits = checked_digit_bits(radix);
     KeyArray out(keys.size());
     detail::check(bsg_count_sort_round_u32(detail::context(), keys.data(), out.data(), keys.size(), round, bits,
@@ -147,7 +147,7 @@ inline KeyArray count_sort_round(const KeyArray& keys, int round, std::uint64_t 
     return out;
 }
 
-inline KeyArray serial_radix_sort(KeyArray keys, std::uint64_t radix) { // radix.hpp:180-201
+inline KeyArray serial_radix_sort(KeyArray keys, std::uint64_t radix) { // radix.hpp:69-90
     const int bits = checked_digit_bits(radix);
     detail::check(bsg_radix_sort_u32(detail::context(), keys.data(), keys.data(), keys.size(), bits, BSG_MEM_HOST,
                                      nullptr));
@@ -155,7 +155,7 @@ inline KeyArray serial_radix_sort(KeyArray keys, std::uint64_t radix) { // radix
 }
 
 namespace detail {
-struct Partition { // radix.hpp:207-229
+struct Partition { // radix.hpp:96-118
     std::uint64_t n = 0;
     int p = 1;
     std::uint64_t small() const { return n / p; }
@@ -164,7 +164,7 @@ struct Partition { // radix.hpp:207-229
     std::uint64_t offset_of(int w) const { return bsg_partition_offset_of(n, p, w); }
     int owner_of(std::uint64_t pos) const { return bsg_partition_owner_of(n, p, pos); }
 };
-struct RadixPlan { // radix.hpp:231-236
+struct RadixPlan { // radix.hpp:120-125
     Partition part;
     std::uint64_t radix = 256;
     int bits = 8;
@@ -172,12 +172,12 @@ struct RadixPlan { // radix.hpp:231-236
 };
 } // namespace detail
 
-struct PreparedRadix { // radix.hpp:339-342 (input kept whole; blocks are its partition)
+struct PreparedRadix { // radix.hpp:228-231 (input kept whole; blocks are its partition)
     detail::RadixPlan plan;
     KeyArray keys;
 };
 
-inline PreparedRadix prepare_parallel_radix(const KeyArray& keys, int p, std::uint64_t radix) { // radix.hpp:344-360
+inline PreparedRadix prepare_parallel_radix(const KeyArray& keys, int p, std::uint64_t radix) { // radix.hpp:233-249
     if (p < 1) throw std::invalid_argument("parallel radix sort: p must be >= 1");
     const int bits = checked_digit_bits(radix);
     PreparedRadix prep;
@@ -189,12 +189,12 @@ inline PreparedRadix prepare_parallel_radix(const KeyArray& keys, int p, std::ui
     return prep;
 }
 
-struct ParallelSortResult { // radix.hpp:362-365
+struct ParallelSortResult { // radix.hpp:251-254
     KeyArray output;
     bsp::RunStats stats;
 };
 
-// radix.hpp:371-414; the executor flag is accepted, results are identical.
+// radix.hpp:260-303; the executor flag is accepted, results are identical.
 inline ParallelSortResult run_parallel_radix(PreparedRadix prep, bool use_sequential_executor = false) {
     (void)use_sequential_executor;
     const int all = key_bits / prep.plan.bits;
@@ -209,7 +209,7 @@ inline ParallelSortResult run_parallel_radix(PreparedRadix prep, bool use_sequen
     return res;
 }
 
-inline KeyArray parallel_radix_sort(const SortInstance& instance) { // radix.hpp:417-423
+inline KeyArray parallel_radix_sort(const SortInstance& instance) { // radix.hpp:306-312
     instance.validate();
     if (instance.algorithm != Algorithm::PR4 && instance.algorithm != Algorithm::PR2)
         throw std::invalid_argument("parallel_radix_sort handles pr4 and pr2 only");

@@ -13,7 +13,7 @@
  * radix_test.cpp:142-151, merge_split KATs netsort_test.cpp:52-82, the
  * reverse-block OET KAT netsort_test.cpp:211-215) -- see
  * tests/test_oracle_golden.py -- and (2) the reference's own headers compiled
- * into oracle/_ref/libbspref.so by oracle/Makefile (tests/test_oracle_vs_ref.py).
+ * into oracle/_ref/libbspref.so by oracle/Makefile (checked against it by tests/test_oracle_golden.py::test_oracle_vs_reference_live).
  *
  * Plain C99, single-threaded, no allocation hidden from the caller except
  * where noted (scratch via malloc, freed before return).
@@ -84,7 +84,7 @@ uint64_t orc_derive_seed(uint64_t seed, int rep) {
     return orc_splitmix64(seed ^ orc_splitmix64((uint64_t)(int64_t)rep));
 }
 
-/* core.hpp:60-64 digit_bits + radix.hpp:143-151 checked_digit_bits:        */
+/* core.hpp:60-64 digit_bits + radix.hpp:32-40 checked_digit_bits:        */
 /* returns lg r, or -1 if r is not a power of two whose width divides 32,  */
 /* or -2 if lg r > 16.                                                      */
 int orc_checked_digit_bits(uint64_t radix) {
@@ -96,12 +96,12 @@ int orc_checked_digit_bits(uint64_t radix) {
     return b;
 }
 
-/* radix.hpp:139-141 digit_of */
+/* radix.hpp:28-30 digit_of */
 static inline uint32_t orc_digit_of(uint32_t key, int round, int bits) {
     return (uint32_t)(((uint64_t)key >> (round * bits)) & ((1ULL << bits) - 1));
 }
 
-/* radix.hpp:155-176 count_sort_round: histogram, exclusive scan, forward   */
+/* radix.hpp:44-65 count_sort_round: histogram, exclusive scan, forward   */
 /* stable scatter.                                                          */
 int orc_count_sort_round(const uint32_t* keys, uint64_t n, int round, uint64_t radix, uint32_t* out) {
     const int bits = orc_checked_digit_bits(radix);
@@ -121,7 +121,7 @@ int orc_count_sort_round(const uint32_t* keys, uint64_t n, int round, uint64_t r
     return ORC_OK;
 }
 
-/* radix.hpp:180-201 serial_radix_sort: 32/lg r rounds with ping-pong.     */
+/* radix.hpp:69-90 serial_radix_sort: 32/lg r rounds with ping-pong.     */
 /* `out` receives the sorted keys; `in` is not modified.                    */
 int orc_serial_radix_sort(const uint32_t* in, uint64_t n, uint64_t radix, uint32_t* out) {
     const int bits = orc_checked_digit_bits(radix);
@@ -154,7 +154,7 @@ int orc_serial_radix_sort(const uint32_t* in, uint64_t n, uint64_t radix, uint32
 }
 
 /* ---------------------------------------------------------------------- */
-/* radix.hpp:207-229 detail::Partition (balanced contiguous cut)           */
+/* radix.hpp:96-118 detail::Partition (balanced contiguous cut)           */
 /* ---------------------------------------------------------------------- */
 uint64_t orc_part_size_of(uint64_t n, int p, int w) {
     return n / (uint64_t)p + ((uint64_t)w < n % (uint64_t)p ? 1 : 0);
@@ -175,15 +175,15 @@ typedef struct {
     uint64_t messages_sent, messages_delivered, words_sent, words_delivered;
 } orc_run_stats;
 
-/* radix.hpp:344-414 prepare_parallel_radix + run_parallel_radix, with      */
+/* radix.hpp:233-303 prepare_parallel_radix + run_parallel_radix, with      */
 /* plan.rounds overridable (rounds_limit < 0 => all 32/lg r rounds), the   */
 /* per-round oracle of SURVEY §8(c).  Restates the BSP program directly:   */
-/* per round every worker counts its digits (radix.hpp:238-243) and sends  */
-/* the count block to all p workers (radix.hpp:386-388); then sorts its   */
+/* per round every worker counts its digits (radix.hpp:127-132) and sends  */
+/* the count block to all p workers (radix.hpp:275-277); then sorts its   */
 /* block with count_sort_round, routes each key to owner_of(next_pos)      */
-/* (radix.hpp:262-290); the owner rebuilds its block by walking (digit,    */
-/* source) and clipping (radix.hpp:295-333).  Output = concatenation of   */
-/* final blocks in worker order (radix.hpp:408-413).  Stats follow          */
+/* (radix.hpp:151-179); the owner rebuilds its block by walking (digit,    */
+/* source) and clipping (radix.hpp:184-222).  Output = concatenation of   */
+/* final blocks in worker order (radix.hpp:297-302).  Stats follow          */
 /* bsp.hpp:50-58,139-148 (words = payload sizes).                          */
 int orc_parallel_radix(const uint32_t* in, uint64_t n, int p, uint64_t radix, int rounds_limit,
                        uint32_t* out, orc_run_stats* stats) {
@@ -219,7 +219,7 @@ int orc_parallel_radix(const uint32_t* in, uint64_t n, int p, uint64_t radix, in
     orc_run_stats st = {0, 0, 0, 0, 0};
 
     for (int round = 0; round < rounds; ++round) {
-        /* superstep 2*round: count_digits + send to all (radix.hpp:386-388) */
+        /* superstep 2*round: count_digits + send to all (radix.hpp:275-277) */
         memset(counts, 0, (size_t)p * radix * sizeof(uint64_t));
         for (int w = 0; w < p; ++w) {
             uint64_t sz = orc_part_size_of(n, p, w);
@@ -227,13 +227,13 @@ int orc_parallel_radix(const uint32_t* in, uint64_t n, int p, uint64_t radix, in
         }
         st.messages_sent += (uint64_t)p * p;
         st.words_sent += (uint64_t)p * p * radix;
-        /* digit_starts (radix.hpp:248-256) */
+        /* digit_starts (radix.hpp:137-145) */
         memset(starts, 0, (radix + 1) * sizeof(uint64_t));
         for (int v = 0; v < p; ++v)
             for (uint64_t d = 0; d < radix; ++d) starts[d + 1] += counts[(uint64_t)v * radix + d];
         for (uint64_t d = 0; d < radix; ++d) starts[d + 1] += starts[d];
 
-        /* superstep 2*round+1: sort_and_scatter (radix.hpp:262-290) */
+        /* superstep 2*round+1: sort_and_scatter (radix.hpp:151-179) */
         for (int w = 0; w < p; ++w) {
             uint64_t sz = orc_part_size_of(n, p, w);
             rc = orc_count_sort_round(blocks[w], sz, round, radix, routed[w]);
@@ -267,7 +267,7 @@ int orc_parallel_radix(const uint32_t* in, uint64_t n, int p, uint64_t radix, in
                 st.words_sent += sz - run_begin;
             }
         }
-        /* superstep 2*round+2 (first half): gather_slices (radix.hpp:295-333) */
+        /* superstep 2*round+2 (first half): gather_slices (radix.hpp:184-222) */
         for (int w = 0; w < p; ++w) {
             const uint64_t lo = orc_part_offset_of(n, p, w);
             const uint64_t hi = lo + orc_part_size_of(n, p, w);

@@ -40,7 +40,7 @@ uint64_t bsg_derive_seed(uint64_t seed, int32_t rep) {
     return splitmix64(seed ^ splitmix64(static_cast<uint64_t>(static_cast<int64_t>(rep))));
 }
 
-// core.hpp:60-64 + radix.hpp:143-151
+// core.hpp:60-64 + radix.hpp:32-40
 int bsg_checked_digit_bits(uint64_t radix) {
     if (radix == 0 || (radix & (radix - 1)) != 0) {
         bsg::set_error("radix must be a power of two whose bit width divides 32");
@@ -100,7 +100,7 @@ int bsg_network_schedule(int network, int p, int32_t* partner, int32_t* keep_low
     return bsg::fail(BSG_EINVAL, "unknown network " + std::to_string(network));
 }
 
-// radix.hpp:207-229
+// radix.hpp:96-118
 uint64_t bsg_partition_size_of(uint64_t n, int p, int w) {
     return n / static_cast<uint64_t>(p) + (static_cast<uint64_t>(w) < n % static_cast<uint64_t>(p) ? 1 : 0);
 }

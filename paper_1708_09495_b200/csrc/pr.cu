@@ -1,17 +1,17 @@
 // pr.cu -- parallel LSD radix sort (PR4 at r = 2^8, PR2 at r = 2^16).
 //
-// Restates one BSP round of run_parallel_radix (radix.hpp:371-414) per
+// Restates one BSP round of run_parallel_radix (radix.hpp:260-303) per
 // worker as device steps, so no per-key owner_of() division and no per-slice
 // vector copies are needed:
-//   count   -- count_digits (radix.hpp:238-243): digit histogram of the block.
+//   count   -- count_digits (radix.hpp:127-132): digit histogram of the block.
 //   plan    -- digit_starts + the routing of sort_and_scatter
-//              (radix.hpp:248-290): from the p x r count matrix compute, per
+//              (radix.hpp:137-179): from the p x r count matrix compute, per
 //              worker, how many keys go to / come from each worker and, for the
 //              rebuild, where the keys of (source v, digit d) land.  Because
 //              global positions increase along a digit-sorted block, every
 //              slice is a contiguous range, found from counts alone.
 //   local   -- the stable local pass of sort_and_scatter (count_sort_round).
-//   rebuild -- gather_slices (radix.hpp:295-333): walking (digit, source) in
+//   rebuild -- gather_slices (radix.hpp:184-222): walking (digit, source) in
 //              order is a stable digit scatter of the source-major receive
 //              buffer, block[delta[v][d] + j] = recv[j].
 // In-process (p logical workers on one GPU, run_parallel_radix_local) the
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kHist16Threads)
 // The rebuild of every worker together is one scatter of the locally sorted
 // blocks: key i of worker v's sorted block with digit d lands at
 //   np(v,d) + (i - ls(v,d)),  np(v,d) = start[d] + sum_{u<v} cnt(u,d)
-// (radix.hpp:257-290 next_pos / gather order), ls(v,d) = first index of d in
+// (radix.hpp:146-179 next_pos / gather order), ls(v,d) = first index of d in
 // v's sorted block.  All tables are O(p r) work.
 
 // ls(v,d) for d in [0, r]: lower bound of digit d in v's sorted block (the
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kScatterThreads)
 }
 
 // BSP accounting only (RunStats): send[v][w] = keys of worker v's block that
-// land in worker w's partition (the slices of radix.hpp:276-289).
+// land in worker w's partition (the slices of radix.hpp:165-178).
 constexpr int kSendThreads = 256;
 __global__ void __launch_bounds__(kSendThreads)
     pr_send_counts_kernel(const uint64_t* __restrict__ starts, const uint64_t* __restrict__ start,
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kSendThreads)
 //   scan: dstart[d] = exclusive scan of coltot (digit_starts)
 //   row:  one CTA per source v: ls(v,d) = row prefix of cnt(v,.), np(v,d) =
 //         dstart[d] + before(v,d); recv/split overlaps with me's partition;
-//         send slices of me (radix.hpp:276-289); delta[v][d] = np - ls.
+//         send slices of me (radix.hpp:165-178); delta[v][d] = np - ls.
 //   adj:  pr_plan2_kernel rebases delta onto me's receive buffer.
 __global__ void __launch_bounds__(kDigChunk)
     pr_plan_col_kernel(const uint64_t* __restrict__ counts, int p, int radix, int64_t* __restrict__ delta,
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kDigChunk)
 
 // ---- fused exchange + rebuild over peer memory (bsg_pr_peer_scatter) -----
 // gd[d] = digit_start[d] + sum_{u<me} cnt(u,d) - ls(me,d): the destination of
-// key i (digit d) of me's sorted block is gd[d] + i (radix.hpp:257-290).
+// key i (digit d) of me's sorted block is gd[d] + i (radix.hpp:146-179).
 // `before` holds sum_{u<me} cnt(u,d) (pr_plan_col_kernel's delta row me).
 __global__ void __launch_bounds__(kDigChunk)
     pr_peer_gd_kernel(const uint64_t* __restrict__ cnt_me, const int64_t* __restrict__ before,
@@ -640,7 +640,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         const int shift = round * bits;
         uint64_t* counts = starts; // [p][radix]
         int64_t* base = gd;        // [p][radix]
-        // count_digits of every worker (radix.hpp:238-243), one launch
+        // count_digits of every worker (radix.hpp:127-132), one launch
         if (!add(launch_pr_seg_count(cur, n, p, bits, shift, counts, stream)))
             return cuda_fail(cudaGetLastError(), "pr count");
         {

@@ -10,18 +10,18 @@ struct bsg_ctx;
 
 namespace bsg {
 
-// count_digits (radix.hpp:238-243) into uint64 counts[radix].
+// count_digits (radix.hpp:127-132) into uint64 counts[radix].
 int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int bits, uint64_t* counts,
                     cudaStream_t stream);
 
-// Routing plan of worker `me` from the p x r count matrix (radix.hpp:248-290).
+// Routing plan of worker `me` from the p x r count matrix (radix.hpp:137-179).
 // scratch: p(1 + c) + 2r + c uint64 words of device workspace, c = ceil(r /
 // 1024) (split = the index in each source's sorted block where the slice for
 // `me` begins, column totals, digit starts, chunk sums).
 int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, uint64_t* send_counts,
                    uint64_t* recv_counts, int64_t* rebuild_delta, cudaStream_t stream, uint64_t* scratch);
 
-// gather_slices (radix.hpp:295-333) as a stable scatter of the source-major
+// gather_slices (radix.hpp:184-222) as a stable scatter of the source-major
 // receive buffer: block[delta[src][digit] + j] = recv[j].
 int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shift, const int64_t* rebuild_delta,
                       uint32_t* block, cudaStream_t stream, const uint64_t* recv_counts, int p);

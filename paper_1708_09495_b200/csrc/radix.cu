@@ -1,7 +1,7 @@
 // radix.cu -- stable LSD radix sort of uint32 keys for sm_100a.
 //
-// Restates the count-sort round of radix.hpp:155-176 (histogram, exclusive
-// scan, stable forward scatter) and serial_radix_sort (radix.hpp:180-201) as
+// Restates the count-sort round of radix.hpp:44-65 (histogram, exclusive
+// scan, stable forward scatter) and serial_radix_sort (radix.hpp:69-90) as
 // three kernels:
 //   K1 hist_kernel      -- one read of the keys, per-CTA shared-memory
 //                          histograms of every digit with per-thread run-length

@@ -1,16 +1,16 @@
 """Multi-GPU parallel radix sort (PR4 at r = 2^8, PR2 at r = 2^16): one
 process per GPU, the reference's BSP supersteps re-expressed over NCCL.
 
-Reference: run_parallel_radix (radix.hpp:371-414).  Per round, on every rank:
+Reference: run_parallel_radix (radix.hpp:260-303).  Per round, on every rank:
 
-  superstep 2k     count_digits(block) (radix.hpp:238-243)          -> kernel
-                   send the r counts to every worker (radix.hpp:386-388)
+  superstep 2k     count_digits(block) (radix.hpp:127-132)          -> kernel
+                   send the r counts to every worker (radix.hpp:275-277)
                                                   -> NCCL all_gather (p x r)
-  superstep 2k+1   sort_and_scatter (radix.hpp:262-290): local stable pass
+  superstep 2k+1   sort_and_scatter (radix.hpp:151-179): local stable pass
                    -> kernel; the routing plan from the count matrix
                    -> kernel; contiguous slices to their owners
                                                   -> NCCL all_to_all_v
-  superstep 2k+2   gather_slices (radix.hpp:295-333) -> rebuild kernel
+  superstep 2k+2   gather_slices (radix.hpp:184-222) -> rebuild kernel
 
 The block a rank holds after round k is bit-identical to worker `rank`'s
 block in run_parallel_radix with plan.rounds = k.  The only host round trip
@@ -169,7 +169,7 @@ def _is_nccl(group) -> bool:
 
 
 def _all_gather_counts(counts: torch.Tensor, p: int, group) -> torch.Tensor:
-    """The count exchange of radix.hpp:386-388 as one all-gather (device
+    """The count exchange of radix.hpp:275-277 as one all-gather (device
     buffers with NCCL; host-staged with other backends)."""
     if _is_nccl(group) or not counts.is_cuda:
         out = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
@@ -185,7 +185,7 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
                         group=None, ops=None, a2a_events: Optional[list] = None, exchange: str = "nccl",
                         peer: Optional[PeerBlocks] = None) -> torch.Tensor:
     """Sorts the globally block-distributed array (rank w holds the keys at
-    Partition(n_total, p).offset_of(w) .. +size_of(w), radix.hpp:207-229).
+    Partition(n_total, p).offset_of(w) .. +size_of(w), radix.hpp:96-118).
     Returns this rank's block of the sorted array (int32 bit patterns of the
     uint32 keys).  `rounds` < 32/lg r stops early (plan.rounds override).
     If `a2a_events` is a list, CUDA event pairs around each all-to-all are

@@ -20,12 +20,12 @@ from .core import Algorithm, SortInstance, key_bits
 
 
 def digit_of(key: int, round: int, bits: int) -> int:
-    """radix.hpp:139-141: digit of `key` in `round`, low digits first."""
+    """radix.hpp:28-30: digit of `key` in `round`, low digits first."""
     return (int(key) >> (round * bits)) & ((1 << bits) - 1)
 
 
 def checked_digit_bits(radix: int) -> int:
-    """radix.hpp:143-151: lg r for r in {2,4,16,256,65536}, else ValueError."""
+    """radix.hpp:32-40: lg r for r in {2,4,16,256,65536}, else ValueError."""
     b = _lib.lib().bsg_checked_digit_bits(int(radix) & (2**64 - 1))
     if b < 0:
         raise ValueError(_lib.last_error())
@@ -33,7 +33,7 @@ def checked_digit_bits(radix: int) -> int:
 
 
 def count_sort_round(keys, round: int, radix: int):
-    """radix.hpp:155-176: one stable bucket pass over digit `round`."""
+    """radix.hpp:44-65: one stable bucket pass over digit `round`."""
     bits = checked_digit_bits(radix)
     if round < 0 or round >= key_bits // bits:
         raise ValueError(f"round {round} outside [0, {key_bits // bits})")
@@ -46,7 +46,7 @@ def count_sort_round(keys, round: int, radix: int):
 
 
 def serial_radix_sort(keys, radix: int):
-    """radix.hpp:180-201: 32/lg r stable rounds, low digit first (SR4 = r 256)."""
+    """radix.hpp:69-90: 32/lg r stable rounds, low digit first (SR4 = r 256)."""
     bits = checked_digit_bits(radix)
     kb = KeyBuf(keys)
     out = kb.empty(kb.n)
@@ -58,7 +58,7 @@ def serial_radix_sort(keys, radix: int):
 
 @dataclass
 class Partition:
-    """radix.hpp:207-229 detail::Partition: balanced contiguous cut."""
+    """radix.hpp:96-118 detail::Partition: balanced contiguous cut."""
 
     n: int = 0
     p: int = 1
@@ -81,7 +81,7 @@ class Partition:
 
 @dataclass
 class RadixPlan:
-    """radix.hpp:231-236 detail::RadixPlan."""
+    """radix.hpp:120-125 detail::RadixPlan."""
 
     part: Partition = field(default_factory=Partition)
     radix: int = 256
@@ -91,7 +91,7 @@ class RadixPlan:
 
 @dataclass
 class PreparedRadix:
-    """radix.hpp:339-342.  `keys` holds the input; `blocks` are the per-worker
+    """radix.hpp:228-231.  `keys` holds the input; `blocks` are the per-worker
     views of the balanced partition.  Setting ``plan.rounds = k`` before
     :func:`run_parallel_radix` stops after k rounds, as in the reference."""
 
@@ -106,14 +106,14 @@ class PreparedRadix:
 
 @dataclass
 class ParallelSortResult:
-    """radix.hpp:362-365 (RunStats as a dict with the bsp.hpp:86-92 fields)."""
+    """radix.hpp:251-254 (RunStats as a dict with the bsp.hpp:86-92 fields)."""
 
     output: object
     stats: dict
 
 
 def prepare_parallel_radix(keys, p: int, radix: int) -> PreparedRadix:
-    """radix.hpp:344-360."""
+    """radix.hpp:233-249."""
     if p < 1:
         raise ValueError("parallel radix sort: p must be >= 1")
     bits = checked_digit_bits(radix)
@@ -123,7 +123,7 @@ def prepare_parallel_radix(keys, p: int, radix: int) -> PreparedRadix:
 
 
 def run_parallel_radix(prep: PreparedRadix, use_sequential_executor: bool = False) -> ParallelSortResult:
-    """radix.hpp:371-414: PR with p logical workers on the GPU.  The executor
+    """radix.hpp:260-303: PR with p logical workers on the GPU.  The executor
     flag is accepted for signature parity; results are identical either way."""
     del use_sequential_executor
     plan = prep.plan
@@ -140,7 +140,7 @@ def run_parallel_radix(prep: PreparedRadix, use_sequential_executor: bool = Fals
 
 
 def parallel_radix_sort(instance: SortInstance):
-    """radix.hpp:417-423: PR4 / PR2 entry point."""
+    """radix.hpp:306-312: PR4 / PR2 entry point."""
     instance.validate()
     if instance.algorithm not in (Algorithm.PR4, Algorithm.PR2):
         raise ValueError("parallel_radix_sort handles pr4 and pr2 only")
@@ -149,7 +149,7 @@ def parallel_radix_sort(instance: SortInstance):
 
 
 def digit_counts(block, round: int, radix: int):
-    """radix.hpp:238-243 count_digits on a device block -> uint64 counts (torch)."""
+    """radix.hpp:127-132 count_digits on a device block -> uint64 counts (torch)."""
     import torch
 
     bits = checked_digit_bits(radix)

@@ -7,9 +7,9 @@ exists); the committed .npz travels to the GPU box.
 
 Contents (key -> uint32/int64 array):
   draws/42/6                 generate_uniform_keys(6, 42)        (core_test.cpp:24-31)
-  csr/<radix>/<round>/<case> count_sort_round outputs           (radix.hpp:155-176)
-  srs/<radix>/<case>         serial_radix_sort outputs          (radix.hpp:180-201)
-  pr/<radix>/<p>/<k>         run_parallel_radix with plan.rounds=k (radix.hpp:371-414)
+  csr/<radix>/<round>/<case> count_sort_round outputs           (radix.hpp:44-65)
+  srs/<radix>/<case>         serial_radix_sort outputs          (radix.hpp:69-90)
+  pr/<radix>/<p>/<k>         run_parallel_radix with plan.rounds=k (radix.hpp:260-303)
   prstats/<radix>/<p>/<k>    its RunStats (supersteps, msgs, words x2)
   net/<btn|oet>/<p>/<s>      run_block_network with stages[:s]   (netsort.hpp:157-199)
   netstats/<btn|oet>/<p>/<s> its RunStats

@@ -145,7 +145,7 @@ def test_large_blocks_per_round(cuda, bsg, orc, p):
 def test_peer_scatter_logical_workers(cuda, bsg, orc, p):
     """bsg_pr_peer_scatter with p logical workers in one process (all
     next-round blocks local): every round's concatenated blocks equal
-    run_parallel_radix with plan.rounds = k (radix.hpp:371-414)."""
+    run_parallel_radix with plan.rounds = k (radix.hpp:260-303)."""
     torch = cuda
     import ctypes
     from paper_1708_09495_b200 import distributed as D
@@ -224,7 +224,7 @@ def test_large_segments_wide_rows(cuda, bsg, radix_log2):
     """Worker blocks above 2^29 keys (p = 2, n = 2^31 + 12345): the segmented
     one-sweep runs its 64-bit status/position rows.  After one round the
     concatenated blocks equal one count_sort_round of the whole array
-    (radix.hpp:371-414 with plan.rounds = 1), and the full run equals the
+    (radix.hpp:260-303 with plan.rounds = 1), and the full run equals the
     serial sort; both compared on the device chunk by chunk."""
     torch = cuda
     n, p = (1 << 31) + 12345, 2
@@ -261,7 +261,7 @@ def test_fused_round_large_blocks(cuda, bsg):
     keys on each GPU): the 64-bit one-sweep rows store into the owners'
     blocks.  Two logical workers in one process; one round on the input
     equals one count_sort_round of the whole array (a PR round is a stable
-    count sort of the block concatenation, radix.hpp:371-414)."""
+    count sort of the block concatenation, radix.hpp:260-303)."""
     torch = cuda
     from paper_1708_09495_b200 import distributed as D
 
