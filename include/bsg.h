@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BSG_ABI_VERSION 1
+#define BSG_ABI_VERSION 2
 
 enum bsg_status {
     BSG_OK = 0,
@@ -49,7 +49,7 @@ enum bsg_status {
     BSG_EPROTO = 2, /* protocol / consistency failure (reference: bsp::bsp_error) */
     BSG_ECUDA = 3,  /* CUDA runtime error or no GPU */
     BSG_ENOMEM = 4, /* device or host allocation failed */
-    BSG_ENCCL = 5   /* reserved for in-library collectives */
+    BSG_ENCCL = 5   /* NCCL failure (group contexts, BSG_PR_NCCL) */
 };
 
 enum bsg_mem_kind { BSG_MEM_HOST = 0, BSG_MEM_DEVICE = 1 };
@@ -160,8 +160,11 @@ int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in,
  * stable local pass, slice routing and the rebuild, all as kernels.
  * rounds_limit >= 0 stops after that many rounds (the reference's
  * plan.rounds override) -- the concatenated per-worker blocks are then the
- * intermediate state.  Multi-GPU (one process per GPU) runs the same steps
- * through paper_1708_09495_b200.distributed over NCCL. */
+ * intermediate state.  On a group context (bsg_ctx_create_group) the
+ * workers are spread over the group's GPUs (BSG_PR_PEER rounds); in/out are
+ * then host pointers (BSG_MEM_HOST) or device pointers on member 0's GPU.
+ * Multi-GPU with one process per GPU runs the same steps through
+ * paper_1708_09495_b200.distributed over torch.distributed / NCCL. */
 int bsg_parallel_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
                                 int p, int radix_log2, int rounds_limit, bsg_run_stats* stats,
                                 int mem_kind, void* stream);
@@ -248,6 +251,53 @@ int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t len,
                        const uint64_t* counts_all, uint64_t n, int p, int me,
                        int round, int radix_log2, uint32_t* const* peer_blocks,
                        void* stream);
+
+/* ---- multi-GPU parallel radix sort in ONE process ----
+ * The reference runs run_parallel_radix's p workers as threads of one
+ * process (radix.hpp:260-303, bsp.hpp:211-315); here a GROUP context spreads
+ * the p logical workers over G GPUs of one node: member g (devices[g]) owns
+ * the contiguous worker group Partition(p, G) block g, i.e. the key range
+ * [bsg_group_range_offset(n,p,G,g), + bsg_group_range_size(n,p,G,g)).
+ * Every round is the reference's round: digit counts per worker, the p x r
+ * count matrix exchanged between members, then
+ *   BSG_PR_PEER: ONE segmented one-sweep pass per member whose write-out
+ *     stores every key at its global position in the owning member's
+ *     next-round buffer over NVLink (peer access; count_sort_round +
+ *     all-to-all-v + gather_slices fused), a cross-GPU event barrier per round;
+ *   BSG_PR_NCCL: the stable local pass, an NCCL all-to-all-v of the
+ *     contiguous slices (ncclSend/ncclRecv in one group, communicators from
+ *     ncclCommInitAll owned by the context) and the rebuild; needs p == G.
+ * Per-round states are bit-identical to run_parallel_radix with
+ * plan.rounds = rounds_limit.  devices may repeat (several members on one
+ * GPU: the same code path with local "peer" stores; NCCL needs distinct
+ * devices). */
+#define BSG_PR_PEER 0
+#define BSG_PR_NCCL 1
+int bsg_ctx_create_group(const int* devices, int ndevices, bsg_ctx** out);
+/* members of a group context (1 for a single-device context) */
+int bsg_ctx_group_size(const bsg_ctx* ctx);
+/* the device of member g */
+int bsg_ctx_group_device(const bsg_ctx* ctx, int member);
+uint64_t bsg_group_range_offset(uint64_t n, int p, int G, int g);
+uint64_t bsg_group_range_size(uint64_t n, int p, int G, int g);
+
+/* Per-phase device time of one group sort, max over members (ms). */
+typedef struct bsg_pr_timing {
+    double total_ms;    /* the whole call (first kernel to last event) */
+    double count_ms;    /* digit counts + count-matrix exchange */
+    double exchange_ms; /* NCCL: the all-to-all-v; PEER: the fused pass (local pass + NVLink stores) */
+    double local_ms;    /* NCCL: local stable pass + rebuild; PEER: 0 (inside the fused pass) */
+    uint64_t remote_bytes; /* key bytes moved to another member, all rounds (from the count matrices) */
+} bsg_pr_timing;
+
+/* blocks[g]: device pointer on member g holding its key range (in/out, sorted
+ * in place).  streams[g] (optional, cudaStream_t): work already queued there
+ * (e.g. what produced blocks[g]) is ordered before the sort; NULL = every
+ * member device is synchronised first.  Synchronous: returns when every
+ * member is done.  stats / timing optional. */
+int bsg_pr_group_sort_u32(bsg_ctx* group, uint32_t* const* blocks, uint64_t n, int p, int radix_log2,
+                          int rounds_limit, int variant, bsg_run_stats* stats, bsg_pr_timing* timing,
+                          void* const* streams);
 
 /* core.hpp:93-99 generate_uniform_keys on the GPU: the same n keys,
  * bit-identical, written to device memory (`out`) on `stream`.  Segments of

@@ -48,6 +48,23 @@ class RunStats(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class PrTiming(ctypes.Structure):
+    """bsg_pr_timing: per-phase device time of one group sort (ms, max over members)."""
+
+    _fields_ = [
+        ("total_ms", ctypes.c_double),
+        ("count_ms", ctypes.c_double),
+        ("exchange_ms", ctypes.c_double),
+        ("local_ms", ctypes.c_double),
+        ("remote_bytes", ctypes.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+PR_PEER, PR_NCCL = 0, 1
+
 _u32p = ctypes.c_void_p
 _vp = ctypes.c_void_p
 _u64 = ctypes.c_uint64
@@ -89,6 +106,14 @@ SIGNATURES = {
     "bsg_ctx_enable_peer_access": (_i, [_vp, ctypes.POINTER(_i)]),
     "bsg_pr_peer_scatter": (_i, [_vp, _u32p, _u64, _vp, _u64, _i, _i, _i, _i, ctypes.POINTER(_vp), _vp]),
     "bsg_pr_fused_round": (_i, [_vp, _u32p, _u64, _vp, _u64, _i, _i, _i, _i, ctypes.POINTER(_vp), _vp]),
+    "bsg_ctx_create_group": (_i, [ctypes.POINTER(_i), _i, ctypes.POINTER(_vp)]),
+    "bsg_ctx_group_size": (_i, [_vp]),
+    "bsg_ctx_group_device": (_i, [_vp, _i]),
+    "bsg_group_range_offset": (ctypes.c_uint64, [_u64, _i, _i, _i]),
+    "bsg_group_range_size": (ctypes.c_uint64, [_u64, _i, _i, _i]),
+    "bsg_pr_group_sort_u32": (
+        _i, [_vp, ctypes.POINTER(_vp), _u64, _i, _i, _i, _i, ctypes.POINTER(RunStats), ctypes.POINTER(PrTiming),
+             ctypes.POINTER(_vp)]),
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -171,6 +196,23 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class GroupContext(Context):
+    """A multi-GPU group context (bsg_ctx_create_group): p logical workers of
+    the parallel radix sort spread over `devices` (may repeat a device)."""
+
+    def __init__(self, devices):
+        devs = (_i * len(devices))(*[int(d) for d in devices])
+        h = _vp()
+        check(lib().bsg_ctx_create_group(devs, len(devices), ctypes.byref(h)), "bsg_ctx_create_group")
+        self.handle = h
+        self.device = int(devices[0])
+        self.devices = [int(d) for d in devices]
+
+    @property
+    def size(self) -> int:
+        return int(lib().bsg_ctx_group_size(self.handle))
 
 
 _contexts: dict = {}

@@ -100,6 +100,50 @@ int radix_bits_or_fail(int radix_log2) {
     return BSG_OK;
 }
 
+// bsg_parallel_radix_sort_u32 on a group context: the member ranges are
+// staged from host memory (BSG_MEM_HOST) or from device memory on member 0's
+// GPU (BSG_MEM_DEVICE, peer copies), sorted by the group (BSG_PR_PEER rounds,
+// or NCCL when the members lack peer access and p equals the group size),
+// and copied back.  Synchronous.
+int parallel_radix_sort_group(bsg_ctx* grp, const uint32_t* in, uint32_t* out, uint64_t n, int p, int bits,
+                              int rounds, bsg_run_stats* stats, int mem_kind, cudaStream_t caller) {
+    if (mem_kind != BSG_MEM_HOST && mem_kind != BSG_MEM_DEVICE)
+        return fail(BSG_EINVAL, "mem_kind must be BSG_MEM_HOST or BSG_MEM_DEVICE");
+    std::lock_guard<std::mutex> lock(grp->mu);
+    const int G = static_cast<int>(grp->members.size());
+    std::vector<uint32_t*> blocks(G);
+    cudaError_t e;
+    if (mem_kind == BSG_MEM_DEVICE) { // caller's work on `in` happens before the staging copies
+        DeviceGuard dg(grp->device);
+        if ((e = cudaStreamSynchronize(caller)) != cudaSuccess) return cuda_fail(e, "group staging");
+    }
+    for (int g = 0; g < G; ++g) {
+        bsg_ctx* m = grp->members[g];
+        DeviceGuard dg(m->device);
+        const uint64_t off = group_range_offset(n, p, G, g), len = group_range_offset(n, p, G, g + 1) - off;
+        if ((e = m->grp_cur.ensure(std::max<uint64_t>(len, 4) * 4)) != cudaSuccess) return cuda_fail(e, "group staging");
+        blocks[g] = m->grp_cur.as<uint32_t>();
+        if (len && (e = cudaMemcpyAsync(blocks[g], in + off, len * 4, cudaMemcpyDefault, grp->member_streams[g])) !=
+                       cudaSuccess)
+            return cuda_fail(e, "group staging");
+    }
+    const int variant = grp->peer_ok || p != G ? BSG_PR_PEER : BSG_PR_NCCL;
+    if (int rc = run_parallel_radix_group(grp, blocks.data(), n, p, bits, rounds, variant, stats, nullptr)) return rc;
+    for (int g = 0; g < G; ++g) {
+        bsg_ctx* m = grp->members[g];
+        DeviceGuard dg(m->device);
+        const uint64_t off = group_range_offset(n, p, G, g), len = group_range_offset(n, p, G, g + 1) - off;
+        if (len && (e = cudaMemcpyAsync(out + off, blocks[g], len * 4, cudaMemcpyDefault, grp->member_streams[g])) !=
+                       cudaSuccess)
+            return cuda_fail(e, "group copy out");
+    }
+    for (int g = 0; g < G; ++g) {
+        DeviceGuard dg(grp->members[g]->device);
+        if ((e = cudaStreamSynchronize(grp->member_streams[g])) != cudaSuccess) return cuda_fail(e, "group copy out");
+    }
+    return BSG_OK;
+}
+
 } // namespace
 
 extern "C" {
@@ -129,6 +173,18 @@ int bsg_ctx_create(int device, bsg_ctx** out) {
 
 int bsg_ctx_destroy(bsg_ctx* ctx) {
     if (!ctx) return BSG_OK;
+    if (!ctx->members.empty()) {
+        destroy_group_nccl(ctx);
+        for (size_t g = 0; g < ctx->members.size(); ++g) {
+            DeviceGuard dg(ctx->members[g]->device);
+            if (ctx->member_streams[g]) cudaStreamDestroy(ctx->member_streams[g]);
+            for (DevBuf* b : {&ctx->members[g]->grp_cur, &ctx->members[g]->grp_nxt, &ctx->members[g]->grp_recv})
+                b->release();
+        }
+        for (bsg_ctx* m : ctx->members) bsg_ctx_destroy(m);
+        ctx->members.clear();
+        ctx->member_streams.clear();
+    }
     {
         CallGuard g(ctx);
         for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
@@ -139,6 +195,64 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
     }
     delete ctx;
     return BSG_OK;
+}
+
+int bsg_ctx_create_group(const int* devices, int ndevices, bsg_ctx** out) {
+    if (!out) return fail(BSG_EINVAL, "null output pointer");
+    *out = nullptr;
+    if (!devices || ndevices < 1 || ndevices > kPeerMax) return fail(BSG_EINVAL, "group: 1..64 member devices");
+    bsg_ctx* grp = nullptr;
+    if (int rc = bsg_ctx_create(devices[0], &grp)) return rc;
+    for (int g = 0; g < ndevices; ++g) {
+        bsg_ctx* m = nullptr;
+        int rc = bsg_ctx_create(devices[g], &m);
+        cudaStream_t s = nullptr;
+        if (rc == BSG_OK) {
+            DeviceGuard dg(devices[g]);
+            cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+            if (e != cudaSuccess) rc = cuda_fail(e, "group stream");
+        }
+        if (rc != BSG_OK) {
+            if (m) bsg_ctx_destroy(m);
+            bsg_ctx_destroy(grp);
+            return rc;
+        }
+        grp->members.push_back(m);
+        grp->member_streams.push_back(s);
+    }
+    // NVLink peer access between every pair of distinct member devices
+    for (int a = 0; a < ndevices && grp->peer_ok; ++a)
+        for (int b = 0; b < ndevices; ++b) {
+            if (devices[a] == devices[b]) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, devices[a], devices[b]) != cudaSuccess || !can) {
+                grp->peer_ok = false;
+                break;
+            }
+            DeviceGuard dg(devices[a]);
+            cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+                e = cudaSuccess;
+            }
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                grp->peer_ok = false;
+                break;
+            }
+        }
+    *out = grp;
+    return BSG_OK;
+}
+
+int bsg_ctx_group_size(const bsg_ctx* ctx) {
+    if (!ctx) return 0;
+    return ctx->members.empty() ? 1 : static_cast<int>(ctx->members.size());
+}
+
+int bsg_ctx_group_device(const bsg_ctx* ctx, int member) {
+    if (!ctx || member < 0 || member >= bsg_ctx_group_size(ctx)) return -1;
+    return ctx->members.empty() ? ctx->device : ctx->members[member]->device;
 }
 
 int bsg_ctx_set_timing(bsg_ctx* ctx, int enable) {
@@ -376,6 +490,8 @@ int bsg_parallel_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out,
     if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
     const int all_rounds = 32 / radix_log2;
     const int rounds = (rounds_limit >= 0 && rounds_limit < all_rounds) ? rounds_limit : all_rounds;
+    if (ctx->members.size() > 1) return parallel_radix_sort_group(ctx, in, out, n, p, radix_log2, rounds, stats, mem_kind,
+                                                                  static_cast<cudaStream_t>(stream));
     CallGuard g(ctx);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -62,6 +63,17 @@ struct bsg_ctx {
     cudaEvent_t last_use = nullptr;
     cudaStream_t last_stream = nullptr;
     bool used = false;
+
+    // Multi-GPU group (bsg_ctx_create_group): one member context per listed
+    // device (owned), each with its own workspace and stream; peer access
+    // enabled between distinct member devices; NCCL communicators built
+    // lazily by the first BSG_PR_NCCL call (ncclCommInitAll over the
+    // members).  Empty for single-device contexts.
+    std::vector<bsg_ctx*> members;
+    std::vector<cudaStream_t> member_streams;
+    bool peer_ok = true;    // every pair of distinct member devices can reach each other
+    void* nccl = nullptr;   // bsg::NcclGroup* (pr.cu)
+    bsg::DevBuf grp_cur, grp_nxt, grp_recv; // per-member range buffers (members only)
 
     // Ensures the radix workspace for n keys and returns a view of it.
     int radix_ws(uint64_t n, bsg::RadixWorkspace* ws);

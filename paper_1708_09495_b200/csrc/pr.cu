@@ -20,7 +20,9 @@
 // scatter of the sorted blocks.  Across GPUs,
 // paper_1708_09495_b200/distributed.py interleaves the count / plan / local /
 // rebuild steps with NCCL all-gather / all-to-all-v.
+#include <dlfcn.h>
 #include <mutex>
+#include <nccl.h>
 #include <algorithm>
 #include <vector>
 
@@ -528,6 +530,31 @@ __global__ void __launch_bounds__(kSendThreads)
         if (s_cnt2[w]) atomicAdd(reinterpret_cast<unsigned long long*>(send + static_cast<uint64_t>(v) * p + w), s_cnt2[w]);
 }
 
+// Exchange + rebuild of one group member's workers (r = 2^16 group rounds):
+// key i of local worker lv's sorted block (global worker wlo + lv) with
+// digit d goes to global position start[d] + gd[wlo+lv][d] + i and is stored
+// in the owning member's next-round buffer (PeerTable over G members).
+__global__ void __launch_bounds__(kScatterThreads)
+    pr_scatter_peer_kernel(const uint32_t* __restrict__ sorted, uint64_t len, int pw, int wlo, int shift,
+                           uint32_t mask, int radix, const uint64_t* __restrict__ start,
+                           const int64_t* __restrict__ gd, const __grid_constant__ PeerTable tab, int G) {
+    const int lv = blockIdx.y;
+    const uint64_t off = part_offset(len, pw, lv), blen = part_size(len, pw, lv);
+    const uint32_t* blk = sorted + off;
+    const int64_t* gdv = gd + static_cast<uint64_t>(wlo + lv) * radix;
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * kScatterThreads;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kScatterThreads + threadIdx.x; i < blen; i += step) {
+        const uint32_t key = __ldg(blk + i);
+        const uint32_t d = (key >> shift) & mask;
+        const uint64_t pos =
+            static_cast<uint64_t>(static_cast<int64_t>(__ldg(start + d)) + __ldg(gdv + d) + static_cast<int64_t>(i));
+        int m = 0;
+        for (int j = 1; j < G; ++j) m += pos >= tab.offset[j] ? 1 : 0;
+        tab.blocks[m][pos - tab.offset[m]] = key;
+    }
+    __threadfence_system();
+}
+
 } // namespace
 
 int launch_pr_count(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int round, int bits, uint64_t* counts,
@@ -940,4 +967,607 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     ctx->launches += static_cast<uint64_t>(l);
     if ((e = cudaPeekAtLastError()) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fused round launch");
     return BSG_OK;
+}
+
+// ===========================================================================
+// Multi-GPU group (one process, G GPUs): bsg_ctx_create_group and
+// bsg_pr_group_sort_u32 (include/bsg.h).  Member g owns the worker group
+// Partition(p, G) block g, i.e. a contiguous key range; its workers' blocks
+// are Partition(len_g, p_g) of that range (the big blocks of Partition(n, p)
+// come first), so every in-process segmented kernel applies per member.
+// ===========================================================================
+namespace bsg {
+
+// NCCL is resolved at run time (dlopen), so libbsg.so loads without it and a
+// process that already holds libnccl.so.2 (torch) shares that one copy.
+struct NcclApi {
+    decltype(&ncclCommInitAll) commInitAll = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGetErrorString) errStr = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+static NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return a;
+        }
+        a.commInitAll = reinterpret_cast<decltype(a.commInitAll)>(dlsym(h, "ncclCommInitAll"));
+        a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.groupStart = reinterpret_cast<decltype(a.groupStart)>(dlsym(h, "ncclGroupStart"));
+        a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+        a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+        a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+        a.errStr = reinterpret_cast<decltype(a.errStr)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.commInitAll && a.commDestroy && a.groupStart && a.groupEnd && a.send && a.recv && a.errStr;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+struct NcclGroup {
+    std::vector<ncclComm_t> comms;
+};
+
+static int nccl_fail(ncclResult_t r, const char* what) {
+    const NcclApi& a = nccl_api();
+    return fail(BSG_ENCCL, std::string(what) + ": " + (a.errStr ? a.errStr(r) : "nccl error"));
+}
+
+void destroy_group_nccl(bsg_ctx* grp) {
+    auto* ng = static_cast<NcclGroup*>(grp->nccl);
+    if (!ng) return;
+    if (nccl_api().ok)
+        for (ncclComm_t c : ng->comms)
+            if (c) nccl_api().commDestroy(c);
+    delete ng;
+    grp->nccl = nullptr;
+}
+
+// Host restatement of the routing for RunStats / remote-byte accounting:
+// slice[v][w] = keys of worker v landing in worker w's partition (the
+// messages of sort_and_scatter, radix.hpp:151-179), from the p x r matrix.
+static void host_slices(const std::vector<uint64_t>& cnt, uint64_t n, int p, int radix,
+                        std::vector<uint64_t>& slice) {
+    slice.assign(static_cast<size_t>(p) * p, 0);
+    std::vector<uint64_t> dstart(radix), before(radix, 0);
+    uint64_t run = 0;
+    for (int d = 0; d < radix; ++d) {
+        dstart[d] = run;
+        for (int v = 0; v < p; ++v) run += cnt[static_cast<size_t>(v) * radix + d];
+    }
+    for (int v = 0; v < p; ++v)
+        for (int d = 0; d < radix; ++d) {
+            const uint64_t c = cnt[static_cast<size_t>(v) * radix + d];
+            if (!c) continue;
+            const uint64_t np = dstart[d] + before[d];
+            before[d] += c;
+            int w = bsg_partition_owner_of(n, p, np);
+            uint64_t pos = np, end = np + c;
+            while (pos < end) {
+                const uint64_t hi = bsg_partition_offset_of(n, p, w) + bsg_partition_size_of(n, p, w);
+                const uint64_t take = std::min(end, hi) - pos;
+                slice[static_cast<size_t>(v) * p + w] += take;
+                pos += take;
+                ++w;
+            }
+        }
+}
+
+struct GroupMember {
+    bsg_ctx* c = nullptr;
+    cudaStream_t s = nullptr;
+    int wlo = 0, pw = 0;       // workers [wlo, wlo + pw)
+    uint64_t off = 0, len = 0; // key range
+    uint32_t* cur = nullptr;
+    uint32_t* nxt = nullptr;
+    cudaEvent_t ev = nullptr;
+    cudaEvent_t t[6] = {};
+};
+
+uint64_t group_range_offset(uint64_t n, int p, int G, int g) {
+    const int wlo = static_cast<int>(bsg_partition_offset_of(static_cast<uint64_t>(p), G, g));
+    return bsg_partition_offset_of(n, p, wlo);
+}
+
+int run_parallel_radix_group(bsg_ctx* grp, uint32_t* const* blocks, uint64_t n, int p, int bits, int rounds,
+                             int variant, bsg_run_stats* stats, bsg_pr_timing* timing) {
+    const int G = static_cast<int>(grp->members.size());
+    if (G < 1) return fail(BSG_EINVAL, "not a group context");
+    if (G > kPeerMax) return fail(BSG_EINVAL, "group: at most 64 members");
+    if (p > kMaxP) return fail(BSG_EINVAL, "parallel radix sort: p must be <= 1024");
+    if (variant != BSG_PR_PEER && variant != BSG_PR_NCCL) return fail(BSG_EINVAL, "group sort: unknown variant");
+    if (variant == BSG_PR_PEER && !grp->peer_ok)
+        return fail(BSG_ECUDA, "group sort: member GPUs lack peer access (use BSG_PR_NCCL)");
+    if (variant == BSG_PR_NCCL && p != G) return fail(BSG_EINVAL, "group sort: BSG_PR_NCCL needs p == group size");
+    const int radix = 1 << bits;
+    const uint32_t mask = static_cast<uint32_t>(radix - 1);
+    const uint64_t pp = static_cast<uint64_t>(p) * p;
+    std::vector<GroupMember> M(G);
+    cudaError_t e;
+    for (int g = 0; g < G; ++g) {
+        GroupMember& m = M[g];
+        m.c = grp->members[g];
+        m.s = grp->member_streams[g];
+        m.wlo = static_cast<int>(bsg_partition_offset_of(static_cast<uint64_t>(p), G, g));
+        m.pw = static_cast<int>(bsg_partition_size_of(static_cast<uint64_t>(p), G, g));
+        m.off = bsg_partition_offset_of(n, p, m.wlo);
+        m.len = bsg_partition_offset_of(n, p, m.wlo + m.pw) - m.off;
+        m.cur = blocks[g];
+        if (m.len && !m.cur) return fail(BSG_EINVAL, "group sort: null member block");
+    }
+    // workspace + events per member
+    for (GroupMember& m : M) {
+        DeviceGuard dg(m.c->device);
+        bsg_ctx* c = m.c;
+        const uint64_t L = std::max<uint64_t>(m.len, 4);
+        if ((e = c->pr_block.ensure(L * 4)) != cudaSuccess) return cuda_fail(e, "group workspace");
+        if ((e = c->pr_counts.ensure(static_cast<uint64_t>(p) * (radix + 1) * 8)) != cudaSuccess)
+            return cuda_fail(e, "group workspace");
+        if ((e = c->pr_delta.ensure(static_cast<uint64_t>(p) * radix * 8)) != cudaSuccess)
+            return cuda_fail(e, "group workspace");
+        if ((e = c->pr_misc.ensure(static_cast<uint64_t>(radix) * 16 + 128 * 8 + pp * 8 + 64)) != cudaSuccess)
+            return cuda_fail(e, "group workspace");
+        if ((e = c->status.ensure(onesweep_seg_status_words(L, std::max(m.pw, 1)) * sizeof(uint32_t))) != cudaSuccess)
+            return cuda_fail(e, "group workspace");
+        if (bits == 16 || variant == BSG_PR_NCCL) {
+            if ((e = c->pr_sorted.ensure(L * 4)) != cudaSuccess) return cuda_fail(e, "group workspace");
+            if ((e = c->stage_b.ensure(L * 4)) != cudaSuccess) return cuda_fail(e, "group workspace");
+            const uint64_t chunks = (static_cast<uint64_t>(radix) + 1023) / 1024;
+            const uint64_t plan_words = static_cast<uint64_t>(p) * (1 + chunks) + 2ull * radix + chunks;
+            if ((e = c->pr_recv.ensure(std::max<uint64_t>(4ull * std::max(m.pw, 1) * 256 + 64, plan_words) * 8)) != cudaSuccess)
+                return cuda_fail(e, "group workspace");
+        }
+        m.nxt = c->pr_block.as<uint32_t>();
+        if ((e = cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "group events");
+        if (timing)
+            for (auto& t : m.t)
+                if ((e = cudaEventCreate(&t)) != cudaSuccess) return cuda_fail(e, "group events");
+    }
+    struct EvFree {
+        std::vector<GroupMember>& M;
+        ~EvFree() {
+            for (auto& m : M) {
+                DeviceGuard dg(m.c->device);
+                if (m.ev) cudaEventDestroy(m.ev);
+                for (auto& t : m.t)
+                    if (t) cudaEventDestroy(t);
+            }
+        }
+    } evfree{M};
+    auto all_wait_all = [&]() -> int {
+        for (auto& m : M) {
+            DeviceGuard dg(m.c->device);
+            if ((e = cudaEventRecord(m.ev, m.s)) != cudaSuccess) return cuda_fail(e, "group barrier");
+        }
+        for (auto& m : M) {
+            DeviceGuard dg(m.c->device);
+            for (auto& o : M)
+                if (&o != &m && (e = cudaStreamWaitEvent(m.s, o.ev, 0)) != cudaSuccess)
+                    return cuda_fail(e, "group barrier");
+        }
+        return BSG_OK;
+    };
+    auto mark = [&](int k) {
+        if (!timing) return;
+        for (auto& m : M) {
+            DeviceGuard dg(m.c->device);
+            cudaEventRecord(m.t[k], m.s);
+        }
+    };
+    // per-phase accumulation (ms, max over members per phase per round)
+    double t_count = 0, t_exch = 0, t_local = 0;
+    uint64_t remote = 0;
+    auto phase_ms = [&](int a, int b) -> double {
+        double mx = 0;
+        for (auto& m : M) {
+            DeviceGuard dg(m.c->device);
+            cudaEventSynchronize(m.t[b]);
+            float f = 0;
+            cudaEventElapsedTime(&f, m.t[a], m.t[b]);
+            mx = std::max(mx, static_cast<double>(f));
+        }
+        return mx;
+    };
+    // the caller's work on member streams is ordered by the synchronous call
+    if (int rc = all_wait_all()) return rc;
+    cudaEvent_t t_begin[kPeerMax] = {}, t_end[kPeerMax] = {};
+    if (timing)
+        for (int g = 0; g < G; ++g) {
+            DeviceGuard dg(M[g].c->device);
+            cudaEventCreate(&t_begin[g]);
+            cudaEventCreate(&t_end[g]);
+            cudaEventRecord(t_begin[g], M[g].s);
+        }
+    bsg_run_stats st{};
+    std::vector<uint64_t> h_cnt, h_slice;
+    uint64_t launches = 0;
+    auto add = [&](int l) -> bool {
+        if (l < 0) return false;
+        launches += static_cast<uint64_t>(l);
+        return true;
+    };
+    // pull the other members' rows of a [p][row] uint64 table into every member's copy
+    auto exchange_rows = [&](auto table_of, uint64_t row) -> int {
+        if (int rc = all_wait_all()) return rc;
+        for (auto& m : M) {
+            DeviceGuard dg(m.c->device);
+            for (auto& o : M) {
+                if (&o == &m || o.pw == 0) continue;
+                const uint64_t b = static_cast<uint64_t>(o.pw) * row * 8;
+                if ((e = cudaMemcpyAsync(table_of(m) + static_cast<uint64_t>(o.wlo) * row,
+                                         table_of(o) + static_cast<uint64_t>(o.wlo) * row, b, cudaMemcpyDefault, m.s)) !=
+                    cudaSuccess)
+                    return cuda_fail(e, "group count exchange");
+            }
+        }
+        return BSG_OK;
+    };
+    auto counts_of = [](GroupMember& m) { return m.c->pr_counts.as<uint64_t>(); };
+    PeerTable tab{};
+    for (int g = 0; g < G; ++g) tab.offset[g] = M[g].off;
+    tab.offset[G] = n;
+    NcclApi& api = nccl_api();
+    if (variant == BSG_PR_NCCL && n) {
+        if (!api.ok) return fail(BSG_ENCCL, "BSG_PR_NCCL: " + api.why);
+        if (!grp->nccl) {
+            auto* ng = new NcclGroup();
+            ng->comms.resize(G);
+            std::vector<int> devs(G);
+            for (int g = 0; g < G; ++g) devs[g] = M[g].c->device;
+            ncclResult_t r = api.commInitAll(ng->comms.data(), G, devs.data());
+            if (r != ncclSuccess) {
+                delete ng;
+                return nccl_fail(r, "ncclCommInitAll");
+            }
+            grp->nccl = ng;
+        }
+    }
+    for (int round = 0; round < rounds && n; ++round) {
+        const int shift = round * bits;
+        mark(0);
+        if (variant == BSG_PR_PEER) {
+            if (bits <= 8) {
+                // count_digits of every local worker (radix.hpp:127-132), then the
+                // count-matrix exchange (the reference's send-to-all of counts)
+                for (auto& m : M) {
+                    DeviceGuard dg(m.c->device);
+                    TimerBinding tb(&m.c->timer);
+                    if (m.pw && !add(launch_pr_seg_count(m.cur, m.len, m.pw, bits, shift,
+                                                         counts_of(m) + static_cast<uint64_t>(m.wlo) * radix, m.s)))
+                        return cuda_fail(cudaGetLastError(), "group count");
+                }
+                if (int rc = exchange_rows(counts_of, radix)) return rc;
+                mark(1);
+                for (auto& m : M) {
+                    DeviceGuard dg(m.c->device);
+                    TimerBinding tb(&m.c->timer);
+                    uint64_t* counts = counts_of(m);
+                    int64_t* base = m.c->pr_delta.as<int64_t>();
+                    uint64_t* coltot = m.c->pr_misc.as<uint64_t>();
+                    uint64_t* dstart = coltot + radix;
+                    uint64_t* colchunk = dstart + radix;
+                    uint32_t* skew = reinterpret_cast<uint32_t*>(colchunk + 64);
+                    const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+                    if ((e = cudaMemsetAsync(skew, 0, sizeof(uint32_t), m.s)) != cudaSuccess) return cuda_fail(e, "group plan");
+                    pr_plan_col_kernel<<<chunks, kDigChunk, 0, m.s>>>(counts, p, radix, base, coltot, colchunk, skew, n);
+                    pr_digit_start_kernel<<<chunks, kDigChunk, 0, m.s>>>(coltot, colchunk, radix, dstart);
+                    const uint64_t pr = static_cast<uint64_t>(p) * radix;
+                    pr_add_dstart_kernel<<<static_cast<unsigned>((pr + 255) / 256), 256, 0, m.s>>>(base, dstart, p, radix);
+                    launches += 3;
+                    PeerTable t = tab;
+                    for (int g = 0; g < G; ++g) t.blocks[g] = M[g].nxt;
+                    // the whole round of every local worker as ONE pass: keys
+                    // stored at their global positions in the owners' buffers
+                    if (m.pw && !add(launch_onesweep_seg_peer(
+                                    m.cur, m.len, m.pw, bits, shift,
+                                    reinterpret_cast<const uint64_t*>(base) + static_cast<uint64_t>(m.wlo) * radix,
+                                    m.c->status.as<uint32_t>(), m.s, skew, t, G, n)))
+                        return cuda_fail(cudaGetLastError(), "group fused pass");
+                }
+            } else {
+                // r = 2^16: local pass of every worker (two segmented byte
+                // sub-passes, segment-local bases), run starts, starts exchange,
+                // then one peer scatter to the global positions
+                for (auto& m : M) {
+                    if (!m.pw) continue;
+                    DeviceGuard dg(m.c->device);
+                    TimerBinding tb(&m.c->timer);
+                    uint64_t* scratch = m.c->pr_recv.as<uint64_t>();
+                    uint64_t* cA = scratch;
+                    uint64_t* cB = cA + static_cast<uint64_t>(m.pw) * 256;
+                    int64_t* bA = reinterpret_cast<int64_t*>(cB + static_cast<uint64_t>(m.pw) * 256);
+                    int64_t* bB = bA + static_cast<uint64_t>(m.pw) * 256;
+                    uint32_t* skew = reinterpret_cast<uint32_t*>(bB + static_cast<uint64_t>(m.pw) * 256);
+                    uint32_t* mid = m.c->stage_b.as<uint32_t>();
+                    uint32_t* S = m.c->pr_sorted.as<uint32_t>();
+                    if (!add(launch_pr_seg_count(m.cur, m.len, m.pw, 8, shift, cA, m.s)) ||
+                        !add(launch_pr_seg_count(m.cur, m.len, m.pw, 8, shift + 8, cB, m.s)))
+                        return cuda_fail(cudaGetLastError(), "group local count");
+                    if ((e = cudaMemsetAsync(skew, 0, 2 * sizeof(uint32_t), m.s)) != cudaSuccess)
+                        return cuda_fail(e, "group local count");
+                    pr_local_base_kernel<<<m.pw, 256, 0, m.s>>>(cA, m.len, m.pw, bA, skew);
+                    pr_local_base_kernel<<<m.pw, 256, 0, m.s>>>(cB, m.len, m.pw, bB, skew + 1);
+                    launches += 2;
+                    if (!add(launch_onesweep_seg(m.cur, mid, m.len, m.pw, 8, shift, reinterpret_cast<const uint64_t*>(bA),
+                                                 m.c->status.as<uint32_t>(), m.s, skew)) ||
+                        !add(launch_onesweep_seg(mid, S, m.len, m.pw, 8, shift + 8, reinterpret_cast<const uint64_t*>(bB),
+                                                 m.c->status.as<uint32_t>(), m.s, skew + 1)))
+                        return cuda_fail(cudaGetLastError(), "group local pass");
+                    pr_run_starts_kernel<<<dim3((radix + 1 + 255) / 256, m.pw), 256, 0, m.s>>>(
+                        S, m.len, m.pw, shift, mask, radix, counts_of(m) + static_cast<uint64_t>(m.wlo) * (radix + 1));
+                    ++launches;
+                }
+                if (int rc = exchange_rows(counts_of, static_cast<uint64_t>(radix) + 1)) return rc;
+                mark(1);
+                for (auto& m : M) {
+                    DeviceGuard dg(m.c->device);
+                    TimerBinding tb(&m.c->timer);
+                    int64_t* gd = m.c->pr_delta.as<int64_t>();
+                    uint64_t* coltot = m.c->pr_misc.as<uint64_t>();
+                    uint64_t* dstart = coltot + radix;
+                    uint64_t* colchunk = dstart + radix;
+                    const int chunks = (radix + kDigChunk - 1) / kDigChunk;
+                    pr_col_prefix_kernel<<<chunks, kDigChunk, 0, m.s>>>(counts_of(m), p, radix, gd, coltot, colchunk);
+                    pr_digit_start_kernel<<<chunks, kDigChunk, 0, m.s>>>(coltot, colchunk, radix, dstart);
+                    launches += 2;
+                    if (!m.pw) continue;
+                    PeerTable t = tab;
+                    for (int g = 0; g < G; ++g) t.blocks[g] = M[g].nxt;
+                    const uint64_t max_len = m.len / m.pw + 1;
+                    const uint64_t want = (max_len + kScatterThreads * kScatterItems - 1) / (kScatterThreads * kScatterItems);
+                    const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(
+                        1, std::min<uint64_t>(want, std::max<uint64_t>(1, kSmCountB200 * 8 / static_cast<uint64_t>(m.pw)))));
+                    pr_scatter_peer_kernel<<<dim3(gx, m.pw), kScatterThreads, 0, m.s>>>(
+                        m.c->pr_sorted.as<uint32_t>(), m.len, m.pw, m.wlo, shift, mask, radix, dstart, gd, t, G);
+                    ++launches;
+                }
+            }
+            mark(2);
+            if (int rc = all_wait_all()) return rc; // every owner's next block is complete
+            for (auto& m : M) std::swap(m.cur, m.nxt);
+            if (timing) {
+                t_count += phase_ms(0, 1);
+                t_exch += phase_ms(1, 2);
+            }
+        } else {
+            // ---- BSG_PR_NCCL: p == G, member g = worker g ----
+            std::vector<uint64_t> h_send(pp), h_recv(pp);
+            for (auto& m : M) {
+                DeviceGuard dg(m.c->device);
+                TimerBinding tb(&m.c->timer);
+                uint64_t* counts = counts_of(m);
+                if (!add(launch_pr_count(m.c, m.cur, m.len, round, bits, counts + static_cast<uint64_t>(m.wlo) * radix, m.s)))
+                    return cuda_fail(cudaGetLastError(), "group count");
+            }
+            if (int rc = exchange_rows(counts_of, radix)) return rc;
+            mark(1);
+            for (int g = 0; g < G; ++g) {
+                GroupMember& m = M[g];
+                DeviceGuard dg(m.c->device);
+                TimerBinding tb(&m.c->timer);
+                uint64_t* scratch = m.c->pr_recv.as<uint64_t>();
+                uint64_t* send = m.c->pr_misc.as<uint64_t>() + 2 * radix + 128; // [p]
+                uint64_t* recv = send + p;                                         // [p]
+                if ((e = cudaMemsetAsync(send, 0, 2ull * p * 8, m.s)) != cudaSuccess) return cuda_fail(e, "group plan");
+                const int l = launch_pr_plan(counts_of(m), n, p, g, bits, send, recv, m.c->pr_delta.as<int64_t>(), m.s,
+                                             scratch);
+                if (!add(l)) return cuda_fail(cudaGetLastError(), "group plan");
+                // local stable pass of sort_and_scatter (radix.hpp:151-179)
+                RadixWorkspace ws;
+                if (int rc = m.c->radix_ws(std::max<uint64_t>(m.len, 1), &ws)) return rc;
+                uint32_t* S = m.c->pr_sorted.as<uint32_t>();
+                if (m.len) {
+                    if (bits <= 8) {
+                        if (!add(launch_count_pass(m.cur, S, m.len, bits, shift, ws, m.s, true)))
+                            return cuda_fail(cudaGetLastError(), "group local pass");
+                    } else {
+                        uint32_t* mid = m.c->stage_b.as<uint32_t>();
+                        if (!add(launch_count_pass(m.cur, mid, m.len, 8, shift, ws, m.s, true)) ||
+                            !add(launch_count_pass(mid, S, m.len, 8, shift + 8, ws, m.s, true)))
+                            return cuda_fail(cudaGetLastError(), "group local pass");
+                    }
+                }
+                if ((e = cudaMemcpyAsync(h_send.data() + static_cast<uint64_t>(g) * p, send, p * 8, cudaMemcpyDeviceToHost,
+                                         m.s)) != cudaSuccess ||
+                    (e = cudaMemcpyAsync(h_recv.data() + static_cast<uint64_t>(g) * p, recv, p * 8, cudaMemcpyDeviceToHost,
+                                         m.s)) != cudaSuccess)
+                    return cuda_fail(e, "group plan");
+            }
+            for (auto& m : M) {
+                DeviceGuard dg(m.c->device);
+                if ((e = cudaStreamSynchronize(m.s)) != cudaSuccess) return cuda_fail(e, "group plan");
+            }
+            // bsp_error checks of gather_slices (radix.hpp:207-220, 283-286)
+            for (int g = 0; g < G; ++g) {
+                uint64_t in_sum = 0, out_sum = 0;
+                for (int h = 0; h < G; ++h) {
+                    in_sum += h_recv[static_cast<uint64_t>(g) * p + h];
+                    out_sum += h_send[static_cast<uint64_t>(g) * p + h];
+                    if (h_send[static_cast<uint64_t>(g) * p + h] != h_recv[static_cast<uint64_t>(h) * p + g])
+                        return fail(BSG_EPROTO, "bsp_error: send/receive counts disagree between workers");
+                }
+                if (in_sum != M[g].len || out_sum != M[g].len)
+                    return fail(BSG_EPROTO, "bsp_error: received slices do not fill the worker's partition");
+            }
+            mark(2);
+            // all-to-all-v of the contiguous slices over NCCL
+            auto* ng = static_cast<NcclGroup*>(grp->nccl);
+            ncclResult_t r = api.groupStart();
+            if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+            for (int g = 0; g < G; ++g) {
+                GroupMember& m = M[g];
+                const uint32_t* S = m.c->pr_sorted.as<uint32_t>();
+                uint32_t* R = m.c->stage_b.as<uint32_t>();
+                uint64_t so = 0, ro = 0;
+                for (int h = 0; h < G; ++h) {
+                    const uint64_t sc = h_send[static_cast<uint64_t>(g) * p + h];
+                    const uint64_t rc = h_recv[static_cast<uint64_t>(g) * p + h];
+                    if (h != g) remote += sc * 4;
+                    if (sc && (r = api.send(S + so, sc, ncclUint32, h, ng->comms[g], m.s)) != ncclSuccess) {
+                        api.groupEnd();
+                        return nccl_fail(r, "ncclSend");
+                    }
+                    if (rc && (r = api.recv(R + ro, rc, ncclUint32, h, ng->comms[g], m.s)) != ncclSuccess) {
+                        api.groupEnd();
+                        return nccl_fail(r, "ncclRecv");
+                    }
+                    so += sc;
+                    ro += rc;
+                }
+            }
+            if ((r = api.groupEnd()) != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+            mark(3);
+            // gather_slices: stable digit scatter of the source-major buffer
+            for (int g = 0; g < G; ++g) {
+                GroupMember& m = M[g];
+                DeviceGuard dg(m.c->device);
+                TimerBinding tb(&m.c->timer);
+                uint64_t* recv = m.c->pr_misc.as<uint64_t>() + 2 * radix + 128 + p;
+                if (!add(launch_pr_rebuild(m.c->stage_b.as<uint32_t>(), m.len, bits, shift, m.c->pr_delta.as<int64_t>(),
+                                           m.cur, m.s, recv, p)))
+                    return cuda_fail(cudaGetLastError(), "group rebuild");
+            }
+            mark(4);
+            if (timing) {
+                t_count += phase_ms(0, 1);
+                t_local += phase_ms(1, 2) + phase_ms(3, 4);
+                t_exch += phase_ms(2, 3);
+            }
+        }
+        if (stats || (timing && variant == BSG_PR_PEER)) {
+            // RunStats (and the remote bytes of the peer rounds) from member
+            // 0's copy of this round's count matrix
+            GroupMember& m0 = M[0];
+            DeviceGuard dg(m0.c->device);
+            const uint64_t row = (variant == BSG_PR_PEER && bits == 16) ? radix + 1 : radix;
+            std::vector<uint64_t> raw(static_cast<size_t>(p) * row);
+            if ((e = cudaMemcpyAsync(raw.data(), counts_of(m0), raw.size() * 8, cudaMemcpyDeviceToHost, m0.s)) != cudaSuccess ||
+                (e = cudaStreamSynchronize(m0.s)) != cudaSuccess)
+                return cuda_fail(e, "group stats");
+            h_cnt.assign(static_cast<size_t>(p) * radix, 0);
+            for (int v = 0; v < p; ++v)
+                for (int d = 0; d < radix; ++d)
+                    h_cnt[static_cast<size_t>(v) * radix + d] =
+                        row == static_cast<uint64_t>(radix) ? raw[static_cast<size_t>(v) * row + d]
+                                                            : raw[static_cast<size_t>(v) * row + d + 1] -
+                                                                  raw[static_cast<size_t>(v) * row + d];
+            host_slices(h_cnt, n, p, radix, h_slice);
+            uint64_t nz = 0;
+            for (uint64_t i = 0; i < pp; ++i) nz += h_slice[i] ? 1 : 0;
+            st.messages_sent += pp + nz;
+            st.words_sent += pp * static_cast<uint64_t>(radix) + n;
+            if (variant == BSG_PR_PEER)
+                for (int v = 0; v < p; ++v)
+                    for (int w = 0; w < p; ++w) {
+                        const int gv = static_cast<int>(std::upper_bound(M.begin(), M.end(), v, [](int x, const GroupMember& m) {
+                                           return x < m.wlo + m.pw;
+                                       }) - M.begin());
+                        const int gw = static_cast<int>(std::upper_bound(M.begin(), M.end(), w, [](int x, const GroupMember& m) {
+                                           return x < m.wlo + m.pw;
+                                       }) - M.begin());
+                        if (gv != gw) remote += h_slice[static_cast<size_t>(v) * p + w] * 4;
+                    }
+        }
+    }
+    // results back into the callers' blocks
+    for (auto& m : M) {
+        DeviceGuard dg(m.c->device);
+        if (m.len && m.cur != blocks[&m - M.data()] &&
+            (e = cudaMemcpyAsync(blocks[&m - M.data()], m.cur, m.len * 4, cudaMemcpyDeviceToDevice, m.s)) != cudaSuccess)
+            return cuda_fail(e, "group copy out");
+    }
+    if (timing)
+        for (int g = 0; g < G; ++g) {
+            DeviceGuard dg(M[g].c->device);
+            cudaEventRecord(t_end[g], M[g].s);
+        }
+    for (auto& m : M) {
+        DeviceGuard dg(m.c->device);
+        if ((e = cudaStreamSynchronize(m.s)) != cudaSuccess) return cuda_fail(e, "group sort");
+    }
+    grp->launches += launches;
+    if (timing) {
+        double tot = 0;
+        for (int g = 0; g < G; ++g) {
+            DeviceGuard dg(M[g].c->device);
+            float f = 0;
+            cudaEventElapsedTime(&f, t_begin[g], t_end[g]);
+            tot = std::max(tot, static_cast<double>(f));
+            cudaEventDestroy(t_begin[g]);
+            cudaEventDestroy(t_end[g]);
+        }
+        timing->total_ms = tot;
+        timing->count_ms = t_count;
+        timing->exchange_ms = t_exch;
+        timing->local_ms = t_local;
+        timing->remote_bytes = remote;
+    }
+    if (stats) {
+        if (n == 0) {
+            st.messages_sent = static_cast<uint64_t>(rounds) * pp;
+            st.words_sent = static_cast<uint64_t>(rounds) * pp * radix;
+        }
+        st.supersteps = 2 * rounds + 1;
+        st.messages_delivered = st.messages_sent;
+        st.words_delivered = st.words_sent;
+        *stats = st;
+    }
+    return BSG_OK;
+}
+
+} // namespace bsg
+
+extern "C" uint64_t bsg_group_range_offset(uint64_t n, int p, int G, int g) {
+    if (p < 1 || G < 1 || g < 0) return 0;
+    if (g >= G) return n;
+    return bsg::group_range_offset(n, p, G, g);
+}
+extern "C" uint64_t bsg_group_range_size(uint64_t n, int p, int G, int g) {
+    if (p < 1 || G < 1 || g < 0 || g >= G) return 0;
+    return bsg::group_range_offset(n, p, G, g + 1) - bsg::group_range_offset(n, p, G, g);
+}
+
+extern "C" int bsg_pr_group_sort_u32(bsg_ctx* grp, uint32_t* const* blocks, uint64_t n, int p, int radix_log2,
+                                     int rounds_limit, int variant, bsg_run_stats* stats, bsg_pr_timing* timing,
+                                     void* const* streams) {
+    using namespace bsg;
+    if (!grp) return fail(BSG_EINVAL, "null context");
+    if (grp->members.empty()) return fail(BSG_EINVAL, "bsg_pr_group_sort_u32 needs a group context (bsg_ctx_create_group)");
+    if (p < 1) return fail(BSG_EINVAL, "parallel radix sort: p must be >= 1");
+    if (radix_log2 != 1 && radix_log2 != 2 && radix_log2 != 4 && radix_log2 != 8 && radix_log2 != 16)
+        return fail(BSG_EINVAL, "radix must be a power of two whose bit width divides 32");
+    if (n && !blocks) return fail(BSG_EINVAL, "null block table");
+    const int all_rounds = 32 / radix_log2;
+    const int rounds = (rounds_limit >= 0 && rounds_limit < all_rounds) ? rounds_limit : all_rounds;
+    std::lock_guard<std::mutex> lock(grp->mu);
+    // order the callers' work on the blocks before the members' streams
+    const int G = static_cast<int>(grp->members.size());
+    for (int g = 0; g < G; ++g) {
+        DeviceGuard dg(grp->members[g]->device);
+        cudaError_t e;
+        if (streams) {
+            cudaEvent_t ev;
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventRecord(ev, static_cast<cudaStream_t>(streams[g]))) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(grp->member_streams[g], ev, 0)) != cudaSuccess)
+                return cuda_fail(e, "group sort: caller stream ordering");
+            cudaEventDestroy(ev);
+        } else if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+            return cuda_fail(e, "group sort: device synchronize");
+        }
+    }
+    return run_parallel_radix_group(grp, blocks, n, p, radix_log2, rounds, variant, stats, timing);
 }

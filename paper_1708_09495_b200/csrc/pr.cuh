@@ -30,4 +30,11 @@ int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shi
 int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, int p, int bits, int rounds,
                              bsg_run_stats* stats, cudaStream_t stream);
 
+// Multi-GPU group (bsg_pr_group_sort_u32): p workers over the group's
+// members; blocks[g] = member g's key range (device g), sorted in place.
+int run_parallel_radix_group(bsg_ctx* grp, uint32_t* const* blocks, uint64_t n, int p, int bits, int rounds,
+                             int variant, bsg_run_stats* stats, bsg_pr_timing* timing);
+uint64_t group_range_offset(uint64_t n, int p, int G, int g);
+void destroy_group_nccl(bsg_ctx* grp);
+
 } // namespace bsg

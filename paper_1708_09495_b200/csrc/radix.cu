@@ -1309,6 +1309,81 @@ int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, i
     }
 }
 
+// Segmented pass whose write-out goes through a PeerTable: the member of a
+// multi-GPU group runs its workers' blocks as segments; key positions are
+// global and land in the owning member's next-round buffer (local or a peer
+// GPU's, NVLink stores).  G = members in the table.
+template <int BITS, int THREADS, int ITEMS, bool WIDE>
+__global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
+    onesweep_seg_peer_kernel(const uint32_t* __restrict__ src, const SegDesc sd, int shift,
+                             const uint64_t* __restrict__ base_table, uint32_t* __restrict__ status,
+                             uint32_t* __restrict__ tile_counter, int32_t neg1, const uint32_t* __restrict__ skew,
+                             const __grid_constant__ PeerTable tab, int G) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t parity = 0;
+    if (BITS == 8 && skew && !*skew)
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PeerSink, default_lb_window<THREADS>(), true>(
+            smem, src, PeerSink{&tab, G}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
+    else
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PeerSink, default_lb_window<THREADS>(), true>(
+            smem, src, PeerSink{&tab, G}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
+    __threadfence_system(); // peer stores performed before the round's cross-GPU barrier
+}
+
+template <int BITS, int THREADS, int ITEMS, bool WIDE = false>
+int launch_onesweep_seg_peer_cfg(const uint32_t* src, uint64_t n, int p, int shift, const uint64_t* base_table,
+                                 uint32_t* status, cudaStream_t stream, const uint32_t* skew, const PeerTable& tab,
+                                 int G) {
+    using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
+    constexpr int RADIX = 1 << BITS;
+    auto kern = onesweep_seg_peer_kernel<BITS, THREADS, ITEMS, WIDE>;
+    static PerDeviceOccupancy occ;
+    const int per_sm = std::max(1, kernel_occupancy(occ, kern, THREADS, L::bytes));
+    const int sms = current_sm_count();
+    SegDesc sd;
+    sd.small = n / static_cast<uint64_t>(p);
+    sd.p = static_cast<uint32_t>(p);
+    sd.nbig = static_cast<uint32_t>(n % static_cast<uint64_t>(p));
+    sd.tiles_big = static_cast<uint32_t>((sd.small + 1 + L::TILE - 1) / L::TILE);
+    sd.tiles_small = static_cast<uint32_t>((sd.small + L::TILE - 1) / L::TILE);
+    const uint64_t tiles = static_cast<uint64_t>(sd.nbig) * sd.tiles_big +
+                           static_cast<uint64_t>(sd.p - sd.nbig) * sd.tiles_small;
+    if (tiles == 0) return 0;
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * per_sm));
+    if (cudaMemsetAsync(status, 0, (32 + tiles * RADIX * (WIDE ? 2 : 1)) * sizeof(uint32_t), stream) != cudaSuccess)
+        return -1;
+    TimedScope ts(3 /*BSG_K_PR*/, stream);
+    kern<<<grid, THREADS, L::bytes, stream>>>(src, sd, shift, base_table, status + 32, status, -1, skew, tab, G);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_onesweep_seg_peer(const uint32_t* src, uint64_t n, int p, int bits, int shift, const uint64_t* base_table,
+                             uint32_t* status, cudaStream_t stream, const uint32_t* skew, const PeerTable& tab, int G,
+                             uint64_t n_total) {
+    if (n == 0) return 0;
+    // 64-bit rows when a segment exceeds a 30-bit look-back count or global
+    // positions exceed 32 bits
+    if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys || n_total > 0xFFFFFFFFull) {
+        switch (bits) {
+        case 1: return launch_onesweep_seg_peer_cfg<1, 512, 24, true>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+        case 2: return launch_onesweep_seg_peer_cfg<2, 512, 24, true>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+        case 4: return launch_onesweep_seg_peer_cfg<4, 512, 24, true>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+        case 8: return launch_onesweep_seg_peer_cfg<8, 512, 24, true>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+        default: return -1;
+        }
+    }
+    switch (bits) {
+    case 1: return launch_onesweep_seg_peer_cfg<1, 512, 16>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+    case 2: return launch_onesweep_seg_peer_cfg<2, 512, 16>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+    case 4: return launch_onesweep_seg_peer_cfg<4, 512, 16>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+    case 8:
+        if (n > (uint64_t{1} << 23))
+            return launch_onesweep_seg_peer_cfg<8, 512, 24>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+        return launch_onesweep_seg_peer_cfg<8, 512, 16>(src, n, p, shift, base_table, status, stream, skew, tab, G);
+    default: return -1;
+    }
+}
+
 uint64_t onesweep_seg_status_words(uint64_t n, int p) {
     // 8192-key tiles at the smallest: one extra partial tile per segment
     // (64-bit words for the large segments of the WIDE rows)

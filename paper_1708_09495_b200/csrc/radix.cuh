@@ -75,6 +75,13 @@ int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, i
                         const uint32_t* skew = nullptr);
 uint64_t onesweep_seg_status_words(uint64_t n, int p);
 
+// launch_onesweep_seg whose write-out stores key position g into
+// tab.blocks[m][g - tab.offset[m]] of the member m owning g (G members,
+// tab.offset[G] = n_total): one multi-GPU group member's PR round.
+int launch_onesweep_seg_peer(const uint32_t* src, uint64_t n, int p, int bits, int shift, const uint64_t* base_table,
+                             uint32_t* status, cudaStream_t stream, const uint32_t* skew, const PeerTable& tab, int G,
+                             uint64_t n_total);
+
 int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shift, const uint64_t* digit_base,
                          uint32_t* status, const PeerTable& tab, int p, cudaStream_t stream,
                          const uint32_t* skew, uint64_t n_total);

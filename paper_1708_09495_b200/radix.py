@@ -122,9 +122,13 @@ def prepare_parallel_radix(keys, p: int, radix: int) -> PreparedRadix:
     return PreparedRadix(plan, kb.obj)
 
 
-def run_parallel_radix(prep: PreparedRadix, use_sequential_executor: bool = False) -> ParallelSortResult:
-    """radix.hpp:260-303: PR with p logical workers on the GPU.  The executor
-    flag is accepted for signature parity; results are identical either way."""
+def run_parallel_radix(prep: PreparedRadix, use_sequential_executor: bool = False,
+                       group: Optional["_lib.GroupContext"] = None) -> ParallelSortResult:
+    """radix.hpp:260-303: PR with p logical workers on the GPU -- or, with a
+    ``group`` (:class:`_lib.GroupContext`), spread over the group's GPUs in
+    this process (numpy input, or a CUDA tensor on the group's first device).
+    The executor flag is accepted for signature parity; results are identical
+    either way."""
     del use_sequential_executor
     plan = prep.plan
     full_rounds = key_bits // plan.bits
@@ -132,7 +136,7 @@ def run_parallel_radix(prep: PreparedRadix, use_sequential_executor: bool = Fals
     kb = KeyBuf(prep.keys)
     out = kb.empty(kb.n)
     stats = _lib.RunStats()
-    ctx = kb.ctx()
+    ctx = group if group is not None else kb.ctx()
     _lib.check(_lib.lib().bsg_parallel_radix_sort_u32(ctx.handle, kb.ptr, KeyBuf(out).ptr, kb.n, plan.part.p,
                                                       plan.bits, rounds_limit, ctypes.byref(stats), kb.mem, kb.stream),
                "run_parallel_radix")
@@ -160,3 +164,31 @@ def digit_counts(block, round: int, radix: int):
     _lib.check(_lib.lib().bsg_pr_count_digits(kb.ctx().handle, kb.ptr, kb.n, round, bits, counts.data_ptr(),
                                               kb.stream), "count_digits")
     return counts
+
+
+def group_sort_blocks(group, blocks, n: int, p: int, radix: int, rounds=None, variant: int = 0,
+                      timing: bool = False):
+    """bsg_pr_group_sort_u32: the parallel radix sort over a group context
+    whose member g holds its key range in ``blocks[g]`` (a CUDA tensor on the
+    member's device, sorted in place).  Returns (RunStats dict, timing dict or
+    None).  variant: _lib.PR_PEER (fused NVLink rounds) or _lib.PR_NCCL."""
+    bits = checked_digit_bits(radix)
+    full_rounds = key_bits // bits
+    rounds_limit = -1 if rounds is None or rounds >= full_rounds else max(0, int(rounds))
+    import torch
+
+    ptrs = (ctypes.c_void_p * len(blocks))(*[b.data_ptr() for b in blocks])
+    # each member waits for the torch stream that produced its block
+    streams = (ctypes.c_void_p * len(blocks))(*[torch.cuda.current_stream(b.device).cuda_stream for b in blocks])
+    stats = _lib.RunStats()
+    tm = _lib.PrTiming()
+    _lib.check(_lib.lib().bsg_pr_group_sort_u32(group.handle, ptrs, int(n), int(p), bits, rounds_limit, int(variant),
+                                                ctypes.byref(stats), ctypes.byref(tm) if timing else None, streams),
+               "group sort")
+    return stats.as_dict(), (tm.as_dict() if timing else None)
+
+
+def group_range(n: int, p: int, G: int, g: int):
+    """(offset, size) of member g's key range in a G-member group."""
+    L = _lib.lib()
+    return int(L.bsg_group_range_offset(n, p, G, g)), int(L.bsg_group_range_size(n, p, G, g))

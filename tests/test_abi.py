@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol(bsg):
     for s in syms:
         assert hasattr(lib, s), s
         assert s in bsg._lib.SIGNATURES, s
-    assert lib.bsg_abi_version() == 1
+    assert lib.bsg_abi_version() == 2
 
 
 def test_cpp_header_mirror_compiles():
