@@ -6,6 +6,7 @@
 // with this header; KeyArray-by-value calls stage through the GPU.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -61,6 +62,8 @@ inline constexpr int digit_bits(std::uint64_t radix) {
 }
 
 namespace bsp {
+using Word = std::uint32_t;          // bsp.hpp:26
+using Block = std::vector<Word>;     // bsp.hpp:27
 // bsp.hpp:38-41; protocol failures reported by the GPU path (BSG_EPROTO).
 class bsp_error : public std::runtime_error {
   public:
@@ -83,7 +86,7 @@ inline void check(int status) {
     if (status == BSG_ENOMEM) throw std::bad_alloc();
     throw std::runtime_error(msg);
 }
-// One context per process (device 0 unless BSG_DEVICE says otherwise).
+// One context per process on device 0.
 inline bsg_ctx* context() {
     static std::once_flag once;
     static bsg_ctx* ctx = nullptr;
@@ -91,6 +94,19 @@ inline bsg_ctx* context() {
     std::call_once(once, [] { rc = bsg_ctx_create(0, &ctx); });
     check(rc);
     return ctx;
+}
+// The process-wide multi-GPU group used by run_parallel_radix once
+// bspsort::gpu::use_devices() was called (nullptr: one GPU).
+struct GroupHolder {
+    std::mutex mu;
+    bsg_ctx* grp = nullptr;
+    ~GroupHolder() {
+        if (grp) bsg_ctx_destroy(grp);
+    }
+};
+inline GroupHolder& group_holder() {
+    static GroupHolder h;
+    return h;
 }
 inline bsp::RunStats to_stats(const bsg_run_stats& s) {
     return bsp::RunStats{s.supersteps, s.messages_sent, s.messages_delivered, s.words_sent, s.words_delivered};
@@ -172,9 +188,9 @@ struct RadixPlan { // radix.hpp:120-125
 };
 } // namespace detail
 
-struct PreparedRadix { // radix.hpp:228-231 (input kept whole; blocks are its partition)
+struct PreparedRadix { // radix.hpp:228-231
     detail::RadixPlan plan;
-    KeyArray keys;
+    std::vector<bsp::Block> blocks;
 };
 
 inline PreparedRadix prepare_parallel_radix(const KeyArray& keys, int p, std::uint64_t radix) { // radix.hpp:233-249
@@ -185,7 +201,11 @@ inline PreparedRadix prepare_parallel_radix(const KeyArray& keys, int p, std::ui
     prep.plan.radix = radix;
     prep.plan.bits = bits;
     prep.plan.rounds = key_bits / bits;
-    prep.keys = keys;
+    prep.blocks.resize(p);
+    for (int w = 0; w < p; ++w) {
+        const auto begin = keys.begin() + static_cast<std::ptrdiff_t>(prep.plan.part.offset_of(w));
+        prep.blocks[w].assign(begin, begin + static_cast<std::ptrdiff_t>(prep.plan.part.size_of(w)));
+    }
     return prep;
 }
 
@@ -195,16 +215,36 @@ struct ParallelSortResult { // radix.hpp:251-254
 };
 
 // radix.hpp:260-303; the executor flag is accepted, results are identical.
+// The workers run on the GPU -- or on every GPU given to gpu::use_devices().
+// Blocks must be the plan's Partition (bsp_error otherwise, as the
+// reference's gather_slices consistency checks would raise).
 inline ParallelSortResult run_parallel_radix(PreparedRadix prep, bool use_sequential_executor = false) {
     (void)use_sequential_executor;
+    const int p = prep.plan.part.p;
+    if (static_cast<int>(prep.blocks.size()) != p) throw bsp::bsp_error("run_parallel_radix: expected p blocks");
+    std::uint64_t n = 0;
+    for (const auto& b : prep.blocks) n += b.size();
+    if (n != prep.plan.part.n) throw bsp::bsp_error("run_parallel_radix: blocks do not hold the plan's n keys");
+    KeyArray keys;
+    keys.reserve(n);
+    for (int w = 0; w < p; ++w) {
+        if (prep.blocks[w].size() != prep.plan.part.size_of(w))
+            throw bsp::bsp_error("run_parallel_radix: block sizes differ from the balanced partition");
+        keys.insert(keys.end(), prep.blocks[w].begin(), prep.blocks[w].end());
+    }
     const int all = key_bits / prep.plan.bits;
     const int limit = prep.plan.rounds >= all ? -1 : prep.plan.rounds;
     ParallelSortResult res;
-    res.output.resize(prep.keys.size());
+    res.output.resize(n);
     bsg_run_stats st{};
-    ::bspsort::detail::check(bsg_parallel_radix_sort_u32(::bspsort::detail::context(), prep.keys.data(),
-                                                         res.output.data(), prep.keys.size(), prep.plan.part.p,
-                                                         prep.plan.bits, limit, &st, BSG_MEM_HOST, nullptr));
+    bsg_ctx* ctx = ::bspsort::detail::context();
+    auto& gh = ::bspsort::detail::group_holder();
+    {
+        std::lock_guard<std::mutex> lk(gh.mu);
+        if (gh.grp) ctx = gh.grp;
+    }
+    ::bspsort::detail::check(bsg_parallel_radix_sort_u32(ctx, keys.data(), res.output.data(), n, p, prep.plan.bits,
+                                                         limit, &st, BSG_MEM_HOST, nullptr));
     res.stats = ::bspsort::detail::to_stats(st);
     return res;
 }
@@ -254,41 +294,88 @@ inline std::vector<std::vector<StageAssignment>> schedule(int network, int p) {
 inline BitonicSchedule bitonic_schedule(int p) { return BitonicSchedule{p, detail::schedule(BSG_NET_BTN, p)}; }
 inline std::vector<std::vector<StageAssignment>> odd_even_rounds(int p) { return detail::schedule(BSG_NET_OET, p); }
 
-struct PreparedNetwork { // netsort.hpp:112-118 (+ which network, for the GPU)
+struct PreparedNetwork { // netsort.hpp:112-118 (+ which network the table came from)
     int p = 1;
-    std::uint64_t n = 0;
-    std::size_t pad = 0;
-    KeyArray keys; // unpadded input; padding happens on the device
+    std::uint64_t n = 0;   // keys before padding
+    std::size_t pad = 0;   // trailing max-value keys to strip from the output
+    std::vector<bsp::Block> blocks;
     std::vector<std::vector<StageAssignment>> stages;
     int network = BSG_NET_BTN;
 };
 
-inline PreparedNetwork prepare_btn(const KeyArray& keys, int p) {
-    PreparedNetwork prep{p, keys.size(), 0, keys, bitonic_schedule(p).stages, BSG_NET_BTN};
-    const std::size_t L = (keys.size() + p - 1) / p;
-    prep.pad = L * p - keys.size();
+namespace detail {
+// netsort.hpp:124-141: blocks of ceil(n/p) keys padded with ~Key{0}
+inline PreparedNetwork prepare_blocks(const KeyArray& keys, int p, std::vector<std::vector<StageAssignment>> stages,
+                                      int network) {
+    PreparedNetwork prep;
+    prep.p = p;
+    prep.n = keys.size();
+    prep.stages = std::move(stages);
+    prep.network = network;
+    const std::size_t block_len = (keys.size() + p - 1) / p;
+    prep.pad = block_len * p - keys.size();
+    prep.blocks.assign(p, {});
+    for (int w = 0; w < p; ++w) {
+        const std::size_t begin = std::min(keys.size(), w * block_len);
+        const std::size_t end = std::min(keys.size(), begin + block_len);
+        prep.blocks[w].assign(keys.begin() + begin, keys.begin() + end);
+        prep.blocks[w].resize(block_len, ~Key{0});
+    }
     return prep;
 }
-inline PreparedNetwork prepare_oet(const KeyArray& keys, int p) {
-    PreparedNetwork prep{p, keys.size(), 0, keys, odd_even_rounds(p), BSG_NET_OET};
-    const std::size_t L = (keys.size() + p - 1) / p;
-    prep.pad = L * p - keys.size();
-    return prep;
+// The GPU path runs the closed-form BTN / OET schedules: a stage table must
+// be a prefix of one of them (a truncated table stops early); other custom
+// tables are rejected rather than silently replaced.
+inline int prefix_of_network(const PreparedNetwork& prep) {
+    const int other = prep.network == BSG_NET_BTN ? static_cast<int>(BSG_NET_OET) : static_cast<int>(BSG_NET_BTN);
+    for (int net : {prep.network, other}) {
+        if (net == BSG_NET_BTN && !is_power_of_two(static_cast<std::uint64_t>(prep.p))) continue;
+        const auto full = schedule(net, prep.p);
+        if (prep.stages.size() > full.size()) continue;
+        bool same = true;
+        for (std::size_t s = 0; s < prep.stages.size() && same; ++s) {
+            if (prep.stages[s].size() != static_cast<std::size_t>(prep.p)) same = false;
+            for (int i = 0; i < prep.p && same; ++i)
+                same = prep.stages[s][i].partner == full[s][i].partner &&
+                       (prep.stages[s][i].partner < 0 || prep.stages[s][i].keep_low == full[s][i].keep_low);
+        }
+        if (same) return net;
+    }
+    throw std::invalid_argument("run_block_network: the GPU path runs the BTN/OET schedules (or a prefix of them); "
+                                "custom stage tables are not supported");
+}
+} // namespace detail
+
+inline PreparedNetwork prepare_btn(const KeyArray& keys, int p) { // netsort.hpp:145-147
+    return detail::prepare_blocks(keys, p, bitonic_schedule(p).stages, BSG_NET_BTN);
+}
+inline PreparedNetwork prepare_oet(const KeyArray& keys, int p) { // netsort.hpp:149-151
+    return detail::prepare_blocks(keys, p, odd_even_rounds(p), BSG_NET_OET);
 }
 
-// netsort.hpp:157-199; a truncated stage table stops the network early.
+// netsort.hpp:157-199; a truncated stage table stops the network early.  The
+// concatenated (padded) blocks are the device input; the output is stripped
+// to n keys (netsort.hpp:197).
 inline radix::ParallelSortResult run_block_network(PreparedNetwork prep, bool use_sequential_executor = false) {
     (void)use_sequential_executor;
+    if (static_cast<int>(prep.blocks.size()) != prep.p) throw bsp::bsp_error("run_block_network: expected p blocks");
+    const std::size_t L = prep.blocks.empty() ? 0 : prep.blocks[0].size();
+    KeyArray keys;
+    keys.reserve(L * prep.p);
+    for (const auto& b : prep.blocks) {
+        if (b.size() != L) throw bsp::bsp_error("merge_split: blocks differ in size"); // netsort.hpp:172-176
+        keys.insert(keys.end(), b.begin(), b.end());
+    }
+    const int net = detail::prefix_of_network(prep);
     int S = 0;
-    ::bspsort::detail::check(bsg_network_schedule(prep.network, prep.p, nullptr, nullptr, 0, &S));
+    ::bspsort::detail::check(bsg_network_schedule(net, prep.p, nullptr, nullptr, 0, &S));
     const int limit = static_cast<int>(prep.stages.size()) >= S ? -1 : static_cast<int>(prep.stages.size());
-    const std::size_t L = (prep.keys.size() + prep.p - 1) / prep.p;
-    KeyArray out(limit < 0 ? prep.keys.size() : L * prep.p);
+    if (keys.size() > 0xFFFFFFFFull) throw std::invalid_argument("block network: n must fit in 32 bits");
+    KeyArray out(keys.size());
     bsg_run_stats st{};
-    ::bspsort::detail::check(bsg_block_network_batched_u32(::bspsort::detail::context(), prep.network,
-                                                           prep.keys.data(), out.data(), prep.keys.empty() ? 0 : 1,
-                                                           static_cast<std::uint32_t>(prep.keys.size()), prep.p, limit,
-                                                           &st, BSG_MEM_HOST, nullptr));
+    ::bspsort::detail::check(bsg_block_network_batched_u32(::bspsort::detail::context(), net, keys.data(), out.data(),
+                                                           keys.empty() ? 0 : 1, static_cast<std::uint32_t>(keys.size()),
+                                                           prep.p, limit, &st, BSG_MEM_HOST, nullptr));
     out.resize(prep.n); // netsort.hpp:197
     return radix::ParallelSortResult{std::move(out), ::bspsort::detail::to_stats(st)};
 }
@@ -305,6 +392,25 @@ inline KeyArray oet_sort(const SortInstance& instance) { // netsort.hpp:210-215
 }
 
 } // namespace netsort
+
+// B200 extension: run the parallel radix sort's p workers over several GPUs
+// of this process (a group context, bsg_ctx_create_group).  Call once before
+// run_parallel_radix / parallel_radix_sort / sort_instance; an empty list
+// returns to one GPU.  Reference code is otherwise unchanged.
+namespace gpu {
+inline void use_devices(const std::vector<int>& devices) {
+    auto& gh = ::bspsort::detail::group_holder();
+    std::lock_guard<std::mutex> lk(gh.mu);
+    if (gh.grp) {
+        bsg_ctx_destroy(gh.grp);
+        gh.grp = nullptr;
+    }
+    if (devices.empty()) return;
+    bsg_ctx* g = nullptr;
+    ::bspsort::detail::check(bsg_ctx_create_group(devices.data(), static_cast<int>(devices.size()), &g));
+    gh.grp = g;
+}
+} // namespace gpu
 
 inline KeyArray sort_instance(const SortInstance& instance) { // bspsort.hpp:15-25
     instance.validate();

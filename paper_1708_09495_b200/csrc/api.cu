@@ -74,12 +74,12 @@ int with_device_io(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n_i
     if ((e = ctx->stage_out.ensure(std::max<uint64_t>(n_out, 4) * 4)) != cudaSuccess) return cuda_fail(e, "host staging");
     uint32_t* d_in = ctx->stage_in.as<uint32_t>();
     uint32_t* d_out = ctx->stage_out.as<uint32_t>();
-    if (n_in && (e = cudaMemcpyAsync(d_in, in, n_in * 4, cudaMemcpyHostToDevice, stream)) != cudaSuccess)
-        return cuda_fail(e, "H2D copy");
+    if (n_in)
+        if (int rc = copy_h2d(ctx, d_in, in, n_in * 4, stream)) return rc;
     int rc = body(d_in, d_out, stream);
     if (rc != BSG_OK) return rc;
-    if (n_out && (e = cudaMemcpyAsync(out, d_out, n_out * 4, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
-        return cuda_fail(e, "D2H copy");
+    if (n_out)
+        if (int rc2 = copy_d2h(ctx, out, d_out, n_out * 4, stream)) return rc2;
     if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "stream synchronize");
     return BSG_OK;
 }
@@ -123,9 +123,12 @@ int parallel_radix_sort_group(bsg_ctx* grp, const uint32_t* in, uint32_t* out, u
         const uint64_t off = group_range_offset(n, p, G, g), len = group_range_offset(n, p, G, g + 1) - off;
         if ((e = m->grp_cur.ensure(std::max<uint64_t>(len, 4) * 4)) != cudaSuccess) return cuda_fail(e, "group staging");
         blocks[g] = m->grp_cur.as<uint32_t>();
-        if (len && (e = cudaMemcpyAsync(blocks[g], in + off, len * 4, cudaMemcpyDefault, grp->member_streams[g])) !=
-                       cudaSuccess)
+        if (len && mem_kind == BSG_MEM_HOST) {
+            if (int rc = copy_h2d(m, blocks[g], in + off, len * 4, grp->member_streams[g])) return rc;
+        } else if (len && (e = cudaMemcpyAsync(blocks[g], in + off, len * 4, cudaMemcpyDefault,
+                                               grp->member_streams[g])) != cudaSuccess) {
             return cuda_fail(e, "group staging");
+        }
     }
     const int variant = grp->peer_ok || p != G ? BSG_PR_PEER : BSG_PR_NCCL;
     if (int rc = run_parallel_radix_group(grp, blocks.data(), n, p, bits, rounds, variant, stats, nullptr)) return rc;
@@ -133,9 +136,12 @@ int parallel_radix_sort_group(bsg_ctx* grp, const uint32_t* in, uint32_t* out, u
         bsg_ctx* m = grp->members[g];
         DeviceGuard dg(m->device);
         const uint64_t off = group_range_offset(n, p, G, g), len = group_range_offset(n, p, G, g + 1) - off;
-        if (len && (e = cudaMemcpyAsync(out + off, blocks[g], len * 4, cudaMemcpyDefault, grp->member_streams[g])) !=
-                       cudaSuccess)
+        if (len && mem_kind == BSG_MEM_HOST) {
+            if (int rc = copy_d2h(m, out + off, blocks[g], len * 4, grp->member_streams[g])) return rc;
+        } else if (len && (e = cudaMemcpyAsync(out + off, blocks[g], len * 4, cudaMemcpyDefault,
+                                               grp->member_streams[g])) != cudaSuccess) {
             return cuda_fail(e, "group copy out");
+        }
     }
     for (int g = 0; g < G; ++g) {
         DeviceGuard dg(grp->members[g]->device);
@@ -192,6 +198,7 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
                           &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->mt_ws})
             b->release();
         if (ctx->last_use) cudaEventDestroy(ctx->last_use);
+        release_stage(ctx);
     }
     delete ctx;
     return BSG_OK;

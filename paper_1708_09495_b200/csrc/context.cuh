@@ -74,6 +74,9 @@ struct bsg_ctx {
     bool peer_ok = true;    // every pair of distinct member devices can reach each other
     void* nccl = nullptr;   // bsg::NcclGroup* (pr.cu)
     bsg::DevBuf grp_cur, grp_nxt, grp_recv; // per-member range buffers (members only)
+    // pinned chunk buffers for pageable BSG_MEM_HOST copies (staging.cu)
+    void* pin_buf[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
 
     // Ensures the radix workspace for n keys and returns a view of it.
     int radix_ws(uint64_t n, bsg::RadixWorkspace* ws);
@@ -95,6 +98,12 @@ struct DeviceGuard {
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
     }
 };
+
+// Host<->device copies of BSG_MEM_HOST calls (staging.cu): pageable host
+// memory is pipelined through the context's pinned chunk buffers.
+int copy_h2d(bsg_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s);
+int copy_d2h(bsg_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s);
+void release_stage(bsg_ctx* c);
 
 // RAII: order this call's stream after the context's previous call (see
 // bsg_ctx::last_use).  Construct with the context mutex held and the

@@ -122,6 +122,49 @@ int main() {
         ok.algorithm = Algorithm::SR4;
         CHECK((sort_instance(ok) == KeyArray{1, 2, 3}));
     }
+    // PreparedRadix::blocks / PreparedNetwork::blocks as in the reference
+    // (radix.hpp:228-249, netsort.hpp:112-141), and the intermediate states
+    // the reference exposes through plan.rounds / a truncated stage table
+    {
+        const auto k = generate_uniform_keys(10007, 5);
+        auto prep = radix::prepare_parallel_radix(k, 3, 256);
+        CHECK(prep.blocks.size() == 3u && prep.blocks[0].size() == 3336u && prep.blocks[2].size() == 3335u);
+        prep.plan.rounds = 1;
+        CHECK(radix::run_parallel_radix(prep).output == radix::count_sort_round(k, 0, 256));
+        prep.blocks[1].pop_back();
+        bool threw = false;
+        try {
+            radix::run_parallel_radix(prep);
+        } catch (const bsp::bsp_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+        auto net = netsort::prepare_btn(k, 4);
+        CHECK(net.blocks.size() == 4u && net.blocks[3].size() == 2502u && net.pad == 1u && net.blocks[3].back() == ~Key{0});
+        CHECK(netsort::run_block_network(net).output == oracle_sort(k));
+        auto bad = net;
+        bad.stages[0][0].partner = 2;
+        CHECK(throws_invalid([&] { netsort::run_block_network(bad); }));
+    }
+    // several GPUs through the unchanged reference API (cuda:0 listed twice
+    // on a one-GPU box: the group code path with local stores)
+    {
+        gpu::use_devices({0, 0});
+        const auto k = generate_uniform_keys(300001, 6);
+        for (int p : {2, 3, 8}) {
+            SortInstance s;
+            s.input = k;
+            s.processors = p;
+            s.algorithm = Algorithm::PR2;
+            s.radix = 65536;
+            CHECK(radix::parallel_radix_sort(s) == oracle_sort(k));
+            auto prep = radix::prepare_parallel_radix(k, p, 256);
+            prep.plan.rounds = 2;
+            KeyArray two = radix::count_sort_round(radix::count_sort_round(k, 0, 256), 1, 256);
+            CHECK(radix::run_parallel_radix(prep).output == two);
+        }
+        gpu::use_devices({});
+    }
     CHECK(verify_sorted_permutation({3, 1, 2}, {1, 2, 3}));
     CHECK(!verify_sorted_permutation({3, 1, 2}, {1, 2, 4}));
     std::printf("%s %d checks, %d failed\n", g_fail ? "FAILED" : "OK", g_checks, g_fail);

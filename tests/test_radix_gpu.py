@@ -373,3 +373,16 @@ def test_aliased_outputs(cuda, bsg, orc):
         for i in (0, 1, 50, num - 1):
             exp, _ = orc.block_network(0, arrs[i], p, stages)
             np.testing.assert_array_equal(got[i], exp)
+
+
+def test_pageable_host_staging(cuda, bsg, orc):
+    """BSG_MEM_HOST with pageable numpy buffers above the 4 MiB direct-copy
+    threshold runs the pinned two-chunk pipeline (staging.cu) both ways:
+    odd sizes, several 64 MiB chunks, a misaligned host pointer."""
+    for n in ((1 << 20) + 1, (1 << 26) + 12345):
+        keys = orc.generate_uniform_keys(n + 1, n)
+        view = keys[1:]  # misaligned host start (4-byte offset)
+        out = bsg.radix.count_sort_round(view, 2, 256)
+        np.testing.assert_array_equal(out, orc.count_sort_round(view, 2, 256))
+    keys = orc.generate_uniform_keys((1 << 25) + 7, 3)
+    np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
