@@ -305,6 +305,11 @@ int bsg_pr_group_sort_u32(bsg_ctx* group, uint32_t* const* blocks, uint64_t n, i
  * derives the generator's characteristic polynomial (host, ~0.1 s). */
 int bsg_generate_uniform_device_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n,
                                     uint64_t seed, void* stream);
+/* Keys [offset, offset + n) of the same stream on the GPU (one jump-ahead of
+ * the seeded state on the host, then as above): a rank's block of a
+ * block-distributed generate_uniform_keys(N, seed) (config 5). */
+int bsg_generate_uniform_device_at_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n,
+                                       uint64_t seed, uint64_t offset, void* stream);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,7 @@ SIGNATURES = {
     "bsg_generate_uniform_u32": (_i, [_u32p, _u64, _u64]),
     "bsg_generate_uniform_at_u32": (_i, [_u32p, _u64, _u64, _u64]),
     "bsg_generate_uniform_device_u32": (_i, [_vp, _u32p, _u64, _u64, _vp]),
+    "bsg_generate_uniform_device_at_u32": (_i, [_vp, _u32p, _u64, _u64, _u64, _vp]),
     "bsg_derive_seed": (ctypes.c_uint64, [_u64, ctypes.c_int32]),
     "bsg_checked_digit_bits": (_i, [_u64]),
     "bsg_generate_skewed_u32": (_i, [_u32p, _u64, _u64, _i, ctypes.c_double]),

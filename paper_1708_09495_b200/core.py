@@ -106,16 +106,18 @@ def generate_uniform_keys_at(n: int, seed: int, offset: int) -> np.ndarray:
     return out
 
 
-def generate_uniform_keys_device(n: int, seed: int, device: int = 0):
+def generate_uniform_keys_device(n: int, seed: int, device: int = 0, offset: int = 0):
     """generate_uniform_keys on the GPU: a torch.uint32 CUDA tensor holding the
-    same n keys, bit for bit (segment starts by jump-ahead)."""
+    same n keys, bit for bit (segment starts by jump-ahead); ``offset`` > 0
+    gives keys [offset, offset + n) of the stream (a rank's block of a
+    block-distributed input)."""
     import torch
 
     out = torch.empty(int(n), dtype=torch.int32, device=torch.device("cuda", device))
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().bsg_generate_uniform_device_u32(ctx.handle, out.data_ptr(), int(n),
-                                                          int(seed) & (2**64 - 1),
-                                                          torch.cuda.current_stream(out.device).cuda_stream),
+    _lib.check(_lib.lib().bsg_generate_uniform_device_at_u32(ctx.handle, out.data_ptr(), int(n),
+                                                             int(seed) & (2**64 - 1), int(offset),
+                                                             torch.cuda.current_stream(out.device).cuda_stream),
                "generate_uniform_keys_device")
     return out.view(torch.uint32)
 

@@ -322,6 +322,11 @@ int bsg_generate_uniform_at_u32(uint32_t* out, uint64_t n, uint64_t seed, uint64
 }
 
 int bsg_generate_uniform_device_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n, uint64_t seed, void* stream) {
+    return bsg_generate_uniform_device_at_u32(ctx, out, n, seed, 0, stream);
+}
+
+int bsg_generate_uniform_device_at_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n, uint64_t seed, uint64_t offset,
+                                       void* stream) {
     using namespace bsg;
     using namespace bsg::mt;
     if (!ctx) return fail(BSG_EINVAL, "null context");
@@ -356,6 +361,7 @@ int bsg_generate_uniform_device_u32(bsg_ctx* ctx, uint32_t* out, uint64_t n, uin
     uint64_t* qdev = states + S * NW;
     std::vector<uint64_t> host(NW + static_cast<uint64_t>(rounds) * PW);
     base_window(seed, host.data());
+    if (offset) jump_host(host.data(), x_pow(offset, P)); // draws [offset, offset + n) of the stream
     for (int k = 0; k < rounds; ++k) std::copy(qs[k].begin(), qs[k].begin() + PW, host.begin() + NW + k * PW);
     // pageable copies are synchronous w.r.t. the host buffer, which then may go out of scope
     if ((e = cudaMemcpyAsync(states, host.data(), NW * sizeof(uint64_t), cudaMemcpyHostToDevice, st)) != cudaSuccess ||

@@ -279,6 +279,18 @@ def test_device_generator_matches_host_stream(cuda, bsg, n):
         np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), bsg.generate_uniform_keys(n, seed))
 
 
+@pytest.mark.parametrize("offset", [1, 311, 312, 100003, (1 << 30) + 5, (1 << 32) - 17])
+def test_device_generator_at_offset(cuda, bsg, orc, offset):
+    """bsg_generate_uniform_device_at_u32: keys [offset, offset + n) of the
+    host stream (a rank's block of config 5's block-distributed input)."""
+    n = (1 << 19) + 3
+    seed = bsg.derive_seed(1, 0)
+    got = bsg.generate_uniform_keys_device(n, seed, offset=offset).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got, bsg.generate_uniform_keys_at(n, seed, offset))
+    if offset < 200000:
+        np.testing.assert_array_equal(got, orc.generate_uniform_keys(offset + n, seed)[offset:])
+
+
 def test_in_place_calls(cuda, bsg, orc):
     """in == out device pointers: count-sort round, block networks and the
     in-process parallel radix sort."""
