@@ -7,9 +7,10 @@ N = 1 (default): config 2 of BASELINE.json -- single-GPU LSD radix sort (SR4:
 radix 2^8, 4 stable count-sort rounds) of n = 2^28 uint32 keys drawn by the
 reference generator (generate_uniform_keys, core.hpp:93-99, seed
 derive_seed(1, 0), bench.hpp:86-88), device-resident; a step is one full sort.
-N > 1 (torchrun, one rank per GPU): the paper's PR4 parallel radix sort,
-weak scaling with 2^28 keys per GPU (block-distributed; rank w's block is
-generate_uniform_keys(2^28, derive_seed(1, w))).  Default --pr-variant P:
+N > 1 (torchrun, one rank per GPU): config 5, the paper's PR4 parallel radix
+sort of n = 2^33 keys in total (strong scaling), block-distributed n/N per
+GPU (rank w generates its Partition block of generate_uniform_keys(n,
+derive_seed(1, 0)) on the device at its stream offset).  Default --pr-variant P:
 each round is ONE one-sweep pass per rank that stores every key at its final
 position in its owner's CUDA-IPC-mapped block over NVLink (counts all-gathered
 with NCCL; a 1-element all-reduce closes the round); A = the same rounds with
@@ -39,6 +40,7 @@ sys.path.insert(0, ROOT)
 METRIC = "uint32 keys sorted/sec"
 UNIT = "keys/s"
 N_PER_GPU = 1 << 28
+N_TOTAL_C5 = 1 << 33  # config 5: 2^33 keys (32 GiB) over the N GPUs
 
 
 def _peaks():
@@ -216,27 +218,30 @@ def _cpu_model() -> str:
     return "unknown CPU"
 
 
-def _config(world: int, variant=None):
+def _config(world: int, variant=None, n_total: int = None):
     if world == 1 and variant is None:
         return {"workload": "config 2: single-GPU LSD radix sort (SR4: radix 2^8, 4 stable count-sort rounds) of "
                             "n=2^28 uint32 keys, generate_uniform_keys(n, derive_seed(1,0))",
                 "n": N_PER_GPU, "radix": 256, "rounds": 4, "parallelism": "single GPU",
                 "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush needed"}
     if variant == "A":
-        what = ("PR4 as run_parallel_radix: per round digit count + NCCL all-gather of counts + NCCL all-to-all-v "
-                "of keys + rebuild (4 exchanges; per-round states bit-identical to the reference)")
+        what = ("PR4 as run_parallel_radix: per round digit count + NCCL all-gather of counts + local stable pass + "
+                "NCCL all-to-all-v of the contiguous slices + rebuild (4 exchanges; per-round states bit-identical "
+                "to the reference)")
     elif variant == "P":
         what = ("PR4 as run_parallel_radix with the exchange fused into the pass: per round digit count + NCCL "
                 "all-gather of counts + ONE one-sweep pass per rank whose write-out stores every key at its final "
                 "position in its owner's IPC-mapped next-round block over NVLink + a 1-element all-reduce barrier "
-                "(per-round states bit-identical to the reference; the exchange timing covers pass + barrier)")
+                "(per-round states bit-identical to the reference)")
     else:
         what = ("variant B: top-digit histogram + NCCL all-gather of counts + one stable partition pass + ONE NCCL "
-                "all-to-all-v + local LSD sort (BASELINE config-5 formulation; same sorted concatenation)")
-    return {"workload": f"config 5 (weak-scaled) over {world} GPUs, 2^28 uint32 keys per GPU (n={N_PER_GPU * world}): "
-                        + what, "variant": variant,
-            "n": N_PER_GPU * world, "n_per_gpu": N_PER_GPU, "radix": 256, "rounds": 4, "parallelism": f"dp{world}",
-            "l2": "inputs larger than L2; no flush needed"}
+                "all-to-all-v + local LSD sort (same sorted concatenation; per-rank sizes cut on digit boundaries)")
+    n_total = n_total or N_TOTAL_C5
+    return {"workload": f"config 5: multi-GPU parallel radix sort of n={n_total} uint32 keys "
+                        f"(generate_uniform_keys(n, derive_seed(1,0)), block-distributed n/p per GPU, generated on "
+                        f"each GPU at its stream offset) over {world} GPUs: " + what,
+            "variant": variant, "n": n_total, "n_per_gpu": n_total // world, "radix": 256, "rounds": 4,
+            "parallelism": f"dp{world}", "l2": "inputs larger than L2; no flush needed"}
 
 
 def run_single(args):
@@ -377,6 +382,10 @@ def run_single(args):
 
 
 def run_multi(args, rank: int, world: int, local_rank: int):
+    """Config 5: n = 2^33 keys in total, Partition(n, N) block w on GPU w
+    (generated there at its offset of the generate_uniform_keys stream),
+    PR4 over torch.distributed / NCCL, one process per GPU; strong scaling
+    (total work fixed).  Timed with CUDA events, max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_1708_09495_b200 as bsg
@@ -385,83 +394,120 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
-    n_local = args.n
-    n_total = n_local * world
-    keys = bsg.generate_uniform_keys(n_local, bsg.derive_seed(1, rank))
-    d_in = torch.from_numpy(keys.view(np.int32)).to(dev)
+    n_total = args.n_total
+    n_local = D.partition_size_of(n_total, world, rank)
+    off = D.partition_offset_of(n_total, world, rank)
+    seed = bsg.derive_seed(1, 0)
+    d_in = bsg.generate_uniform_keys_device(n_local, seed, device=local_rank, offset=off).view(torch.int32)
     ctx = _lib.context(local_rank)
 
     peer = None
     if args.pr_variant == "P":
         # map every rank's next-round blocks (CUDA IPC); if any rank cannot,
-        # all ranks agree to run variant B instead and say so in the JSON line
+        # all ranks agree to run variant A instead and say so in the JSON line
         try:
             peer = D.PeerBlocks(n_total, device=dev)
             okflag = 1
         except Exception as exc:  # noqa: BLE001
-            print(f"rank {rank}: peer mapping failed ({exc}); falling back to variant B", file=sys.stderr)
+            print(f"rank {rank}: peer mapping failed ({exc}); falling back to variant A", file=sys.stderr)
             okflag = 0
         flag = torch.tensor([okflag], dtype=torch.int32, device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
             args.fallback_from = "P"
-            args.pr_variant = "B"
+            args.pr_variant = "A"
             peer = None
 
-    def step(events=None):
+    def step(events=None, cevents=None, blk=None):
+        blk = d_in if blk is None else blk
         if args.pr_variant == "A":
-            return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events)
+            return D.parallel_radix_sort(blk, n_total, radix=256, a2a_events=events, count_events=cevents)
         if args.pr_variant == "P":
-            return D.parallel_radix_sort(d_in, n_total, radix=256, a2a_events=events, exchange="peer", peer=peer)
-        return D.parallel_radix_sort_single_exchange(d_in, a2a_events=events)
+            return D.parallel_radix_sort(blk, n_total, radix=256, a2a_events=events, exchange="peer", peer=peer,
+                                         count_events=cevents)
+        return D.parallel_radix_sort_single_exchange(blk, a2a_events=events)
 
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize()
     dist.barrier()
     l0 = ctx.launches
-    ev = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         dist.barrier()
         torch.cuda.synchronize()
         e0.record()
         for _ in range(args.steps):
-            out = step(ev)
+            out = step()
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    a2a_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    t = torch.tensor([ms, a2a_ms], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, a2a_max = t.tolist()
     launches = ctx.launches - l0
-    # verification (untimed): local sortedness, boundaries, global checksum
-    o64 = out.to(torch.int64) & 0xFFFFFFFF
-    local_ok = bool((o64[1:] >= o64[:-1]).all()) if o64.numel() > 1 else True
-    ends = torch.tensor([o64[0].item(), o64[-1].item()] if o64.numel() else [-1, -1], dtype=torch.int64, device=dev)
+    # phase split (separate, untimed steps with events): count + count
+    # all-gather, and the exchange -- A/B: the NCCL all-to-all-v; P: the fused
+    # pass + round barrier, compared with the same one-sweep pass storing
+    # locally (bsg_count_sort_round on the rank's block), whose difference is
+    # the NVLink cost the fused pass adds
+    ev, cev = [], []
+    for _ in range(2):
+        step(ev, cev)
+    torch.cuda.synchronize()
+    ksteps = 2
+    a2a_ms = sum(a.elapsed_time(b) for a, b in ev) / ksteps
+    cnt_ms = sum(a.elapsed_time(b) for a, b in cev) / ksteps
+    local_pass_ms = 0.0
+    if args.pr_variant == "P":
+        # the same fused-round kernel over the same block, as a one-worker
+        # round (p = 1): identical work, every store local
+        ops = D.CudaStepOps(dev)
+        tmp = torch.empty_like(d_in)
+        cnts = [ops.count(d_in, rnd, 8) for rnd in range(4)]
+        le0, le1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        le0.record()
+        for _ in range(ksteps):
+            for rnd in range(4):
+                ops.fused_round(d_in, cnts[rnd], n_local, 1, 0, rnd, 8, [tmp.data_ptr()])
+        le1.record()
+        torch.cuda.synchronize()
+        local_pass_ms = le0.elapsed_time(le1) / ksteps
+        del tmp, cnts
+    t = torch.tensor([ms, a2a_ms, cnt_ms, local_pass_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, a2a_max, cnt_max, local_max = t.tolist()
+    # verification (untimed): local sortedness, boundaries, global checksums
+    # (chunked: no n-sized int64 temporaries at 2^32 keys per GPU)
+    m = 1000003
+    sums = [0, 0, 0, 0]
+    local_ok = True
+    prev = None
+    step_c = 1 << 27
+    for a in range(0, n_local, step_c):
+        x = d_in[a:a + step_c].to(torch.int64) & 0xFFFFFFFF
+        y = out[a:a + step_c].to(torch.int64) & 0xFFFFFFFF
+        local_ok = local_ok and bool((y[1:] >= y[:-1]).all()) and (prev is None or int(y[0]) >= prev)
+        prev = int(y[-1])
+        sums[0] += int((x % m).sum()); sums[1] += int((y % m).sum())
+        sums[2] += int(((x % m) * (x % m) % m).sum()); sums[3] += int(((y % m) * (y % m) % m).sum())
+        del x, y
+    first = int(out[0].view(torch.int32).item()) & 0xFFFFFFFF if n_local else -1
+    ends = torch.tensor([first, prev if prev is not None else -1], dtype=torch.int64, device=dev)
     allends = [torch.empty_like(ends) for _ in range(world)]
     dist.all_gather(allends, ends)
     nonempty = [e for e in allends if e[0].item() >= 0]
     bounds_ok = all(nonempty[w][1].item() <= nonempty[w + 1][0].item() for w in range(len(nonempty) - 1))
-    cs = torch.tensor([(d_in.to(torch.int64) & 0xFFFFFFFF).sum().item(), o64.sum().item(), int(local_ok)],
-                      dtype=torch.float64, device=dev)
+    cs = torch.tensor([s_ % m for s_ in sums] + [int(local_ok)], dtype=torch.float64, device=dev)
     dist.all_reduce(cs)
-    ok = bounds_ok and cs[0].item() == cs[1].item() and int(cs[2].item()) == world
+    ok = bounds_ok and int(cs[0].item()) % m == int(cs[1].item()) % m and \
+        int(cs[2].item()) % m == int(cs[3].item()) % m and int(cs[4].item()) == world
 
     # e2e: each rank's block from pinned host memory, sort, result back
-    h_in = torch.from_numpy(keys.view(np.int32)).pin_memory()
+    h_in = d_in.cpu().pin_memory()
     h_out = torch.empty_like(h_in).pin_memory()
 
     def e2e_step():
         blk = h_in.to(dev, non_blocking=True)
-        if args.pr_variant == "A":
-            res = D.parallel_radix_sort(blk, n_total, radix=256)
-        elif args.pr_variant == "P":
-            res = D.parallel_radix_sort(blk, n_total, radix=256, exchange="peer", peer=peer)
-        else:
-            res = D.parallel_radix_sort_single_exchange(blk)
+        res = step(blk=blk)
         h_out[: res.numel()].copy_(res, non_blocking=True)
 
     e2e_step()
@@ -477,16 +523,26 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = te.item()
     if rank == 0:
+        remote = 4.0 * n_total * 4 * (world - 1) / world  # key bytes crossing GPUs per step (uniform keys: (N-1)/N per round)
         line = {
             "metric": METRIC, "value": n_total / (ms_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference generator, seeded per rank)",
-            "config": dict(_config(world, args.pr_variant),
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference generator, seeded; each GPU generates "
+                                                          "its block of the stream on the device)",
+            "config": dict(_config(world, args.pr_variant, n_total),
                            **({"fallback_from": args.fallback_from} if getattr(args, "fallback_from", None) else {})),
             "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_total,
                     "d2h_bytes_per_step": 4 * n_total, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
-            "nvlink_all_to_all_ms_per_step": a2a_max, "nvlink_share_of_step": a2a_max / ms_max,
+            "phases_ms_per_step": {"count_and_count_allgather": cnt_max,
+                                   ("fused_pass_and_barrier" if args.pr_variant == "P" else "all_to_all_v"): a2a_max,
+                                   **({"same_passes_local_stores_only": local_max} if args.pr_variant == "P" else {})},
+            "nvlink_all_to_all_ms_per_step": (max(0.0, a2a_max - local_max) if args.pr_variant == "P" else a2a_max),
+            "nvlink_share_of_step": (max(0.0, a2a_max - local_max) if args.pr_variant == "P" else a2a_max) / ms_max,
+            "nvlink_share_how": ("fused pass + barrier minus the same fused-round kernel as a one-worker round "
+                                 "(same block, all stores local)"
+                                 if args.pr_variant == "P" else "CUDA events around the NCCL all-to-all-v"),
+            "nvlink_bytes_per_step": remote,
             "clocks": clk.summary(), "verified": ok,
         }
         print(json.dumps(line), flush=True)
@@ -499,7 +555,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU")
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys (single GPU)")
+    ap.add_argument("--n-total", type=int, default=N_TOTAL_C5, help="config 5 keys over all GPUs (N > 1)")
     ap.add_argument("--ref-n", type=int, default=0, help="keys per reference step (default: config 2's 2^28)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-inflight", type=int, default=4,

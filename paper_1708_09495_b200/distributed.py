@@ -183,13 +183,15 @@ def _all_gather_counts(counts: torch.Tensor, p: int, group) -> torch.Tensor:
 
 def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rounds: Optional[int] = None,
                         group=None, ops=None, a2a_events: Optional[list] = None, exchange: str = "nccl",
-                        peer: Optional[PeerBlocks] = None) -> torch.Tensor:
+                        peer: Optional[PeerBlocks] = None, count_events: Optional[list] = None) -> torch.Tensor:
     """Sorts the globally block-distributed array (rank w holds the keys at
     Partition(n_total, p).offset_of(w) .. +size_of(w), radix.hpp:96-118).
     Returns this rank's block of the sorted array (int32 bit patterns of the
     uint32 keys).  `rounds` < 32/lg r stops early (plan.rounds override).
     If `a2a_events` is a list, CUDA event pairs around each all-to-all are
-    appended to it (NVLink share of the step)."""
+    appended to it (NVLink share of the step); with exchange="peer" they
+    bracket the fused pass + round barrier.  `count_events` likewise brackets
+    each round's digit count + count all-gather."""
     bits = checked_digit_bits(radix)
     p = dist.get_world_size(group)
     me = dist.get_rank(group)
@@ -203,13 +205,15 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
     all_rounds = 32 // bits
     rounds = all_rounds if rounds is None else max(0, min(int(rounds), all_rounds))
     if exchange == "peer":
-        return _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_events, peer)
+        return _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_events, peer, count_events)
     if exchange != "nccl":
         raise ValueError(f"exchange must be 'nccl' or 'peer', not {exchange!r}")
     for rnd in range(rounds):
+        c0 = _event(count_events, block)
         counts = ops.count(block, rnd, bits)
         counts_all = torch.empty(p * counts.numel(), dtype=counts.dtype, device=counts.device)
         dist.all_gather_into_tensor(counts_all, counts, group=group)
+        _close(count_events, c0)
         sorted_ = ops.local_sort(block, rnd, bits)
         send, recv, recv_dev, delta = ops.plan(counts_all, n_total, p, me, rnd, bits)
         recv_buf = ops.keys(sum(recv))
@@ -224,7 +228,22 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
     return block
 
 
-def _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_events, peer):
+def _event(lst, block):
+    if lst is None or not block.is_cuda:
+        return None
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def _close(lst, e0):
+    if e0 is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        lst.append((e0, e1))
+
+
+def _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_events, peer, count_events=None):
     p = dist.get_world_size(group)
     me = dist.get_rank(group)
     if peer is None:
@@ -233,8 +252,10 @@ def _parallel_radix_sort_peer(block, n_total, bits, rounds, group, ops, a2a_even
         raise ValueError("PeerBlocks were mapped for a different (n, p)")
     size = partition_size_of(n_total, p, me)
     for rnd in range(rounds):
+        c0 = _event(count_events, block)
         counts = ops.count(block, rnd, bits)
         counts_all = _all_gather_counts(counts, p, group)
+        _close(count_events, c0)
         b = rnd % 2
         if a2a_events is not None and block.is_cuda:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
