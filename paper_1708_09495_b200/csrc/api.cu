@@ -338,14 +338,10 @@ int bsg_count_sort_round_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         if (radix_log2 <= 8) {
             l = launch_count_pass(d_in, d_out, n, radix_log2, round * radix_log2, ws, s, true);
         } else {
-            // stable 16-bit digit pass = stable pass on its low byte, then on
-            // its high byte, ping-ponging through stage_b.
-            cudaError_t e = ctx->stage_b.ensure(std::max<uint64_t>(n, 4) * 4);
-            if (e != cudaSuccess) return cuda_fail(e, "workspace");
-            uint32_t* mid = ctx->stage_b.as<uint32_t>();
-            const int l1 = launch_count_pass(d_in, mid, n, 8, 16 * round, ws, s, true);
-            const int l2 = l1 < 0 ? -1 : launch_count_pass(mid, d_out, n, 8, 16 * round + 8, ws, s, true);
-            l = (l1 < 0 || l2 < 0) ? -1 : l1 + l2;
+            // K4: one r = 2^16 round = a stable pass on the digit's low byte,
+            // then on its high byte (stable LSD within the digit), both byte
+            // histograms from ONE read of the input: 4 + 8 + 8 B/key
+            l = launch_byte_passes(d_in, d_out, n, 2 * round, 2, ws, s, true);
         }
         if (l < 0) return cuda_fail(cudaGetLastError(), "count-sort round launch");
         ctx->launches += static_cast<uint64_t>(l);

@@ -1398,29 +1398,47 @@ uint64_t onesweep_status_words(uint64_t n) {
 
 int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws,
                        cudaStream_t stream, bool allow_tma) {
-    constexpr int PASSES = 4;
+    return launch_byte_passes(in, out, n, 0, 4, ws, stream, allow_tma);
+}
+
+// `passes` stable 8-bit passes over bytes first_byte .. first_byte+passes-1:
+// ONE histogram read for all of them (digit histograms are properties of the
+// multiset, so every pass's bases come from the input), one scan/plan, the
+// passes ping-ponging through ws.tmp.  passes = 4: the full sort (SR4, and
+// the r = 2^16 sort as 2 rounds x 2 byte sub-passes); passes = 2: one
+// r = 2^16 count-sort round (radix.hpp:44-65 at r = 65536) at 20 B/key.
+int launch_byte_passes(const uint32_t* in, uint32_t* out, uint64_t n, int first_byte, int passes,
+                       const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma) {
     constexpr int RADIX = 256;
     const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
     int launches = 0;
-    {
+    if (passes == 4 && first_byte == 0) {
         const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
         const int l = launch_small_sort(in, out, n, ws, stream, tma);
         if (l != 0) return l;
     }
-    if (cudaMemsetAsync(ws.hist, 0, chunks * PASSES * RADIX * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    if (passes < 1 || passes > 4 || first_byte + passes > 4) return -1;
+    if (cudaMemsetAsync(ws.hist, 0, chunks * passes * RADIX * sizeof(uint32_t), stream) != cudaSuccess) return -1;
     for (uint64_t c = 0; c < chunks && n; ++c) {
         const uint64_t off = c * kChunkKeys;
         const uint64_t len = std::min<uint64_t>(kChunkKeys, n - off);
         TimedScope ts(1 /*BSG_K_HIST*/, stream);
-        launch_hist<8, PASSES>(in + off, len, 0, ws.hist + c * PASSES * RADIX, stream);
+        uint32_t* h = ws.hist + c * passes * RADIX;
+        switch (passes) {
+        case 1: launch_hist<8, 1>(in + off, len, 8 * first_byte, h, stream); break;
+        case 2: launch_hist<8, 2>(in + off, len, 8 * first_byte, h, stream); break;
+        case 3: launch_hist<8, 3>(in + off, len, 8 * first_byte, h, stream); break;
+        default: launch_hist<8, 4>(in + off, len, 8 * first_byte, h, stream); break;
+        }
         ++launches;
     }
-    scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), PASSES, RADIX, n, ws.base,
+    scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), passes, RADIX, n, ws.base,
                                                      ws.plan, in, out, ws.tmp, 1);
     ++launches;
     const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
-    for (int p = 0; p < PASSES && n; ++p) {
-        const int l = launch_onesweep_pass<8>(ws.plan, p, n, 8 * p, ws.base + p * RADIX, PASSES, ws.status, stream, tma);
+    for (int p = 0; p < passes && n; ++p) {
+        const int l = launch_onesweep_pass<8>(ws.plan, p, n, 8 * (first_byte + p), ws.base + p * RADIX, passes,
+                                              ws.status, stream, tma);
         if (l < 0) return -1;
         launches += l;
     }
