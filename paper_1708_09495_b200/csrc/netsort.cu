@@ -35,6 +35,9 @@ constexpr int kMK = BSG_NET_MK;
 #ifndef BSG_NET_MINB
 #define BSG_NET_MINB 5
 #endif
+#ifndef BSG_NET_REG
+#define BSG_NET_REG 1 // register/shuffle network for power-of-two block lengths >= 16
+#endif
 #ifndef BSG_NET_SORT32
 #define BSG_NET_SORT32 1
 #endif // outputs per thread-chunk of the shared-memory merges
@@ -381,6 +384,280 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register block network (block length L a power of two, 16 <= L, p*L <=
+// kNetMaxPadded).  Every thread holds 16 consecutive keys of the CTA's key
+// space in registers for the whole run; only the exchanges between threads of
+// different warps go through shared memory.
+//
+// All networks are written in the "ascending only" bitonic form: phase k of
+// the local sort first compares element e with its mirror e ^ (k-1) inside
+// the k-group, then e with e ^ j for j = k/4 .. 1; the lower index always
+// keeps the minimum.  A merge_split stage (netsort.hpp:30-51) is the same
+// mirror step between worker i's block and its partner's block (the keep_low
+// worker keeps min(own[k], partner[L-1-k]), the other the max: the L smallest
+// resp. largest keys of the pair, as a bitonic sequence) followed by the
+// bitonic merge j = L/2 .. 1.  Only key values move, so which of two equal
+// keys is taken cannot change a block state.  An idle OET edge worker runs
+// the merge steps on its sorted block, which leaves it unchanged.
+//
+// Partner distances by element bit: < 16 inside the thread's registers, 16 ..
+// 511 a warp shuffle, >= 512 a shared-memory exchange (double-buffered, one
+// barrier each).  Shared-memory chunks are swizzled so that every quarter warp
+// of 128-bit accesses hits 8 distinct 16-byte bank groups.
+// ---------------------------------------------------------------------------
+constexpr int kRK = 16;
+
+__device__ __forceinline__ uint32_t minmax_sel(uint32_t a, uint32_t b, bool up) { return up ? max(a, b) : min(a, b); }
+
+__device__ __forceinline__ uint32_t rslot(uint32_t t, int c) { return t * 4u + (static_cast<uint32_t>(c) ^ ((t >> 1) & 3u)); }
+
+__device__ __forceinline__ void put16(uint4* S, uint32_t t, const uint32_t (&v)[kRK]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) S[rslot(t, c)] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+__device__ __forceinline__ void get16(const uint4* S, uint32_t t, uint32_t (&x)[kRK]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint4 q = S[rslot(t, c)];
+        x[4 * c] = q.x;
+        x[4 * c + 1] = q.y;
+        x[4 * c + 2] = q.z;
+        x[4 * c + 3] = q.w;
+    }
+}
+// x[r] = thread t's key 15 - r
+__device__ __forceinline__ void get16_rev(const uint4* S, uint32_t t, uint32_t (&x)[kRK]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint4 q = S[rslot(t, 3 - c)];
+        x[4 * c] = q.w;
+        x[4 * c + 1] = q.z;
+        x[4 * c + 2] = q.y;
+        x[4 * c + 3] = q.x;
+    }
+}
+
+// bitonic merge steps j = 8, 4, 2, 1 inside the thread (ascending)
+__device__ __forceinline__ void reg_merge16(uint32_t (&v)[kRK]) {
+#pragma unroll
+    for (int j = 8; j >= 1; j >>= 1)
+#pragma unroll
+        for (int r = 0; r < kRK; ++r)
+            if ((r & j) == 0) cas(v[r], v[r + j]);
+}
+
+// Shared-memory exchange buffers of a CTA (two, used alternately: one
+// barrier per exchange).
+struct RegNet {
+    uint4* S;        // two buffers of blockDim.x * 4 chunks
+    uint32_t stride; // chunks per buffer
+    uint32_t b = 0;
+    uint32_t t;
+
+    // x = thread tp's keys (reversed if REV)
+    template <bool REV>
+    __device__ __forceinline__ void exchange(const uint32_t (&v)[kRK], uint32_t tp, uint32_t (&x)[kRK]) {
+        uint4* buf = S + b;
+        put16(buf, t, v);
+        __syncthreads();
+        if (REV) get16_rev(buf, tp, x);
+        else get16(buf, tp, x);
+        b ^= stride;
+    }
+    // compare with thread t ^ TM, same register; the lower thread keeps the min
+    template <uint32_t TM>
+    __device__ __forceinline__ void cross_step(uint32_t (&v)[kRK]) {
+        const bool up = (t & TM) != 0;
+        if constexpr (TM < 32) {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r) v[r] = minmax_sel(v[r], __shfl_xor_sync(0xffffffffu, v[r], TM), up);
+        } else {
+            uint32_t x[kRK];
+            exchange<false>(v, t ^ TM, x);
+            if (up) {
+#pragma unroll
+                for (int r = 0; r < kRK; ++r) v[r] = max(v[r], x[r]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < kRK; ++r) v[r] = min(v[r], x[r]);
+            }
+        }
+    }
+    // mirror step of a group of 2*HALF threads (k = 32*HALF keys): thread t
+    // pairs with t ^ (2*HALF-1), register r with 15-r
+    template <uint32_t HALF>
+    __device__ __forceinline__ void mirror_step(uint32_t (&v)[kRK]) {
+        constexpr uint32_t TM = 2 * HALF - 1;
+        const bool up = (t & HALF) != 0;
+        if constexpr (TM < 32) {
+#pragma unroll
+            for (int r = 0; r < kRK / 2; ++r) {
+                const uint32_t xa = __shfl_xor_sync(0xffffffffu, v[kRK - 1 - r], TM);
+                const uint32_t xb = __shfl_xor_sync(0xffffffffu, v[r], TM);
+                v[r] = minmax_sel(v[r], xa, up);
+                v[kRK - 1 - r] = minmax_sel(v[kRK - 1 - r], xb, up);
+            }
+        } else {
+            uint32_t x[kRK];
+            exchange<true>(v, t ^ TM, x);
+            if (up) {
+#pragma unroll
+                for (int r = 0; r < kRK; ++r) v[r] = max(v[r], x[r]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < kRK; ++r) v[r] = min(v[r], x[r]);
+            }
+        }
+    }
+    // bitonic merge steps with thread distances TM, TM/2, .., 1, then in-thread
+    template <uint32_t TM>
+    __device__ __forceinline__ void merge_from(uint32_t (&v)[kRK]) {
+        if constexpr (TM >= 1) {
+            cross_step<TM>(v);
+            merge_from<TM / 2>(v);
+        } else {
+            reg_merge16(v);
+        }
+    }
+    // local-sort phases k = 32*HALF .. 16*SPT
+    template <uint32_t HALF, uint32_t SPT>
+    __device__ __forceinline__ void sort_phases(uint32_t (&v)[kRK]) {
+        if constexpr (2 * HALF <= SPT) {
+            mirror_step<HALF>(v);
+            merge_from<HALF / 2>(v);
+            sort_phases<2 * HALF, SPT>(v);
+        }
+    }
+};
+
+template <int kThreads, int MINB, int LOGL>
+__global__ void __launch_bounds__(kThreads, MINB)
+    block_network_reg_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t num_arrays,
+                             uint32_t len, int p, int network, int run_stages, int full, int apc, int vec_in,
+                             int vec_out) {
+    extern __shared__ __align__(16) uint4 reg_smem[];
+    constexpr uint32_t L = 1u << LOGL;
+    constexpr uint32_t spt = L / kRK; // threads per block (worker)
+    RegNet net;
+    net.t = threadIdx.x;
+    net.S = reg_smem;
+    net.stride = blockDim.x * 4;
+    const uint32_t t = threadIdx.x;
+    const uint32_t P = L * static_cast<uint32_t>(p);
+    const uint64_t array0 = static_cast<uint64_t>(blockIdx.x) * apc;
+    const uint32_t na = static_cast<uint32_t>(min(static_cast<uint64_t>(apc), num_arrays - array0));
+    const uint32_t seg = t / spt;     // worker block of this thread in the CTA
+    const uint32_t c = t % spt;       // chunk inside the block
+    const uint32_t a = seg / static_cast<uint32_t>(p);
+    const int i = static_cast<int>(seg - a * static_cast<uint32_t>(p));
+    const uint32_t o = static_cast<uint32_t>(i) * L + c * kRK; // offset in the (padded) array
+    const bool live = a < na;
+
+    // prepare_blocks: load + pad (netsort.hpp:131-139)
+    uint32_t v[kRK];
+    {
+        const uint32_t* src = in + (array0 + a) * len + o;
+        if (live && vec_in) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (o + 4 * q < len) {
+                    const uint4 w = __ldg(reinterpret_cast<const uint4*>(src) + q);
+                    v[4 * q] = w.x;
+                    v[4 * q + 1] = w.y;
+                    v[4 * q + 2] = w.z;
+                    v[4 * q + 3] = w.w;
+                } else {
+                    v[4 * q] = v[4 * q + 1] = v[4 * q + 2] = v[4 * q + 3] = kPad;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r) v[r] = (live && o + r < len) ? __ldg(src + r) : kPad;
+        }
+    }
+
+    // superstep 0: local sort of every block (16-key Batcher network, then
+    // the bitonic phases k = 32 .. L)
+    sort16(v);
+    net.sort_phases<1, spt>(v);
+
+    // supersteps 1..S: merge_split stages
+    for (int s = 0; s < run_stages; ++s) {
+        bool keep_low = false;
+        const int q = !live ? -1 : (network == 0 ? btn_partner(s, i, keep_low) : oet_partner(s, i, p, keep_low));
+        uint32_t x[kRK];
+        net.exchange<true>(v, (seg - static_cast<uint32_t>(i) + static_cast<uint32_t>(max(q, 0))) * spt + (spt - 1 - c),
+                           x);
+        // the keep_low worker keeps the L smallest keys of the pair, the other
+        // the L largest (warp-uniform for blocks of >= 512 keys)
+        const bool lo = q >= 0 && keep_low, hi = q >= 0 && !keep_low;
+        if (__all_sync(0xffffffffu, lo)) {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r) v[r] = min(v[r], x[r]);
+        } else if (__all_sync(0xffffffffu, hi)) {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r) v[r] = max(v[r], x[r]);
+        } else if (q >= 0) {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r) v[r] = minmax_sel(v[r], x[r], !keep_low);
+        }
+        net.merge_from<spt / 2>(v);
+    }
+
+    // concatenate (+ strip the pad when the network ran to completion)
+    if (!live) return;
+    if (full) {
+        uint32_t* dst = out + (array0 + a) * len + o;
+        if (vec_out) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (o + 4 * q < len)
+                    reinterpret_cast<uint4*>(dst)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r)
+                if (o + r < len) dst[r] = v[r];
+        }
+    } else {
+        uint32_t* dst = out + (array0 + a) * P + o;
+        if (vec_out) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                reinterpret_cast<uint4*>(dst)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < kRK; ++r) dst[r] = v[r];
+        }
+    }
+}
+
+template <int kThreads, int MINB, int LOGL>
+int launch_reg_network(const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p, int network,
+                       int run_stages, int full, int apc, int vec_in, int vec_out, unsigned grid, unsigned threads,
+                       cudaStream_t stream) {
+    static PerDeviceOccupancy occ;
+    kernel_occupancy(occ, block_network_reg_kernel<kThreads, MINB, LOGL>, kThreads, 2 * kThreads * kRK * 4);
+    block_network_reg_kernel<kThreads, MINB, LOGL><<<grid, threads, 2 * threads * kRK * 4, stream>>>(
+        in, out, num_arrays, len, p, network, run_stages, full, apc, vec_in, vec_out);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <int kThreads, int MINB, int LOGL = 4>
+int dispatch_reg_network(int logl, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p,
+                         int network, int run_stages, int full, int apc, int vec_in, int vec_out, unsigned grid,
+                         unsigned threads, cudaStream_t stream) {
+    if constexpr ((1 << LOGL) > kThreads * kRK) {
+        return -1;
+    } else {
+        if (logl == LOGL)
+            return launch_reg_network<kThreads, MINB, LOGL>(in, out, num_arrays, len, p, network, run_stages, full, apc,
+                                                            vec_in, vec_out, grid, threads, stream);
+        return dispatch_reg_network<kThreads, MINB, LOGL + 1>(logl, in, out, num_arrays, len, p, network, run_stages,
+                                                              full, apc, vec_in, vec_out, grid, threads, stream);
+    }
+}
+
 constexpr int kMsThreads = 256;
 
 __global__ void __launch_bounds__(kMsThreads)
@@ -452,7 +729,28 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     const uint32_t P = L * static_cast<uint32_t>(p);
     if (P == 0 || P > kNetMaxPadded) return -1;
     const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
-    const size_t padded = static_cast<size_t>(apc) * P + (static_cast<size_t>(apc) * P >> 5) + 1;
+    if (BSG_NET_REG && L >= kRK && (L & (L - 1)) == 0) {
+        // register network: 16 keys per thread, one CTA per apc arrays
+        const uint64_t grid = (num_arrays + apc - 1) / apc;
+        if (grid > 0x7FFFFFFFull) return -1;
+        const uint32_t threads = ((static_cast<uint32_t>(apc) * P / kRK) + 31u) & ~31u;
+        const int vec_in = (len % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
+        const int vec_out = (len % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
+        int logl = 0;
+        while ((1u << logl) < L) ++logl;
+        TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
+        const unsigned g = static_cast<unsigned>(grid);
+        const int f = full ? 1 : 0;
+        if (threads <= 256)
+            return dispatch_reg_network<256, 4>(logl, in, out, num_arrays, len, p, network, run_stages, f, apc, vec_in,
+                                                vec_out, g, threads, stream);
+        if (threads <= 512)
+            return dispatch_reg_network<512, 2>(logl, in, out, num_arrays, len, p, network, run_stages, f, apc, vec_in,
+                                                vec_out, g, threads, stream);
+        return dispatch_reg_network<1024, 1>(logl, in, out, num_arrays, len, p, network, run_stages, f, apc, vec_in,
+                                             vec_out, g, threads, stream);
+    }
+    const size_t padded =static_cast<size_t>(apc) * P + (static_cast<size_t>(apc) * P >> 5) + 1;
     const size_t smem = 2ull * padded * sizeof(uint32_t);
     const uint64_t grid = (num_arrays + apc - 1) / apc;
     if (grid > 0x7FFFFFFFull) return -1;

@@ -28,7 +28,7 @@ if ok is None:
 ts.sort(); print("RESULT", min(ts), ts[len(ts) // 2], ok)
 '''
 
-repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+repo = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 res = {}
 for rnd in range(int(os.environ.get("AB_ROUNDS", "3"))):
     for spec in sys.argv[1:]:

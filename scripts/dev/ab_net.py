@@ -24,7 +24,7 @@ for net in (0, 1):
         ok = bool(torch.equal(out.view(torch.int32).to(torch.int64).view(num, ln) & 0xFFFFFFFF, ref))
         print("RESULT", net, p, min(ts), ok)
 '''
-repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+repo = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 for rnd in range(2):
     for lib in sys.argv[1:]:
         env = dict(os.environ, REPO=repo, BSG_LIB=os.path.abspath(lib))

@@ -1,6 +1,6 @@
 """Quick GPU timing probe (development aid, not the bench contract)."""
 import sys, os, time, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 import paper_1708_09495_b200 as bsg

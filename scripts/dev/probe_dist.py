@@ -1,7 +1,7 @@
 """Times distributed.parallel_radix_sort (variant A) per radix on this rank's
 block (development aid; world size from torchrun, default 1)."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch, torch.distributed as dist
 import paper_1708_09495_b200 as bsg
 from paper_1708_09495_b200 import distributed as D

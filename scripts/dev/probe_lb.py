@@ -1,6 +1,6 @@
 """Look-back statistics of one 2^28-key pass (needs a build with -DBSG_LB_STATS=1)."""
 import sys, os, ctypes
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_1708_09495_b200 import _lib
 n = 1 << int(os.environ.get("LGN", "28"))

@@ -1,7 +1,7 @@
 """Times one 8-bit count-sort pass and a full SR4 sort at 2^28 (config/dbg via env)."""
 import sys, os, faulthandler
 faulthandler.dump_traceback_later(int(os.environ.get("PROBE_TO", "45")), exit=True)
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_1708_09495_b200 as bsg
 from paper_1708_09495_b200 import _lib

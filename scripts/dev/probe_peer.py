@@ -1,6 +1,6 @@
 """Times the fused peer-store PR4 round path (variant P) with one rank (development aid)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, torch.distributed as dist
 import paper_1708_09495_b200 as bsg
 from paper_1708_09495_b200 import distributed as D

@@ -1,7 +1,7 @@
 """One-sweep phase breakdown (BSG_OS_DBG=8): cycles per phase summed over CTAs."""
 import sys, os, ctypes
 os.environ["BSG_OS_DBG"] = str(int(os.environ.get("BSG_OS_DBG", "0")) | 8)
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_1708_09495_b200 import _lib
 n = 1 << int(os.environ.get("LGN", "28"))

@@ -1,6 +1,6 @@
 """In-process PR timing at one (n, p, radix) (development aid)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_1708_09495_b200 as bsg
 from paper_1708_09495_b200 import _lib

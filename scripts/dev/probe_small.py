@@ -1,6 +1,6 @@
 """Small-n SR4 latency probe: CUDA-event time per sort (development aid)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_1708_09495_b200 as bsg
 from paper_1708_09495_b200 import _lib

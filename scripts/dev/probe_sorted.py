@@ -1,6 +1,6 @@
 """Sort time of structured 2^28 inputs (sorted, reverse-sorted, runs) -- development aid."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_1708_09495_b200 import _lib
 n = 1 << 28
