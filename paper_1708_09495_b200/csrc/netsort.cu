@@ -38,6 +38,9 @@ constexpr int kMK = BSG_NET_MK;
 #ifndef BSG_NET_REG
 #define BSG_NET_REG 1 // register/shuffle network for power-of-two block lengths >= 16
 #endif
+#ifndef BSG_NET_FMA_SORT16
+#define BSG_NET_FMA_SORT16 1 // register network: sort16 maxima on the FMA pipe
+#endif
 #ifndef BSG_NET_SORT32
 #define BSG_NET_SORT32 1
 #endif // outputs per thread-chunk of the shared-memory merges
@@ -60,71 +63,33 @@ __device__ __forceinline__ void cas(uint32_t& a, uint32_t& b) {
 
 // Batcher's odd-even merge sort network on 16 registers (63 comparators,
 // generated and checked against all 2^16 zero-one inputs).
-__device__ __forceinline__ void sort16(uint32_t (&v)[16]) {
-    cas(v[0], v[1]);
-    cas(v[2], v[3]);
-    cas(v[4], v[5]);
-    cas(v[6], v[7]);
-    cas(v[8], v[9]);
-    cas(v[10], v[11]);
-    cas(v[12], v[13]);
-    cas(v[14], v[15]);
-    cas(v[0], v[2]);
-    cas(v[1], v[3]);
-    cas(v[4], v[6]);
-    cas(v[5], v[7]);
-    cas(v[8], v[10]);
-    cas(v[9], v[11]);
-    cas(v[12], v[14]);
-    cas(v[13], v[15]);
-    cas(v[1], v[2]);
-    cas(v[5], v[6]);
-    cas(v[9], v[10]);
-    cas(v[13], v[14]);
-    cas(v[0], v[4]);
-    cas(v[1], v[5]);
-    cas(v[2], v[6]);
-    cas(v[3], v[7]);
-    cas(v[8], v[12]);
-    cas(v[9], v[13]);
-    cas(v[10], v[14]);
-    cas(v[11], v[15]);
-    cas(v[2], v[4]);
-    cas(v[3], v[5]);
-    cas(v[10], v[12]);
-    cas(v[11], v[13]);
-    cas(v[1], v[2]);
-    cas(v[3], v[4]);
-    cas(v[5], v[6]);
-    cas(v[9], v[10]);
-    cas(v[11], v[12]);
-    cas(v[13], v[14]);
-    cas(v[0], v[8]);
-    cas(v[1], v[9]);
-    cas(v[2], v[10]);
-    cas(v[3], v[11]);
-    cas(v[4], v[12]);
-    cas(v[5], v[13]);
-    cas(v[6], v[14]);
-    cas(v[7], v[15]);
-    cas(v[4], v[8]);
-    cas(v[5], v[9]);
-    cas(v[6], v[10]);
-    cas(v[7], v[11]);
-    cas(v[2], v[4]);
-    cas(v[3], v[5]);
-    cas(v[6], v[8]);
-    cas(v[7], v[9]);
-    cas(v[10], v[12]);
-    cas(v[11], v[13]);
-    cas(v[1], v[2]);
-    cas(v[3], v[4]);
-    cas(v[5], v[6]);
-    cas(v[7], v[8]);
-    cas(v[9], v[10]);
-    cas(v[11], v[12]);
-    cas(v[13], v[14]);
+__device__ constexpr uint8_t kSort16[63][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}, {8, 9}, {10, 11}, {12, 13}, {14, 15}, {0, 2}, {1, 3}, {4, 6}, {5, 7}, {8, 10}, {9, 11}, {12, 14}, {13, 15}, {1, 2}, {5, 6}, {9, 10}, {13, 14}, {0, 4}, {1, 5}, {2, 6}, {3, 7}, {8, 12}, {9, 13}, {10, 14}, {11, 15}, {2, 4}, {3, 5}, {10, 12}, {11, 13}, {1, 2}, {3, 4}, {5, 6}, {9, 10}, {11, 12}, {13, 14}, {0, 8}, {1, 9}, {2, 10}, {3, 11}, {4, 12}, {5, 13}, {6, 14}, {7, 15}, {4, 8}, {5, 9}, {6, 10}, {7, 11}, {2, 4}, {3, 5}, {6, 8}, {7, 9}, {10, 12}, {11, 13}, {1, 2}, {3, 4}, {5, 6}, {7, 8}, {9, 10}, {11, 12}, {13, 14}};
+template <typename Cas>
+__device__ __forceinline__ void sort16(uint32_t (&v)[16], const Cas& c) {
+#pragma unroll
+    for (int k = 0; k < 63; ++k) c(v[kSort16[k][0]], v[kSort16[k][1]]);
 }
+struct CasAlu {
+    __device__ __forceinline__ void operator()(uint32_t& a, uint32_t& b) const { cas(a, b); }
+};
+__device__ __forceinline__ void sort16(uint32_t (&v)[16]) { sort16(v, CasAlu{}); }
+
+// Compare-exchange with the maximum on the FMA pipe: hi = a + b - min(a, b)
+// (exact mod 2^32) as two IMADs.  `one` = 1 and `neg1` = -1 are runtime values
+// so that ptxas keeps the IMADs instead of folding them into an IADD3 on the
+// integer ALU pipe, which min/max already saturate.
+struct CasFma {
+    uint32_t one;
+    uint32_t neg1;
+    __device__ __forceinline__ void operator()(uint32_t& a, uint32_t& b) const {
+        const uint32_t lo = min(a, b);
+        uint32_t s, hi;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(a), "r"(one), "r"(b));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"(lo), "r"(neg1), "r"(s));
+        a = lo;
+        b = hi;
+    }
+};
 
 // Shared-memory index with one pad word per 32: the stride-4/stride-8 access
 // patterns of merge-path chunks (8 outputs per lane) become conflict-free.
@@ -386,181 +351,269 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
 
 // ---------------------------------------------------------------------------
 // Register block network (block length L a power of two, 16 <= L, p*L <=
-// kNetMaxPadded).  Every thread holds 16 consecutive keys of the CTA's key
-// space in registers for the whole run; only the exchanges between threads of
-// different warps go through shared memory.
+// kNetMaxPadded).  Every thread holds R (16 or 32) consecutive keys of the
+// CTA's key space in registers for the whole run.
 //
 // All networks are written in the "ascending only" bitonic form: phase k of
-// the local sort first compares element e with its mirror e ^ (k-1) inside
-// the k-group, then e with e ^ j for j = k/4 .. 1; the lower index always
-// keeps the minimum.  A merge_split stage (netsort.hpp:30-51) is the same
-// mirror step between worker i's block and its partner's block (the keep_low
-// worker keeps min(own[k], partner[L-1-k]), the other the max: the L smallest
-// resp. largest keys of the pair, as a bitonic sequence) followed by the
-// bitonic merge j = L/2 .. 1.  Only key values move, so which of two equal
-// keys is taken cannot change a block state.  An idle OET edge worker runs
-// the merge steps on its sorted block, which leaves it unchanged.
+// the local sort first compares key e with its mirror e ^ (k-1) inside the
+// k-group, then e with e ^ j for j = k/4 .. 1; the lower index always keeps
+// the minimum.  A merge_split stage (netsort.hpp:30-51) is the same mirror
+// step between worker i's block and its partner's block (the keep_low worker
+// keeps min(own[k], partner[L-1-k]), the other the max: the L smallest resp.
+// largest keys of the pair, as a bitonic sequence) followed by the bitonic
+// merge j = L/2 .. 1.  Only key values move, so which of two equal keys is
+// taken cannot change a block state.  An idle OET edge worker runs the merge
+// steps on its sorted block, which leaves it unchanged.
 //
-// Partner distances by element bit: < 16 inside the thread's registers, 16 ..
-// 511 a warp shuffle, >= 512 a shared-memory exchange (double-buffered, one
-// barrier each).  Shared-memory chunks are swizzled so that every quarter warp
-// of 128-bit accesses hits 8 distinct 16-byte bank groups.
+// Two register layouts of a warp's 32R keys (e = warp-local key index):
+//   A: lane l holds e = R*l + r: the low log2(R) key bits in registers;
+//   B: lane l holds e = 32*r + l: key bits 5 .. 4+log2(R) in registers.
+// A step on a register bit is one compare-exchange per pair inside the
+// thread; a step on a lane bit costs a shuffle and a select per key (min/max
+// run on the integer ALU pipe, the bound here).  Merges over key bits >= 5
+// inside the warp therefore run in layout B, reached by a warp-local
+// transpose through shared memory (the exchange buffer the next CTA exchange
+// will use: its previous readers are past the last barrier); with R = 16, key
+// bit 4 stays a shuffle in A.  Partner distances beyond the warp go through a
+// CTA exchange (double-buffered, one barrier each).
+//
+// Shared memory holds CTA key E at word E + 4*(E >> 5): 128-bit accesses of A
+// chunks and 32-bit accesses of B rows are both bank-conflict-free, and every
+// address is a per-thread base plus a compile-time offset.
 // ---------------------------------------------------------------------------
-constexpr int kRK = 16;
+#ifndef BSG_NET_R
+#define BSG_NET_R 16 // keys per thread of the register network (16 or 32; 32 measured slower)
+#endif
+#ifndef BSG_NET_BMIN16
+#define BSG_NET_BMIN16 7 // R = 16: merges from key bit >= this run their bits >= 5 in layout B
+#endif
+#ifndef BSG_NET_BMIN32
+#define BSG_NET_BMIN32 5 // R = 32: same
+#endif
+#ifndef BSG_NET_FMA_STEPS
+#define BSG_NET_FMA_STEPS 0xF // register steps (masks) whose maxima go to the FMA pipe
+#endif
 
 __device__ __forceinline__ uint32_t minmax_sel(uint32_t a, uint32_t b, bool up) { return up ? max(a, b) : min(a, b); }
 
-__device__ __forceinline__ uint32_t rslot(uint32_t t, int c) { return t * 4u + (static_cast<uint32_t>(c) ^ ((t >> 1) & 3u)); }
+template <int R>
+struct RegShape {
+    static constexpr int LR = R == 32 ? 5 : 4; // log2 R
+    static constexpr int BMIN = R == 32 ? BSG_NET_BMIN32 : BSG_NET_BMIN16;
+    // word of thread u's key 0
+    static __device__ __forceinline__ uint32_t a_word(uint32_t u) { return R == 32 ? 36u * u : 16u * u + 4u * (u >> 1); }
+};
 
-__device__ __forceinline__ void put16(uint4* S, uint32_t t, const uint32_t (&v)[kRK]) {
+template <int R>
+__device__ __forceinline__ void put_a(uint32_t* S, uint32_t u, const uint32_t (&v)[R]) {
+    uint4* p = reinterpret_cast<uint4*>(S + RegShape<R>::a_word(u));
 #pragma unroll
-    for (int c = 0; c < 4; ++c) S[rslot(t, c)] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    for (int c = 0; c < R / 4; ++c) p[c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
 }
-__device__ __forceinline__ void get16(const uint4* S, uint32_t t, uint32_t (&x)[kRK]) {
+template <int R>
+__device__ __forceinline__ void get_a(const uint32_t* S, uint32_t u, uint32_t (&v)[R]) {
+    const uint4* p = reinterpret_cast<const uint4*>(S + RegShape<R>::a_word(u));
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint4 q = S[rslot(t, c)];
-        x[4 * c] = q.x;
-        x[4 * c + 1] = q.y;
-        x[4 * c + 2] = q.z;
-        x[4 * c + 3] = q.w;
+    for (int c = 0; c < R / 4; ++c) {
+        const uint4 q = p[c];
+        v[4 * c] = q.x;
+        v[4 * c + 1] = q.y;
+        v[4 * c + 2] = q.z;
+        v[4 * c + 3] = q.w;
     }
 }
-// x[r] = thread t's key 15 - r
-__device__ __forceinline__ void get16_rev(const uint4* S, uint32_t t, uint32_t (&x)[kRK]) {
+// v[r] = OP(v[r], thread u's key r) (or key R-1-r if REV)
+template <int R, bool REV, typename Op>
+__device__ __forceinline__ void apply_a(const uint32_t* S, uint32_t u, uint32_t (&v)[R], Op op) {
+    const uint4* p = reinterpret_cast<const uint4*>(S + RegShape<R>::a_word(u));
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint4 q = S[rslot(t, 3 - c)];
-        x[4 * c] = q.w;
-        x[4 * c + 1] = q.z;
-        x[4 * c + 2] = q.y;
-        x[4 * c + 3] = q.x;
+    for (int c = 0; c < R / 4; ++c) {
+        const uint4 q = p[REV ? R / 4 - 1 - c : c];
+        v[4 * c] = op(v[4 * c], REV ? q.w : q.x);
+        v[4 * c + 1] = op(v[4 * c + 1], REV ? q.z : q.y);
+        v[4 * c + 2] = op(v[4 * c + 2], REV ? q.y : q.z);
+        v[4 * c + 3] = op(v[4 * c + 3], REV ? q.x : q.w);
     }
 }
 
-// bitonic merge steps j = 8, 4, 2, 1 inside the thread (ascending)
-__device__ __forceinline__ void reg_merge16(uint32_t (&v)[kRK]) {
+// bitonic steps on register masks J, J/2, .., 1 (ascending); the masks in
+// BSG_NET_FMA_STEPS take their maxima on the FMA pipe
+template <int J, int R>
+__device__ __forceinline__ void reg_steps(uint32_t (&v)[R], const CasFma& f) {
 #pragma unroll
-    for (int j = 8; j >= 1; j >>= 1)
+    for (int j = J; j >= 1; j >>= 1)
 #pragma unroll
-        for (int r = 0; r < kRK; ++r)
-            if ((r & j) == 0) cas(v[r], v[r + j]);
+        for (int r = 0; r < R; ++r)
+            if ((r & j) == 0) {
+                if (BSG_NET_FMA_STEPS & j) f(v[r], v[r + j]);
+                else cas(v[r], v[r + j]);
+            }
 }
 
-// Shared-memory exchange buffers of a CTA (two, used alternately: one
-// barrier per exchange).
+struct OpMin {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return min(a, b); }
+};
+struct OpMax {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return max(a, b); }
+};
+struct OpSel {
+    bool up;
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return minmax_sel(a, b, up); }
+};
+
+template <int R>
 struct RegNet {
-    uint4* S;        // two buffers of blockDim.x * 4 chunks
-    uint32_t stride; // chunks per buffer
-    uint32_t b = 0;
-    uint32_t t;
+    using Sh = RegShape<R>;
+    uint32_t* S;     // two exchange buffers of `stride` words
+    uint32_t stride; // (R + R/8) * blockDim.x words per buffer
+    uint32_t b = 0;  // word offset of the buffer the next exchange uses
+    uint32_t t, lane, warp;
+    CasFma fc;
 
-    // x = thread tp's keys (reversed if REV)
+    // v[r] = OP(v[r], thread tp's key r (REV: R-1-r)), the lower thread of
+    // a pair keeping the min
     template <bool REV>
-    __device__ __forceinline__ void exchange(const uint32_t (&v)[kRK], uint32_t tp, uint32_t (&x)[kRK]) {
-        uint4* buf = S + b;
-        put16(buf, t, v);
+    __device__ __forceinline__ void exchange_step(uint32_t (&v)[R], uint32_t tp, bool up) {
+        uint32_t* buf = S + b;
+        put_a<R>(buf, t, v);
         __syncthreads();
-        if (REV) get16_rev(buf, tp, x);
-        else get16(buf, tp, x);
+        if (up) apply_a<R, REV>(buf, tp, v, OpMax{});
+        else apply_a<R, REV>(buf, tp, v, OpMin{});
         b ^= stride;
     }
-    // compare with thread t ^ TM, same register; the lower thread keeps the min
+    // warp-local transposes A -> B and B -> A
+    __device__ __forceinline__ void to_B(uint32_t (&v)[R]) {
+        uint32_t* buf = S + b;
+        put_a<R>(buf, t, v);
+        __syncwarp();
+        const uint32_t* row = buf + 36u * R * warp + lane;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = row[36 * r];
+        __syncwarp();
+    }
+    __device__ __forceinline__ void to_A(uint32_t (&v)[R]) {
+        uint32_t* buf = S + b;
+        uint32_t* row = buf + 36u * R * warp + lane;
+#pragma unroll
+        for (int r = 0; r < R; ++r) row[36 * r] = v[r];
+        __syncwarp();
+        get_a<R>(buf, t, v);
+        __syncwarp();
+    }
+    // compare with thread t ^ TM, same register
     template <uint32_t TM>
-    __device__ __forceinline__ void cross_step(uint32_t (&v)[kRK]) {
+    __device__ __forceinline__ void cross_step(uint32_t (&v)[R]) {
         const bool up = (t & TM) != 0;
         if constexpr (TM < 32) {
 #pragma unroll
-            for (int r = 0; r < kRK; ++r) v[r] = minmax_sel(v[r], __shfl_xor_sync(0xffffffffu, v[r], TM), up);
+            for (int r = 0; r < R; ++r) v[r] = minmax_sel(v[r], __shfl_xor_sync(0xffffffffu, v[r], TM), up);
         } else {
-            uint32_t x[kRK];
-            exchange<false>(v, t ^ TM, x);
-            if (up) {
-#pragma unroll
-                for (int r = 0; r < kRK; ++r) v[r] = max(v[r], x[r]);
-            } else {
-#pragma unroll
-                for (int r = 0; r < kRK; ++r) v[r] = min(v[r], x[r]);
-            }
+            exchange_step<false>(v, t ^ TM, up);
         }
     }
-    // mirror step of a group of 2*HALF threads (k = 32*HALF keys): thread t
-    // pairs with t ^ (2*HALF-1), register r with 15-r
+    // mirror step of a group of 2*HALF threads: thread t pairs with
+    // t ^ (2*HALF-1), register r with R-1-r
     template <uint32_t HALF>
-    __device__ __forceinline__ void mirror_step(uint32_t (&v)[kRK]) {
+    __device__ __forceinline__ void mirror_step(uint32_t (&v)[R]) {
         constexpr uint32_t TM = 2 * HALF - 1;
         const bool up = (t & HALF) != 0;
         if constexpr (TM < 32) {
 #pragma unroll
-            for (int r = 0; r < kRK / 2; ++r) {
-                const uint32_t xa = __shfl_xor_sync(0xffffffffu, v[kRK - 1 - r], TM);
+            for (int r = 0; r < R / 2; ++r) {
+                const uint32_t xa = __shfl_xor_sync(0xffffffffu, v[R - 1 - r], TM);
                 const uint32_t xb = __shfl_xor_sync(0xffffffffu, v[r], TM);
                 v[r] = minmax_sel(v[r], xa, up);
-                v[kRK - 1 - r] = minmax_sel(v[kRK - 1 - r], xb, up);
+                v[R - 1 - r] = minmax_sel(v[R - 1 - r], xb, up);
             }
         } else {
-            uint32_t x[kRK];
-            exchange<true>(v, t ^ TM, x);
-            if (up) {
-#pragma unroll
-                for (int r = 0; r < kRK; ++r) v[r] = max(v[r], x[r]);
+            exchange_step<true>(v, t ^ TM, up);
+        }
+    }
+    // bitonic merge steps on key bits TOP, TOP-1, .., 0
+    template <int TOP>
+    __device__ __forceinline__ void merge_bits(uint32_t (&v)[R]) {
+        if constexpr (TOP < 0) {
+        } else if constexpr (TOP >= Sh::LR + 5) { // another warp
+            cross_step<(1u << (TOP - Sh::LR))>(v);
+            merge_bits<TOP - 1>(v);
+        } else if constexpr (TOP >= 5 && TOP >= Sh::BMIN) { // bits TOP..5 in layout B
+            to_B(v);
+            reg_steps<(1 << (TOP - 5))>(v, fc);
+            to_A(v);
+            merge_bits<4>(v);
+        } else if constexpr (TOP >= Sh::LR) { // another lane
+            cross_step<(1u << (TOP - Sh::LR))>(v);
+            merge_bits<TOP - 1>(v);
+        } else {
+            reg_steps<(1 << TOP)>(v, fc);
+        }
+    }
+    // in-thread sort of the R keys
+    __device__ __forceinline__ void sort_r(uint32_t (&v)[R]) {
+        if constexpr (R == 16) {
+            if (BSG_NET_FMA_SORT16) sort16(v, fc);
+            else sort16(v);
+        } else {
+            uint32_t(&lo)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[0]);
+            uint32_t(&hi)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[16]);
+            if (BSG_NET_FMA_SORT16) {
+                sort16(lo, fc);
+                sort16(hi, fc);
             } else {
-#pragma unroll
-                for (int r = 0; r < kRK; ++r) v[r] = min(v[r], x[r]);
+                sort16(lo);
+                sort16(hi);
             }
+#pragma unroll
+            for (int r = 0; r < 16; ++r) fc(v[r], v[31 - r]);
+            reg_steps<8>(v, fc);
         }
     }
-    // bitonic merge steps with thread distances TM, TM/2, .., 1, then in-thread
-    template <uint32_t TM>
-    __device__ __forceinline__ void merge_from(uint32_t (&v)[kRK]) {
-        if constexpr (TM >= 1) {
-            cross_step<TM>(v);
-            merge_from<TM / 2>(v);
-        } else {
-            reg_merge16(v);
-        }
-    }
-    // local-sort phases k = 32*HALF .. 16*SPT
-    template <uint32_t HALF, uint32_t SPT>
-    __device__ __forceinline__ void sort_phases(uint32_t (&v)[kRK]) {
-        if constexpr (2 * HALF <= SPT) {
-            mirror_step<HALF>(v);
-            merge_from<HALF / 2>(v);
-            sort_phases<2 * HALF, SPT>(v);
+    // local-sort phases k = 2^M .. 2^LOGL (the first LR phases are sort_r)
+    template <int M, int LOGL>
+    __device__ __forceinline__ void sort_phases(uint32_t (&v)[R]) {
+        if constexpr (M <= LOGL) {
+            mirror_step<(1u << (M - 1 - Sh::LR))>(v);
+            merge_bits<M - 2>(v);
+            sort_phases<M + 1, LOGL>(v);
         }
     }
 };
 
-template <int kThreads, int MINB, int LOGL>
+template <int R, int kThreads, int MINB, int LOGL>
 __global__ void __launch_bounds__(kThreads, MINB)
     block_network_reg_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t num_arrays,
                              uint32_t len, int p, int network, int run_stages, int full, int apc, int vec_in,
-                             int vec_out) {
-    extern __shared__ __align__(16) uint4 reg_smem[];
+                             int vec_out, uint32_t one, uint32_t neg1) {
+    extern __shared__ __align__(16) uint32_t reg_smem[];
+    using Sh = RegShape<R>;
     constexpr uint32_t L = 1u << LOGL;
-    constexpr uint32_t spt = L / kRK; // threads per block (worker)
-    RegNet net;
+    constexpr uint32_t spt = L / R; // threads per block (worker)
+    static_assert(spt >= 1, "block shorter than a thread's keys");
+    RegNet<R> net;
     net.t = threadIdx.x;
+    net.lane = threadIdx.x & 31;
+    net.warp = threadIdx.x >> 5;
+    net.fc = CasFma{one, neg1};
     net.S = reg_smem;
-    net.stride = blockDim.x * 4;
+    net.stride = blockDim.x * (R + R / 8);
     const uint32_t t = threadIdx.x;
     const uint32_t P = L * static_cast<uint32_t>(p);
     const uint64_t array0 = static_cast<uint64_t>(blockIdx.x) * apc;
     const uint32_t na = static_cast<uint32_t>(min(static_cast<uint64_t>(apc), num_arrays - array0));
-    const uint32_t seg = t / spt;     // worker block of this thread in the CTA
-    const uint32_t c = t % spt;       // chunk inside the block
+    const uint32_t seg = t / spt; // worker block of this thread in the CTA
+    const uint32_t c = t % spt;   // chunk inside the block
     const uint32_t a = seg / static_cast<uint32_t>(p);
     const int i = static_cast<int>(seg - a * static_cast<uint32_t>(p));
-    const uint32_t o = static_cast<uint32_t>(i) * L + c * kRK; // offset in the (padded) array
+    const uint32_t o = static_cast<uint32_t>(i) * L + c * R; // offset in the (padded) array
     const bool live = a < na;
 
     // prepare_blocks: load + pad (netsort.hpp:131-139)
-    uint32_t v[kRK];
+    uint32_t v[R];
     {
         const uint32_t* src = in + (array0 + a) * len + o;
         if (live && vec_in) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < R / 4; ++q) {
                 if (o + 4 * q < len) {
                     const uint4 w = __ldg(reinterpret_cast<const uint4*>(src) + q);
                     v[4 * q] = w.x;
@@ -573,36 +626,74 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
         } else {
 #pragma unroll
-            for (int r = 0; r < kRK; ++r) v[r] = (live && o + r < len) ? __ldg(src + r) : kPad;
+            for (int r = 0; r < R; ++r) v[r] = (live && o + r < len) ? __ldg(src + r) : kPad;
         }
     }
 
-    // superstep 0: local sort of every block (16-key Batcher network, then
-    // the bitonic phases k = 32 .. L)
-    sort16(v);
-    net.sort_phases<1, spt>(v);
+    // superstep 0: local sort of every block (in-thread network, then the
+    // bitonic phases k = 2R .. L)
+    net.sort_r(v);
+    net.template sort_phases<Sh::LR + 1, LOGL>(v);
 
-    // supersteps 1..S: merge_split stages
+    // supersteps 1..S: merge_split stages.  BTN stage partners are advanced
+    // incrementally (bitonic_schedule, netsort.hpp:76-88: merge level a,
+    // step jidx of a).
+    int lvl = 1, jidx = 0;
     for (int s = 0; s < run_stages; ++s) {
         bool keep_low = false;
-        const int q = !live ? -1 : (network == 0 ? btn_partner(s, i, keep_low) : oet_partner(s, i, p, keep_low));
-        uint32_t x[kRK];
-        net.exchange<true>(v, (seg - static_cast<uint32_t>(i) + static_cast<uint32_t>(max(q, 0))) * spt + (spt - 1 - c),
-                           x);
-        // the keep_low worker keeps the L smallest keys of the pair, the other
-        // the L largest (warp-uniform for blocks of >= 512 keys)
-        const bool lo = q >= 0 && keep_low, hi = q >= 0 && !keep_low;
-        if (__all_sync(0xffffffffu, lo)) {
-#pragma unroll
-            for (int r = 0; r < kRK; ++r) v[r] = min(v[r], x[r]);
-        } else if (__all_sync(0xffffffffu, hi)) {
-#pragma unroll
-            for (int r = 0; r < kRK; ++r) v[r] = max(v[r], x[r]);
-        } else if (q >= 0) {
-#pragma unroll
-            for (int r = 0; r < kRK; ++r) v[r] = minmax_sel(v[r], x[r], !keep_low);
+        int q = -1;
+        if (live) {
+            if (network == 0) {
+                q = i ^ (1 << (lvl - 1 - jidx));
+                keep_low = ((i >> lvl) & 1) == 0 ? (i < q) : (i > q);
+            } else {
+                q = oet_partner(s, i, p, keep_low);
+            }
         }
-        net.merge_from<spt / 2>(v);
+        if (++jidx == lvl) {
+            ++lvl;
+            jidx = 0;
+        }
+        const uint32_t pseg = seg - static_cast<uint32_t>(i) + static_cast<uint32_t>(max(q, 0)); // partner block
+        // the keep_low worker keeps the L smallest keys of the pair, the other
+        // the L largest (warp-uniform for blocks of >= 32R keys)
+        const bool lo = q >= 0 && keep_low, hi = q >= 0 && !keep_low;
+        constexpr bool DIRECT_B = spt == 32 && Sh::BMIN <= LOGL - 1;
+        if constexpr (DIRECT_B) {
+            // one block per warp: read the own block and the partner's
+            // reversed block straight into layout B
+            uint32_t* buf = net.S + net.b;
+            put_a<R>(buf, t, v);
+            __syncthreads();
+            const uint32_t* own = buf + 36u * R * net.warp + net.lane;
+            const uint32_t* par = buf + 36u * R * pseg + 36u * R - 5u - net.lane;
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = own[36 * r];
+            if (__all_sync(0xffffffffu, lo)) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = min(v[r], par[-36 * r]);
+            } else if (__all_sync(0xffffffffu, hi)) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = max(v[r], par[-36 * r]);
+            } else if (q >= 0) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = minmax_sel(v[r], par[-36 * r], !keep_low);
+            }
+            net.b ^= net.stride;
+            reg_steps<(1 << (LOGL - 6))>(v, net.fc);
+            net.to_A(v);
+            net.template merge_bits<4>(v);
+        } else {
+            uint32_t* buf = net.S + net.b;
+            put_a<R>(buf, t, v);
+            __syncthreads();
+            const uint32_t tp = pseg * spt + (spt - 1 - c);
+            if (__all_sync(0xffffffffu, lo)) apply_a<R, true>(buf, tp, v, OpMin{});
+            else if (__all_sync(0xffffffffu, hi)) apply_a<R, true>(buf, tp, v, OpMax{});
+            else if (q >= 0) apply_a<R, true>(buf, tp, v, OpSel{!keep_low});
+            net.b ^= net.stride;
+            net.template merge_bits<LOGL - 1>(v);
+        }
     }
 
     // concatenate (+ strip the pad when the network ran to completion)
@@ -611,51 +702,79 @@ __global__ void __launch_bounds__(kThreads, MINB)
         uint32_t* dst = out + (array0 + a) * len + o;
         if (vec_out) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < R / 4; ++q)
                 if (o + 4 * q < len)
                     reinterpret_cast<uint4*>(dst)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
 #pragma unroll
-            for (int r = 0; r < kRK; ++r)
+            for (int r = 0; r < R; ++r)
                 if (o + r < len) dst[r] = v[r];
         }
     } else {
         uint32_t* dst = out + (array0 + a) * P + o;
         if (vec_out) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < R / 4; ++q)
                 reinterpret_cast<uint4*>(dst)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
 #pragma unroll
-            for (int r = 0; r < kRK; ++r) dst[r] = v[r];
+            for (int r = 0; r < R; ++r) dst[r] = v[r];
         }
     }
 }
 
-template <int kThreads, int MINB, int LOGL>
+template <int R, int kThreads, int MINB, int LOGL>
 int launch_reg_network(const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p, int network,
                        int run_stages, int full, int apc, int vec_in, int vec_out, unsigned grid, unsigned threads,
                        cudaStream_t stream) {
+    constexpr size_t kWords = R + R / 8; // words per thread per exchange buffer
     static PerDeviceOccupancy occ;
-    kernel_occupancy(occ, block_network_reg_kernel<kThreads, MINB, LOGL>, kThreads, 2 * kThreads * kRK * 4);
-    block_network_reg_kernel<kThreads, MINB, LOGL><<<grid, threads, 2 * threads * kRK * 4, stream>>>(
-        in, out, num_arrays, len, p, network, run_stages, full, apc, vec_in, vec_out);
+    kernel_occupancy(occ, block_network_reg_kernel<R, kThreads, MINB, LOGL>, kThreads, 2 * kThreads * kWords * 4);
+    block_network_reg_kernel<R, kThreads, MINB, LOGL><<<grid, threads, 2 * threads * kWords * 4, stream>>>(
+        in, out, num_arrays, len, p, network, run_stages, full, apc, vec_in, vec_out, 1u, 0xFFFFFFFFu);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <int kThreads, int MINB, int LOGL = 4>
+template <int R, int kThreads, int MINB, int LOGL = 4>
 int dispatch_reg_network(int logl, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p,
                          int network, int run_stages, int full, int apc, int vec_in, int vec_out, unsigned grid,
                          unsigned threads, cudaStream_t stream) {
-    if constexpr ((1 << LOGL) > kThreads * kRK) {
+    if constexpr ((1 << LOGL) > kThreads * R) {
         return -1;
+    } else if constexpr ((1 << LOGL) < R) {
+        return dispatch_reg_network<R, kThreads, MINB, LOGL + 1>(logl, in, out, num_arrays, len, p, network,
+                                                                 run_stages, full, apc, vec_in, vec_out, grid, threads,
+                                                                 stream);
     } else {
         if (logl == LOGL)
-            return launch_reg_network<kThreads, MINB, LOGL>(in, out, num_arrays, len, p, network, run_stages, full, apc,
-                                                            vec_in, vec_out, grid, threads, stream);
-        return dispatch_reg_network<kThreads, MINB, LOGL + 1>(logl, in, out, num_arrays, len, p, network, run_stages,
-                                                              full, apc, vec_in, vec_out, grid, threads, stream);
+            return launch_reg_network<R, kThreads, MINB, LOGL>(in, out, num_arrays, len, p, network, run_stages, full,
+                                                               apc, vec_in, vec_out, grid, threads, stream);
+        return dispatch_reg_network<R, kThreads, MINB, LOGL + 1>(logl, in, out, num_arrays, len, p, network,
+                                                                 run_stages, full, apc, vec_in, vec_out, grid, threads,
+                                                                 stream);
     }
+}
+
+// Register network launch: R keys per thread, one CTA per apc arrays.
+template <int R>
+int launch_reg(int logl, const uint32_t* in, uint32_t* out, uint64_t num_arrays, uint32_t len, int p, uint32_t P,
+               int network, int run_stages, int full, int apc, int vec_in, int vec_out, cudaStream_t stream) {
+    const uint64_t grid = (num_arrays + apc - 1) / apc;
+    if (grid > 0x7FFFFFFFull) return -1;
+    const uint32_t threads = ((static_cast<uint32_t>(apc) * P / R) + 31u) & ~31u;
+    const unsigned g = static_cast<unsigned>(grid);
+    constexpr int T0 = 4096 / R;      // CTA of 4096 keys
+    constexpr int M0 = 1024 / T0;     // CTAs per SM at <= 64 registers
+    if (threads <= T0)
+        return dispatch_reg_network<R, T0, M0>(logl, in, out, num_arrays, len, p, network, run_stages, full, apc,
+                                                vec_in, vec_out, g, threads, stream);
+    if (threads <= 2 * T0)
+        return dispatch_reg_network<R, 2 * T0, (M0 / 2 > 0 ? M0 / 2 : 1)>(logl, in, out, num_arrays, len, p, network,
+                                                                         run_stages, full, apc, vec_in, vec_out, g,
+                                                                         threads, stream);
+    return dispatch_reg_network<R, 4 * T0, (M0 / 4 > 0 ? M0 / 4 : 1)>(logl, in, out, num_arrays, len, p, network,
+                                                                     run_stages, full, apc, vec_in, vec_out, g,
+                                                                     threads, stream);
 }
 
 constexpr int kMsThreads = 256;
@@ -729,26 +848,18 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     const uint32_t P = L * static_cast<uint32_t>(p);
     if (P == 0 || P > kNetMaxPadded) return -1;
     const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
-    if (BSG_NET_REG && L >= kRK && (L & (L - 1)) == 0) {
-        // register network: 16 keys per thread, one CTA per apc arrays
-        const uint64_t grid = (num_arrays + apc - 1) / apc;
-        if (grid > 0x7FFFFFFFull) return -1;
-        const uint32_t threads = ((static_cast<uint32_t>(apc) * P / kRK) + 31u) & ~31u;
+    if (BSG_NET_REG && L >= 16 && (L & (L - 1)) == 0) {
         const int vec_in = (len % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
         const int vec_out = (len % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
         int logl = 0;
         while ((1u << logl) < L) ++logl;
         TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
-        const unsigned g = static_cast<unsigned>(grid);
         const int f = full ? 1 : 0;
-        if (threads <= 256)
-            return dispatch_reg_network<256, 4>(logl, in, out, num_arrays, len, p, network, run_stages, f, apc, vec_in,
-                                                vec_out, g, threads, stream);
-        if (threads <= 512)
-            return dispatch_reg_network<512, 2>(logl, in, out, num_arrays, len, p, network, run_stages, f, apc, vec_in,
-                                                vec_out, g, threads, stream);
-        return dispatch_reg_network<1024, 1>(logl, in, out, num_arrays, len, p, network, run_stages, f, apc, vec_in,
-                                             vec_out, g, threads, stream);
+        if (BSG_NET_R == 32 && L >= 32)
+            return launch_reg<32>(logl, in, out, num_arrays, len, p, P, network, run_stages, f, apc, vec_in, vec_out,
+                                  stream);
+        return launch_reg<16>(logl, in, out, num_arrays, len, p, P, network, run_stages, f, apc, vec_in, vec_out,
+                              stream);
     }
     const size_t padded =static_cast<size_t>(apc) * P + (static_cast<size_t>(apc) * P >> 5) + 1;
     const size_t smem = 2ull * padded * sizeof(uint32_t);
