@@ -174,6 +174,8 @@ class Reference:
         h.ref_time_parallel_radix.restype = ctypes.c_double
         h.ref_time_block_network.argtypes = [i, vp, u64, u64, i, vp]
         h.ref_time_block_network.restype = ctypes.c_double
+        h.ref_time_network_once.argtypes = [i, vp, u64, i, vp]
+        h.ref_time_network_once.restype = ctypes.c_double
 
     def generate_uniform_keys(self, n: int, seed: int) -> np.ndarray:
         out = np.empty(n, dtype=np.uint32)
@@ -256,6 +258,15 @@ class Reference:
         a = _u32(arrays)
         out = np.empty_like(a)
         t = self.h.ref_time_block_network(network, _p(a), a.shape[0], a.shape[1], p, _p(out))
+        if t < 0:
+            raise RuntimeError("reference block network failed")
+        return t, out
+
+    def time_network_once(self, network: int, keys, p: int):
+        """bench.hpp run_once timing of run_block_network (default executor)."""
+        k = _u32(keys)
+        out = np.empty_like(k)
+        t = self.h.ref_time_network_once(network, _p(k), k.size, p, _p(out))
         if t < 0:
             raise RuntimeError("reference block network failed")
         return t, out

@@ -189,6 +189,22 @@ double ref_time_block_network(int network, const std::uint32_t* in, std::uint64_
     }
 }
 
+// bench.hpp:131-137 run_once for BTN/OET: run_block_network with its default
+// executor, timed around the call (bench CSV rows, scripts/bench_csv.py).
+double ref_time_network_once(int network, const std::uint32_t* in, std::uint64_t len, int p, std::uint32_t* out) {
+    try {
+        KeyArray keys(in, in + len);
+        auto prep = network == 0 ? netsort::prepare_btn(keys, p) : netsort::prepare_oet(keys, p);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto res = netsort::run_block_network(std::move(prep));
+        const auto t1 = std::chrono::steady_clock::now();
+        std::memcpy(out, res.output.data(), len * sizeof(std::uint32_t));
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (...) {
+        return -1.0;
+    }
+}
+
 // The 5-way dispatch of bspsort.hpp:15-25 (that header needs Boost).
 // algorithm: 0 SR4, 1 PR4, 2 PR2, 3 BTN, 4 OET (core.hpp:24 order).
 int ref_sort_instance(const std::uint32_t* in, std::uint64_t n, int processors, int algorithm,

@@ -560,11 +560,15 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
     cudaError_t e = ctx->pr_recv.ensure(
         (static_cast<uint64_t>(p) * (1 + chunks) + (uint64_t{2} << radix_log2) + chunks) * sizeof(uint64_t));
     if (e != cudaSuccess) return cuda_fail(e, "pr_plan scratch");
-    const int l = launch_pr_plan(counts, n, p, me, radix_log2, send_counts, recv_counts, rebuild_delta,
-                                 static_cast<cudaStream_t>(stream), ctx->pr_recv.as<uint64_t>());
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* flag = nullptr;
+    if (int rc = proto_begin(ctx, st, &flag)) return rc;
+    if (check_count_rows(counts, p, 1 << radix_log2, n, flag, st) < 0) return cuda_fail(cudaGetLastError(), "pr_plan check");
+    const int l = launch_pr_plan(counts, n, p, me, radix_log2, send_counts, recv_counts, rebuild_delta, st,
+                                 ctx->pr_recv.as<uint64_t>());
     if (l < 0) return cuda_fail(cudaGetLastError(), "pr_plan launch");
-    ctx->launches += static_cast<uint64_t>(l);
-    return BSG_OK;
+    ctx->launches += static_cast<uint64_t>(l) + 1;
+    return proto_end(ctx, st, "bsp_error: a worker's exchanged digit counts do not sum to its block size");
 }
 
 int bsg_ctx_enable_peer_access(bsg_ctx* ctx, int* enabled) {
@@ -599,15 +603,17 @@ int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len, const 
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = radix_bits_or_fail(radix_log2)) return rc;
     if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
-    (void)recv_counts;
-    (void)p;
+    if (p < 1 || !recv_counts || (recv_len && (!recv || !block || !rebuild_delta))) return fail(BSG_EINVAL, "null pointer");
     CallGuard g(ctx);
-    StreamOrder order(ctx, static_cast<cudaStream_t>(stream));
-    const int l = launch_pr_rebuild(recv, recv_len, radix_log2, round * radix_log2, rebuild_delta, block,
-                                    static_cast<cudaStream_t>(stream), recv_counts, p);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(ctx, st);
+    uint32_t* flag = nullptr;
+    if (int rc = proto_begin(ctx, st, &flag)) return rc;
+    const int l = launch_pr_rebuild(recv, recv_len, radix_log2, round * radix_log2, rebuild_delta, block, st,
+                                    recv_counts, p, flag);
     if (l < 0) return cuda_fail(cudaGetLastError(), "rebuild launch");
     ctx->launches += static_cast<uint64_t>(l);
-    return BSG_OK;
+    return proto_end(ctx, st, "bsp_error: received key slices do not fill the rebuilt block");
 }
 
 } // extern "C"

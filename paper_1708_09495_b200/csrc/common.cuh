@@ -2,6 +2,7 @@
 // for relaxed/acquire global accesses, mbarrier + cp.async.bulk (TMA bulk
 // copy), lane masks) and the launch-accounting hook.
 #pragma once
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -30,6 +31,17 @@ inline int kernel_occupancy(PerDeviceOccupancy& cache, K kern, int threads, size
         v = per < 1 ? -1 : per; // -1: does not fit (recorded so it is not re-queried)
     }
     return v;
+}
+// Development knobs (BSG_OS_CFG, BSG_OS_RANK, BSG_SMALL, ...): environment
+// variables are read only in development builds (-DBSG_DEV_KNOBS=1, see
+// scripts/build_variant.sh); the product library always uses the defaults.
+#ifndef BSG_DEV_KNOBS
+#define BSG_DEV_KNOBS 0
+#endif
+inline int dev_knob(const char* name, int def) {
+    if (!BSG_DEV_KNOBS) return def;
+    const char* e = getenv(name);
+    return e ? atoi(e) : def;
 }
 inline int current_sm_count() {
     int dev = 0, sms = kSmCountB200;

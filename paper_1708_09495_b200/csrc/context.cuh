@@ -55,6 +55,7 @@ struct bsg_ctx {
     bsg::DevBuf stage_in, stage_out, stage_b;
     bsg::DevBuf pr_counts, pr_sorted, pr_recv, pr_block, pr_misc, pr_delta;
     bsg::DevBuf net_sched, cnt32;
+    bsg::DevBuf proto; // protocol-check flag word (bsp_error equivalent, pr.cu)
     bsg::DevBuf mt_ws; // device generator: segment start windows + jump polynomials
     // Cross-stream ordering of the shared workspace: every call records
     // `last_use` on its stream; a call on a different stream first waits on

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kRebuildThreads)
     pr_rebuild_kernel(const uint32_t* __restrict__ recv, uint64_t recv_len, int p,
                       const uint64_t* __restrict__ recv_counts,
                       uint32_t mask, int shift, int radix, const int64_t* __restrict__ delta,
-                      uint32_t* __restrict__ block) {
+                      uint32_t* __restrict__ block, uint32_t* __restrict__ proto) {
     __shared__ uint64_t s_off[kMaxP + 1];
     if (threadIdx.x == 0) {
         uint64_t run = 0;
@@ -89,6 +89,8 @@ __global__ void __launch_bounds__(kRebuildThreads)
             run += recv_counts[v];
         }
         s_off[p] = run;
+        // the received slices must fill the block exactly (radix.hpp:207-220)
+        if (run != recv_len && proto && blockIdx.x == 0) atomicOr(proto, 1u);
     }
     __syncthreads();
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kRebuildThreads;
@@ -102,7 +104,12 @@ __global__ void __launch_bounds__(kRebuildThreads)
         const int v = lo;
         const uint32_t key = recv[j];
         const uint32_t d = (key >> shift) & mask;
-        block[static_cast<uint64_t>(delta[static_cast<uint64_t>(v) * radix + d] + static_cast<int64_t>(j))] = key;
+        const int64_t dst = delta[static_cast<uint64_t>(v) * radix + d] + static_cast<int64_t>(j);
+        if (dst < 0 || static_cast<uint64_t>(dst) >= recv_len) { // a slice disagrees with the counts
+            if (proto) atomicOr(proto, 1u);
+            continue;
+        }
+        block[dst] = key;
     }
 }
 
@@ -404,11 +411,33 @@ __global__ void __launch_bounds__(kScatterThreads)
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kScatterThreads + threadIdx.x; i < len; i += step) {
         const uint32_t key = __ldg(sorted + i);
         const uint64_t pos = static_cast<uint64_t>(__ldg(gd + ((key >> shift) & mask)) + static_cast<int64_t>(i));
+        if (pos >= tab.offset[p]) continue; // inconsistent count matrix (reported by the row check)
         int w = 0;
         for (int j = 1; j < p; ++j) w += pos >= tab.offset[j] ? 1 : 0;
         tab.blocks[w][pos - tab.offset[w]] = key;
     }
     __threadfence_system(); // peer stores performed before the round's barrier
+}
+
+// Protocol check of an exchanged count matrix (the reference's bsp_error,
+// radix.hpp:207-220 and 283-286): row v (worker v's digit counts) must sum to
+// Partition(n, p).size_of(v).  One CTA per row; a mismatch sets *flag.
+__global__ void __launch_bounds__(256) pr_check_rows_kernel(const uint64_t* __restrict__ counts, int p, int radix,
+                                                            uint64_t n, uint32_t* __restrict__ flag) {
+    __shared__ uint64_t s_part[8];
+    const int v = blockIdx.x;
+    uint64_t sum = 0;
+    for (int d = threadIdx.x; d < radix; d += 256) sum += counts[static_cast<uint64_t>(v) * radix + d];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t tot = 0;
+        for (int w = 0; w < 8; ++w) tot += s_part[w];
+        const uint64_t want = n / static_cast<uint64_t>(p) + (static_cast<uint64_t>(v) < n % static_cast<uint64_t>(p) ? 1 : 0);
+        if (tot != want) atomicOr(flag, 1u);
+    }
 }
 
 // digit_base[d] = digit_start[d] + sum_{u<me} cnt(u,d): global position of
@@ -604,15 +633,38 @@ int launch_pr_plan(const uint64_t* counts, uint64_t n, int p, int me, int bits, 
     return cudaPeekAtLastError() == cudaSuccess ? 5 : -1;
 }
 
+// Protocol flag of a call: zeroed on the call's stream before its kernels
+// (proto_begin), read back with a stream synchronisation after them
+// (proto_end -> BSG_EPROTO).  Kernels never store outside their blocks when
+// the flag is raised.
+int proto_begin(bsg_ctx* ctx, cudaStream_t st, uint32_t** flag) {
+    cudaError_t e = ctx->proto.ensure(sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->proto.as<uint32_t>(), 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "protocol flag");
+    *flag = ctx->proto.as<uint32_t>();
+    return BSG_OK;
+}
+int proto_end(bsg_ctx* ctx, cudaStream_t st, const char* what) {
+    uint32_t h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, ctx->proto.as<uint32_t>(), sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "protocol flag");
+    return h ? fail(BSG_EPROTO, what) : BSG_OK;
+}
+int check_count_rows(const uint64_t* counts, int p, int radix, uint64_t n, uint32_t* flag, cudaStream_t st) {
+    pr_check_rows_kernel<<<p, 256, 0, st>>>(counts, p, radix, n, flag);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 int launch_pr_rebuild(const uint32_t* recv, uint64_t recv_len, int bits, int shift, const int64_t* rebuild_delta,
-                      uint32_t* block, cudaStream_t stream, const uint64_t* recv_counts, int p) {
+                      uint32_t* block, cudaStream_t stream, const uint64_t* recv_counts, int p, uint32_t* proto) {
     if (p > kMaxP) return -1;
     if (recv_len == 0) return 0;
     const uint64_t want = (recv_len + kRebuildThreads * 8 - 1) / (kRebuildThreads * 8);
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, kSmCountB200 * 8)));
     TimedScope ts(3 /*BSG_K_PR*/, stream);
     pr_rebuild_kernel<<<grid, kRebuildThreads, 0, stream>>>(recv, recv_len, p, recv_counts, (1u << bits) - 1u,
-                                                           shift, 1 << bits, rebuild_delta, block);
+                                                           shift, 1 << bits, rebuild_delta, block, proto);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -811,6 +863,12 @@ extern "C" int bsg_pr_plan_host(const uint64_t* counts, uint64_t n, int p, int m
         const uint64_t lo = a0 > b0 ? a0 : b0, hi = a1 < b1 ? a1 : b1;
         return hi > lo ? hi - lo : 0;
     };
+    for (int v = 0; v < p; ++v) { // bsp_error: every row sums to its worker's block size
+        uint64_t row = 0;
+        for (uint64_t d = 0; d < r; ++d) row += counts[static_cast<uint64_t>(v) * r + d];
+        if (row != bsg_partition_size_of(n, p, v))
+            return fail(BSG_EPROTO, "bsp_error: a worker's exchanged digit counts do not sum to its block size");
+    }
     std::vector<uint64_t> starts(r), before(r, 0), split(p);
     uint64_t run = 0;
     for (uint64_t d = 0; d < r; ++d) {
@@ -884,8 +942,11 @@ extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_
         tab.offset[w] = bsg_partition_offset_of(n, p, w);
     }
     tab.offset[p] = n;
+    uint32_t* flag = nullptr;
+    if (int rc = proto_begin(ctx, st, &flag)) return rc;
     {
         TimedScope ts(3 /*BSG_K_PR*/, st);
+        if (check_count_rows(counts_all, p, radix, n, flag, st) < 0) return cuda_fail(cudaGetLastError(), "peer scatter check");
         pr_plan_col_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all, p, radix, before, coltot, colchunk);
         pr_digit_start_kernel<<<chunks, kDigChunk, 0, st>>>(coltot, colchunk, radix, dstart);
         pr_peer_gd_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all + static_cast<uint64_t>(me) * radix,
@@ -900,7 +961,7 @@ extern "C" int bsg_pr_peer_scatter(bsg_ctx* ctx, const uint32_t* sorted, uint64_
         }
     }
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer scatter launch");
-    return BSG_OK;
+    return proto_end(ctx, st, "bsp_error: a worker's exchanged digit counts do not sum to its block size");
 }
 
 // A whole PR round fused with its exchange (see bsg.h).
@@ -952,8 +1013,11 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
         tab.offset[w] = bsg_partition_offset_of(n, p, w);
     }
     tab.offset[p] = n;
+    uint32_t* flag = nullptr;
+    if (int rc = proto_begin(ctx, st, &flag)) return rc;
     {
         TimedScope ts(3 /*BSG_K_PR*/, st);
+        if (check_count_rows(counts_all, p, radix, n, flag, st) < 0) return cuda_fail(cudaGetLastError(), "fused round check");
         if ((e = cudaMemsetAsync(skew, 0, sizeof(uint32_t), st)) != cudaSuccess) return cuda_fail(e, "fused round plan");
         pr_plan_col_kernel<<<chunks, kDigChunk, 0, st>>>(counts_all, p, radix, before, coltot, colchunk, skew, n);
         pr_digit_start_kernel<<<chunks, kDigChunk, 0, st>>>(coltot, colchunk, radix, dstart);
@@ -964,9 +1028,9 @@ extern "C" int bsg_pr_fused_round(bsg_ctx* ctx, const uint32_t* block, uint64_t 
     const int l = launch_onesweep_peer(block, len, radix_log2, round * radix_log2, base, ctx->status.as<uint32_t>(),
                                        tab, p, st, skew, n);
     if (l < 0) return cuda_fail(cudaGetLastError(), "fused round launch");
-    ctx->launches += static_cast<uint64_t>(l);
+    ctx->launches += static_cast<uint64_t>(l) + 1;
     if ((e = cudaPeekAtLastError()) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fused round launch");
-    return BSG_OK;
+    return proto_end(ctx, st, "bsp_error: a worker's exchanged digit counts do not sum to its block size");
 }
 
 // ===========================================================================
@@ -1437,7 +1501,7 @@ int run_parallel_radix_group(bsg_ctx* grp, uint32_t* const* blocks, uint64_t n, 
                 TimerBinding tb(&m.c->timer);
                 uint64_t* recv = m.c->pr_misc.as<uint64_t>() + 2 * radix + 128 + p;
                 if (!add(launch_pr_rebuild(m.c->stage_b.as<uint32_t>(), m.len, bits, shift, m.c->pr_delta.as<int64_t>(),
-                                           m.cur, m.s, recv, p)))
+                                           m.cur, m.s, recv, p, nullptr)))
                     return cuda_fail(cudaGetLastError(), "group rebuild");
             }
             mark(4);

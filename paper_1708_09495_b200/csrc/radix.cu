@@ -368,6 +368,7 @@ struct PeerSink {
     template <typename Off>
     __device__ __forceinline__ void store(Off pos, uint32_t key) const {
         const uint64_t g = static_cast<uint64_t>(pos);
+        if (g >= tab->offset[p]) return; // inconsistent count matrix (reported by the caller's row check)
         int w = 0;
         for (int j = 1; j < p; ++j) w += g >= tab->offset[j] ? 1 : 0; // owner: p compares, no division
         tab->blocks[w][g - tab->offset[w]] = key;
@@ -860,28 +861,20 @@ __global__ void __launch_bounds__(THREADS, (onesweep_min_blocks<THREADS, ITEMS>(
 constexpr int kMinTile = 4096;
 
 // 0 = auto by n; otherwise a fixed THREADS x ITEMS row (see launch_onesweep_pass).
-// Initialised from BSG_OS_CFG; bsg_debug_set_onesweep_cfg overrides it (tests).
+// Initialised from BSG_OS_CFG (development builds only); bsg_debug_set_onesweep_cfg
+// overrides it (tests).
 inline int& onesweep_cfg_ref() {
-    static int cfg = [] {
-        const char* e = getenv("BSG_OS_CFG");
-        return e ? atoi(e) : 0;
-    }();
+    static int cfg = dev_knob("BSG_OS_CFG", 0);
     return cfg;
 }
 inline int onesweep_cfg() { return onesweep_cfg_ref(); }
 inline int onesweep_dbg() {
-    static int d = [] {
-        const char* e = getenv("BSG_OS_DBG");
-        return e ? atoi(e) : 0;
-    }();
+    static int d = dev_knob("BSG_OS_DBG", 0);
     return d;
 }
 
 inline int onesweep_rank_mode() {
-    static int r = [] {
-        const char* e = getenv("BSG_OS_RANK");
-        return e ? atoi(e) : 0;
-    }();
+    static int r = dev_knob("BSG_OS_RANK", 0);
     return r;
 }
 
@@ -1123,10 +1116,7 @@ __global__ void __launch_bounds__(kSmallThreads, (kSmallThreads <= 512 ? 2 : 1))
 }
 
 int& small_sort_flag() {
-    static int on = [] {
-        const char* e = getenv("BSG_SMALL");
-        return e ? atoi(e) : 1;
-    }();
+    static int on = dev_knob("BSG_SMALL", 1);
     return on;
 }
 bool small_sort_enabled() { return small_sort_flag() != 0; }
@@ -1145,10 +1135,7 @@ int launch_small_sort(const uint32_t* in, uint32_t* out, uint64_t n, const Radix
     if (cudaMemsetAsync(ws.status, 0, small_ws_words(n) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
     // grid: every tile gets a CTA, at least one CTA per SM for the histogram
     // (measured: 2^20 keys 56 us at 148 CTAs vs 59 us at all 296 resident)
-    static const int gmin = [] {
-        const char* e = getenv("BSG_SMALL_GRID");
-        return e ? atoi(e) : kSmCountB200;
-    }();
+    static const int gmin = dev_knob("BSG_SMALL_GRID", kSmCountB200);
     const uint64_t tiles = (n + kSmallThreads * kSmallItems - 1) / (kSmallThreads * kSmallItems);
     unsigned grid = static_cast<unsigned>(per_sm * sms);
     if (gmin > 0) grid = static_cast<unsigned>(std::min<uint64_t>(grid, std::max<uint64_t>(tiles, gmin)));

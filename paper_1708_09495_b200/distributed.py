@@ -216,6 +216,7 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
         _close(count_events, c0)
         sorted_ = ops.local_sort(block, rnd, bits)
         send, recv, recv_dev, delta = ops.plan(counts_all, n_total, p, me, rnd, bits)
+        _check_exchange(send, recv, block.numel(), partition_size_of(n_total, p, me), me, rnd)
         recv_buf = ops.keys(sum(recv))
         if a2a_events is not None and block.is_cuda:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -226,6 +227,17 @@ def parallel_radix_sort(block: torch.Tensor, n_total: int, radix: int = 256, rou
             a2a_events.append((e0, e1))
         block = ops.rebuild(recv_buf, recv_dev, p, rnd, bits, delta, partition_size_of(n_total, p, me))
     return block
+
+
+def _check_exchange(send, recv, block_len: int, want_len, me: int, rnd: int) -> None:
+    """bsp_error equivalents (radix.hpp:207-220, 283-286): this rank sends
+    every key of its block exactly once and, in PR, receives exactly its
+    partition's size -- before any byte moves."""
+    if sum(send) != block_len:
+        raise _lib.BspError(f"worker {me}, round {rnd}: send counts sum to {sum(send)}, block has {block_len} keys")
+    if want_len is not None and sum(recv) != want_len:
+        raise _lib.BspError(f"worker {me}, round {rnd}: receive counts sum to {sum(recv)}, "
+                            f"expected {want_len} keys")
 
 
 def _event(lst, block):
@@ -314,6 +326,7 @@ def parallel_radix_sort_single_exchange(block: torch.Tensor, group=None, ops=Non
     mine = cm[me]
     send = [int(mine[cuts[w]:cuts[w + 1]].sum()) for w in range(p)]
     recv = [int(cm[v, cuts[me]:cuts[me + 1]].sum()) for v in range(p)]
+    _check_exchange(send, recv, block.numel(), None, me, 0)
     recv_buf = ops.keys(sum(recv))
     if a2a_events is not None and block.is_cuda:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -375,9 +388,15 @@ def block_network_sort(block: torch.Tensor, network: int = 0, stages: Optional[i
             continue
         other = torch.empty_like(state)
         if p > 1:
-            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, state, q, group),
-                                           dist.P2POp(dist.irecv, other, q, group)])
+            # NCCL moves device blocks peer to peer; gloo has no device
+            # point-to-point, so CUDA blocks are staged through host memory
+            stage = state.is_cuda and not _is_nccl(group)
+            snd = state.cpu() if stage else state
+            rcv = torch.empty_like(snd)
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, snd, q, group),
+                                           dist.P2POp(dist.irecv, rcv, q, group)])
             for r in reqs:
                 r.wait()
+            other = rcv.to(state.device) if stage else rcv
         state = ops.merge_keep(state, other, keep_low)
     return state

@@ -65,11 +65,14 @@ def test_superstep_counts(cuda, bsg, orc):
 @pytest.mark.parametrize("p", [1, 2, 3, 8])
 def test_device_plan_equals_host_plan(cuda, bsg, orc, bits, p):
     torch = cuda
+    from paper_1708_09495_b200 import distributed as D
+
     rng = np.random.default_rng(bits * 100 + p)
     r = 1 << bits
-    counts = rng.integers(0, 50, size=p * r).astype(np.uint64)
-    counts[rng.integers(0, p * r, size=5)] = 0
-    n = int(counts.sum())
+    n = 25 * p * r + 7
+    # row v: worker v's digit counts, summing to Partition(n, p).size_of(v)
+    counts = np.concatenate([rng.multinomial(D.partition_size_of(n, p, v), np.full(r, 1.0 / r))
+                             for v in range(p)]).astype(np.uint64)
     L = bsg._lib.lib()
     ctx = bsg._lib.context(0)
     dc = torch.from_numpy(counts.view(np.int64)).cuda()
@@ -374,3 +377,75 @@ def test_distributed_world1_large_block(cuda, bsg):
         torch.cuda.empty_cache()
     finally:
         dist.destroy_process_group()
+
+
+def test_protocol_errors_raise_bsp_error(cuda, bsg):
+    """bsp_error equivalents (radix.hpp:207-220, 283-286): count matrices whose
+    rows do not sum to the workers' block sizes, and received slices that do
+    not fill the rebuilt block, fail with BSG_EPROTO -- and no kernel stores
+    outside its blocks (canaries after every block stay intact)."""
+    torch = cuda
+    import ctypes
+    from paper_1708_09495_b200 import distributed as D
+
+    L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    p, bits, n = 4, 8, 40003
+    ops = D.CudaStepOps(torch.device("cuda", 0))
+    keys = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device="cuda")
+    sizes = [D.partition_size_of(n, p, w) for w in range(p)]
+    offs = [D.partition_offset_of(n, p, w) for w in range(p)]
+    blocks = [keys[offs[w]:offs[w] + sizes[w]] for w in range(p)]
+    good = torch.cat([ops.count(b, 0, bits) for b in blocks])
+    bad = good.clone()
+    bad[3] += 1                                   # worker 0 claims one key too many
+    sr = torch.empty(2 * p, dtype=torch.int64, device="cuda")
+    delta = torch.empty(p << bits, dtype=torch.int64, device="cuda")
+    assert L.bsg_pr_plan(ctx.handle, good.data_ptr(), n, p, 1, 0, bits, sr.data_ptr(), sr[p:].data_ptr(),
+                         delta.data_ptr(), st) == 0
+    assert L.bsg_pr_plan(ctx.handle, bad.data_ptr(), n, p, 1, 0, bits, sr.data_ptr(), sr[p:].data_ptr(),
+                         delta.data_ptr(), st) == bsg._lib.BSG_EPROTO
+    assert "bsp_error" in bsg._lib.last_error()
+    hb = bad.cpu().numpy().view(np.uint64).copy()
+    hs, hr, hd = np.zeros(p, np.uint64), np.zeros(p, np.uint64), np.zeros(p << bits, np.int64)
+    assert L.bsg_pr_plan_host(hb.ctypes.data, n, p, 1, bits, hs.ctypes.data, hr.ctypes.data,
+                              hd.ctypes.data) == bsg._lib.BSG_EPROTO
+    with pytest.raises(bsg._lib.BspError):
+        ops.plan(bad, n, p, 1, 0, bits)
+
+    CAN = 0x5A5A5A5A
+    def canaried():
+        bufs = [torch.full((sz + 64,), CAN, dtype=torch.int32, device="cuda") for sz in sizes]
+        return bufs, [t.data_ptr() for t in bufs]
+    def intact(bufs):
+        return all(bool((b[sz:] == CAN).all()) for b, sz in zip(bufs, sizes))
+    for fn in ("fused_round", "peer_scatter"):
+        bufs, ptrs = canaried()
+        with pytest.raises(bsg._lib.BspError):
+            src = blocks[0] if fn == "fused_round" else ops.local_sort(blocks[0], 0, bits)
+            getattr(ops, fn)(src, bad, n, p, 0, 0, bits, ptrs)
+        torch.cuda.synchronize()
+        assert intact(bufs), fn
+        bufs, ptrs = canaried()
+        for me in range(p):
+            src = blocks[me] if fn == "fused_round" else ops.local_sort(blocks[me], 0, bits)
+            getattr(ops, fn)(src, good, n, p, me, 0, bits, ptrs)
+        torch.cuda.synchronize()
+        assert intact(bufs), fn
+
+    # rebuild: receive counts that do not add up to the received keys
+    send, recv, recv_dev, dl = ops.plan(good, n, p, 1, 0, bits)
+    recv_buf = torch.randint(-2**31, 2**31 - 1, (sum(recv),), dtype=torch.int32, device="cuda")
+    out = torch.full((sum(recv) + 64,), CAN, dtype=torch.int32, device="cuda")
+    wrong = recv_dev.clone()
+    wrong[0] += 5
+    assert L.bsg_pr_rebuild(ctx.handle, recv_buf.data_ptr(), recv_buf.numel(), wrong.data_ptr(), p, 0, bits,
+                            dl.data_ptr(), out.data_ptr(), st) == bsg._lib.BSG_EPROTO
+    torch.cuda.synchronize()
+    assert bool((out[sum(recv):] == CAN).all())
+    # exchange sizes checked on the host before any byte moves
+    with pytest.raises(bsg._lib.BspError):
+        D._check_exchange([1, 2], [3, 4], 4, 7, 0, 0)
+    with pytest.raises(bsg._lib.BspError):
+        D._check_exchange([1, 2], [3, 3], 3, 7, 0, 0)
