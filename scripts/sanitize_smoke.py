@@ -1,6 +1,5 @@
 """Small invocations of every kernel family with result checks: a quick
-all-paths sanity run (compute-sanitizer itself is not available on the GPU
-pool).  Development aid."""
+all-paths sanity run (run it under compute-sanitizer --tool memcheck/racecheck/synccheck).  Development aid."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -32,6 +31,14 @@ arrs = keys[:64 * 300].reshape(64, 300)
 for net in (0, 1):
     out, _ = bsg.netsort.block_network_batched(arrs, 4, net)
     assert np.array_equal(out, np.sort(arrs, axis=1))
+# register networks (power-of-two blocks): in-warp, layout-B and cross-warp paths
+for ln, p in ((4096, 8), (1024, 2), (16384, 2), (256, 16)):
+    arrs = keys[:8 * ln].reshape(8, ln) if 8 * ln <= keys.size else np.tile(keys[:ln], 8).reshape(8, ln)
+    for net in (0, 1):
+        out, _ = bsg.netsort.block_network_batched(arrs, p, net)
+        assert np.array_equal(out, np.sort(arrs, axis=1))
+        S = len(D.network_schedule(net, p))
+        bsg.netsort.block_network_batched(arrs, p, net, S // 2)
 big = keys[:40000]
 assert np.array_equal(bsg.netsort.oet_sort(bsg.SortInstance(big, 5, bsg.Algorithm.OET)), np.sort(big))
 lo, hi = bsg.netsort.merge_split(np.sort(keys[:500]), np.sort(keys[500:1100]))
