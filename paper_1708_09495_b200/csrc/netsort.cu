@@ -393,6 +393,12 @@ __global__ void __launch_bounds__(kNetThreads, MINB)
 #ifndef BSG_NET_FMA_STEPS
 #define BSG_NET_FMA_STEPS 0xF // register steps (masks) whose maxima go to the FMA pipe
 #endif
+#ifndef BSG_NET_CTA_KEYS
+#define BSG_NET_CTA_KEYS 4096 // keys per CTA of the register network (arrays shorter than this share a CTA)
+#endif
+#ifndef BSG_NET_REG_TPSM
+#define BSG_NET_REG_TPSM 1024 // threads per SM the register network is compiled for (64 registers)
+#endif
 
 __device__ __forceinline__ uint32_t minmax_sel(uint32_t a, uint32_t b, bool up) { return up ? max(a, b) : min(a, b); }
 
@@ -763,8 +769,8 @@ int launch_reg(int logl, const uint32_t* in, uint32_t* out, uint64_t num_arrays,
     if (grid > 0x7FFFFFFFull) return -1;
     const uint32_t threads = ((static_cast<uint32_t>(apc) * P / R) + 31u) & ~31u;
     const unsigned g = static_cast<unsigned>(grid);
-    constexpr int T0 = 4096 / R;      // CTA of 4096 keys
-    constexpr int M0 = 1024 / T0;     // CTAs per SM at <= 64 registers
+    constexpr int T0 = BSG_NET_CTA_KEYS / R;      // threads of a CTA of BSG_NET_CTA_KEYS keys
+    constexpr int M0 = BSG_NET_REG_TPSM / T0;     // CTAs per SM (register cap 65536 / BSG_NET_REG_TPSM)
     if (threads <= T0)
         return dispatch_reg_network<R, T0, M0>(logl, in, out, num_arrays, len, p, network, run_stages, full, apc,
                                                 vec_in, vec_out, g, threads, stream);
@@ -847,8 +853,8 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
     const uint32_t L = (len + static_cast<uint32_t>(p) - 1) / static_cast<uint32_t>(p);
     const uint32_t P = L * static_cast<uint32_t>(p);
     if (P == 0 || P > kNetMaxPadded) return -1;
-    const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
     if (BSG_NET_REG && L >= 16 && (L & (L - 1)) == 0) {
+        const int apc = static_cast<int>(std::max<uint32_t>(1, BSG_NET_CTA_KEYS / P));
         const int vec_in = (len % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
         const int vec_out = (len % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
         int logl = 0;
@@ -861,6 +867,7 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
         return launch_reg<16>(logl, in, out, num_arrays, len, p, P, network, run_stages, f, apc, vec_in, vec_out,
                               stream);
     }
+    const int apc = static_cast<int>(std::max<uint32_t>(1, 4096 / P));
     const size_t padded =static_cast<size_t>(apc) * P + (static_cast<size_t>(apc) * P >> 5) + 1;
     const size_t smem = 2ull * padded * sizeof(uint32_t);
     const uint64_t grid = (num_arrays + apc - 1) / apc;
