@@ -376,9 +376,85 @@ def run_single(args):
         "clocks": clk.summary(),
         "verified": ok and ok_e2e,
     }
+    if not args.no_other_configs:
+        line["other_configs"] = other_configs(bsg, _lib, L, ctx, d_in, d_out, stream, n)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(keys)
     print(json.dumps(line), flush=True)
+
+
+def other_configs(bsg, _lib, L, ctx, d_in, d_out, stream, n):
+    """The other BASELINE configs that fit one GPU, measured in the same run
+    (device-resident inputs, CUDA events on the launching stream, median of
+    a few reps after a warm-up, every output compared bit for bit with
+    torch.sort of the same keys on the device): C1 latency, C2 at r = 2^16,
+    C3's three skewed 2^28 inputs, C4's 2^16 x 4096 batches (BTN/OET, p = 8)
+    and PR4/PR2 with 8 logical workers on the config-2 keys."""
+    import torch
+
+    sh = stream.cuda_stream
+    res = {}
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    def u64(t):
+        return t.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+
+    def sort_row(t, o, radix_log2, reps, label):
+        m = t.numel()
+        ms = timed(lambda: _lib.check(L.bsg_radix_sort_u32(ctx.handle, t.data_ptr(), o.data_ptr(), m, radix_log2,
+                                                           _lib.MEM_DEVICE, sh)), reps)
+        ok = bool(torch.equal(u64(o), torch.sort(u64(t)).values))
+        return {"workload": label, "n": m, "ms": ms, "keys_per_s": m / ms * 1e3, "verified": ok}
+
+    # C1: 2^20 keys (latency; one fused cooperative launch)
+    n1 = 1 << 20
+    k1 = torch.from_numpy(bsg.generate_uniform_keys(n1, bsg.derive_seed(1, 0)).view(np.int32)).cuda()
+    o1 = torch.empty_like(k1)
+    res["C1"] = sort_row(k1, o1, 8, 50, "config 1: SR4 of 2^20 uniform keys")
+    res["C1"]["us"] = res["C1"]["ms"] * 1e3
+    # C2 at r = 2^16 (2 rounds, each two stable byte sub-passes from one histogram read)
+    res["C2_r65536"] = sort_row(d_in, d_out, 16, 5, "config 2 at radix 2^16 (2 count-sort rounds)")
+    # C3: skewed 2^28 inputs (narrow = the config-2 keys & 0xFFFF, bsg_generate_skewed kind 0)
+    t = torch.empty_like(d_in)
+    for name, make in (("narrow16", lambda: torch.bitwise_and(d_in, 0xFFFF, out=t)),
+                       ("all_equal", lambda: t.fill_(int(np.uint32(0xABCD1234).view(np.int32)))),
+                       ("zipf1.1", lambda: t.copy_(torch.from_numpy(
+                           bsg.generate_skewed_keys(n, bsg.derive_seed(1, 0), 1, 1.1).view(np.int32))))):
+        make()
+        res["C3_" + name] = sort_row(t, d_out, 8, 5, f"config 3: SR4 of 2^28 keys, {name}")
+    del t
+    # C4: 2^16 arrays x 4096 keys (the config-2 keys), BTN and OET at p = 8
+    num, ln = 1 << 16, 4096
+    if n >= num * ln:
+        ref = torch.sort(u64(d_in[:num * ln]).view(num, ln), dim=1).values
+        for net, name in ((0, "BTN"), (1, "OET")):
+            ms = timed(lambda: _lib.check(L.bsg_block_network_batched_u32(ctx.handle, net, d_in.data_ptr(),
+                                                                          d_out.data_ptr(), num, ln, 8, -1, None,
+                                                                          _lib.MEM_DEVICE, sh)), 5)
+            ok = bool(torch.equal(u64(d_out[:num * ln]).view(num, ln), ref))
+            res["C4_" + name + "_p8"] = {"workload": f"config 4: {name}, 2^16 arrays x 4096 keys, p = 8",
+                                         "n": num * ln, "ms": ms, "keys_per_s": num * ln / ms * 1e3, "verified": ok}
+        del ref
+    # PR4 / PR2 with p = 8 logical workers on one GPU (the per-round BSP algorithm)
+    ref = torch.sort(u64(d_in)).values
+    for bits, name in ((8, "PR4"), (16, "PR2")):
+        ms = timed(lambda: _lib.check(L.bsg_parallel_radix_sort_u32(ctx.handle, d_in.data_ptr(), d_out.data_ptr(), n,
+                                                                    8, bits, -1, None, _lib.MEM_DEVICE, sh)), 5)
+        res[name + "_p8"] = {"workload": f"{name} with 8 logical workers, 2^28 keys, one GPU", "n": n, "ms": ms,
+                             "keys_per_s": n / ms * 1e3, "verified": bool(torch.equal(u64(d_out), ref))}
+    return res
 
 
 def run_multi(args, rank: int, world: int, local_rank: int):
@@ -559,6 +635,8 @@ def main():
     ap.add_argument("--n-total", type=int, default=N_TOTAL_C5, help="config 5 keys over all GPUs (N > 1)")
     ap.add_argument("--ref-n", type=int, default=0, help="keys per reference step (default: config 2's 2^28)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the C1/C3/C4/PR rows measured after the config-2 line")
     ap.add_argument("--e2e-inflight", type=int, default=4,
                     help="sorts in flight in the e2e measurement (host threads, one context/stream each)")
     ap.add_argument("--pr-variant", choices=["A", "B", "P"], default="P",
