@@ -646,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // step jidx of a).
     int lvl = 1, jidx = 0;
     for (int s = 0; s < run_stages; ++s) {
+        if (network == 1 && p - (s & 1) < 2) continue; // an OET round with no pair (p = 2, odd rounds)
         bool keep_low = false;
         int q = -1;
         if (live) {
@@ -671,6 +672,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
             uint32_t* buf = net.S + net.b;
             put_a<R>(buf, t, v);
             __syncthreads();
+            if (__all_sync(0xffffffffu, q < 0)) { // idle OET edge worker: its sorted block stays
+                net.b ^= net.stride;
+                continue;
+            }
             const uint32_t* own = buf + 36u * R * net.warp + net.lane;
             const uint32_t* par = buf + 36u * R * pseg + 36u * R - 5u - net.lane;
 #pragma unroll
@@ -693,6 +698,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
             uint32_t* buf = net.S + net.b;
             put_a<R>(buf, t, v);
             __syncthreads();
+            if (LOGL - 1 < Sh::LR + 5 && __all_sync(0xffffffffu, q < 0)) {
+                // idle OET edge workers only (their merge steps stay inside the warp)
+                net.b ^= net.stride;
+                continue;
+            }
             const uint32_t tp = pseg * spt + (spt - 1 - c);
             if (__all_sync(0xffffffffu, lo)) apply_a<R, true>(buf, tp, v, OpMin{});
             else if (__all_sync(0xffffffffu, hi)) apply_a<R, true>(buf, tp, v, OpMax{});
