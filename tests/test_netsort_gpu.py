@@ -134,3 +134,27 @@ def test_resident_1024_thread_path_per_stage(cuda, bsg, orc, network, p):
             exp, est = orc.block_network(network, keys, p, s)
             np.testing.assert_array_equal(got.reshape(-1), exp)
             assert st == est
+
+
+@pytest.mark.parametrize("network,p,L", [(1, 3, 16), (1, 3, 512), (1, 5, 64), (1, 7, 2048), (0, 4, 16),
+                                         (0, 2, 8192), (1, 6, 256), (0, 16, 32)])
+def test_register_network_shapes_per_stage(cuda, bsg, orc, network, p, L):
+    """The register network runs every power-of-two block length, including
+    non-power-of-two OET worker counts (CTAs padded with idle dummy threads,
+    e.g. p = 3, L = 16: 85 arrays of 48 keys on 256 threads) and ragged last
+    arrays of a batch; every truncated stage table vs the oracle."""
+    n = p * L
+    num = 37
+    keys = orc.generate_uniform_keys(num * n, 1000 + p * L + network)
+    arrs = keys.reshape(num, n)
+    S = orc.schedule(network, p)[0].shape[0]
+    for s in sorted({0, 1, S // 2, S}):
+        got, st = bsg.netsort.block_network_batched(arrs, p, network, s)
+        for i in (0, num // 2, num - 1):
+            exp, est = orc.block_network(network, arrs[i], p, s)
+            np.testing.assert_array_equal(got[i], exp)
+            assert st == est
+    # ragged last block (len not a multiple of p, same power-of-two L)
+    m = n - 3
+    got, _ = bsg.netsort.block_network_batched(keys[:num * m].reshape(num, m), p, network)
+    np.testing.assert_array_equal(got, np.sort(keys[:num * m].reshape(num, m), axis=1))
