@@ -82,6 +82,9 @@ uint64_t bsg_ctx_launch_count(const bsg_ctx* ctx);
  * serialises its calls internally; use one per host thread for concurrency. */
 int bsg_ctx_create(int device, bsg_ctx** out);
 int bsg_ctx_destroy(bsg_ctx* ctx);
+/* Frees the context's cached device workspace (after its last queued call
+ * completes); the context stays usable and re-allocates on demand. */
+int bsg_ctx_release(bsg_ctx* ctx);
 /* Pre-sizes the workspace for sorts of up to n keys (optional). */
 int bsg_ctx_reserve(bsg_ctx* ctx, uint64_t n);
 

@@ -77,6 +77,7 @@ SIGNATURES = {
     "bsg_ctx_launch_count": (ctypes.c_uint64, [_vp]),
     "bsg_ctx_create": (_i, [_i, ctypes.POINTER(_vp)]),
     "bsg_ctx_destroy": (_i, [_vp]),
+    "bsg_ctx_release": (_i, [_vp]),
     "bsg_ctx_reserve": (_i, [_vp, _u64]),
     "bsg_ctx_set_timing": (_i, [_vp, _i]),
     "bsg_ctx_get_timing": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
@@ -187,6 +188,10 @@ class Context:
     def reserve(self, n: int) -> None:
         check(lib().bsg_ctx_reserve(self.handle, n), "bsg_ctx_reserve")
 
+    def release(self) -> None:
+        """Frees the cached device workspace (the context stays usable)."""
+        check(lib().bsg_ctx_release(self.handle), "bsg_ctx_release")
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             lib().bsg_ctx_destroy(self.handle)
@@ -231,6 +236,12 @@ def context(device: Optional[int] = None) -> Context:
                 ctx = Context(device)
                 _contexts[device] = ctx
     return ctx
+
+
+def release_all() -> None:
+    """Frees the cached workspace of every default context."""
+    for ctx in list(_contexts.values()):
+        ctx.release()
 
 
 def _current_device() -> int:

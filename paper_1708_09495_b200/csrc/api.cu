@@ -177,6 +177,23 @@ int bsg_ctx_create(int device, bsg_ctx** out) {
     return BSG_OK;
 }
 
+int bsg_ctx_release(bsg_ctx* ctx) {
+    if (int rc = check_ctx(ctx)) return rc;
+    for (bsg_ctx* m : ctx->members)
+        if (int rc = bsg_ctx_release(m)) return rc;
+    CallGuard g(ctx);
+    if (ctx->used && ctx->last_use) {
+        const cudaError_t e = cudaEventSynchronize(ctx->last_use);
+        if (e != cudaSuccess) return cuda_fail(e, "ctx release");
+    }
+    for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
+                      &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
+                      &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws, &ctx->grp_cur,
+                      &ctx->grp_nxt, &ctx->grp_recv})
+        b->release();
+    return BSG_OK;
+}
+
 int bsg_ctx_destroy(bsg_ctx* ctx) {
     if (!ctx) return BSG_OK;
     if (!ctx->members.empty()) {
@@ -195,7 +212,7 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
         CallGuard g(ctx);
         for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
                           &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
-                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->mt_ws})
+                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws})
             b->release();
         if (ctx->last_use) cudaEventDestroy(ctx->last_use);
         release_stage(ctx);

@@ -696,18 +696,29 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                     mbar_wait_parity(&s_bar[cur ^ 1], (bar_parity >> (cur ^ 1)) & 1u);
                     bar_parity ^= 1u << (cur ^ 1);
                     const uint32_t* nbuf = s_in + (cur ^ 1) * TILE;
+                    if (nbody == static_cast<uint32_t>(TILE)) {
+                        // whole tile delivered by TMA (full, 16-byte aligned): no guards
 #pragma unroll
-                    for (int i = 0; i < ITEMS; ++i) {
-                        const uint32_t idx = wbase + i * 32 + lane;
-                        const uint32_t rel = idx - nhw;
-                        keys[i] = idx < nvalid ? (rel < nbody ? nbuf[rel] : __ldg(src + nstart + idx)) : 0u;
-                    }
+                        for (int i = 0; i < ITEMS; ++i) keys[i] = nbuf[wbase + i * 32 + lane];
 #pragma unroll
-                    for (int i = 0; i < ITEMS; ++i) {
-                        const uint32_t idx = wbase + i * 32 + lane;
-                        if (idx < nvalid) {
+                        for (int i = 0; i < ITEMS; ++i) {
                             const uint32_t d = digit_of_key<BITS>(keys[i], shift);
                             atomicAdd(row + (d >> 1), 1u << ((d & 1u) * 16u));
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < ITEMS; ++i) {
+                            const uint32_t idx = wbase + i * 32 + lane;
+                            const uint32_t rel = idx - nhw;
+                            keys[i] = idx < nvalid ? (rel < nbody ? nbuf[rel] : __ldg(src + nstart + idx)) : 0u;
+                        }
+#pragma unroll
+                        for (int i = 0; i < ITEMS; ++i) {
+                            const uint32_t idx = wbase + i * 32 + lane;
+                            if (idx < nvalid) {
+                                const uint32_t d = digit_of_key<BITS>(keys[i], shift);
+                                atomicAdd(row + (d >> 1), 1u << ((d & 1u) * 16u));
+                            }
                         }
                     }
                     have_next = true;

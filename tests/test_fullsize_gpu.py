@@ -167,6 +167,7 @@ def test_c5_full_size_bit_exact(cuda, bsg):
 
     torch = cuda
     n, p = 1 << 33, 8
+    bsg._lib.release_all()  # earlier tests' workspaces (e.g. 2^32-key sorts) must not count against 2^33
     torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 17 * n:
@@ -217,4 +218,5 @@ def test_c5_full_size_bit_exact(cuda, bsg):
         ctx2.close()
     print(f"c5: host reference {t1 - t0:.1f} s, GPU sorts + compare {t2 - t1:.1f} s")
     del keys, out, exp
+    bsg._lib.release_all()
     torch.cuda.empty_cache()

@@ -118,6 +118,7 @@ def test_group_global_positions_above_2_32(cuda, bsg):
     array; the full sort equals the single-GPU sort."""
     torch = cuda
     n, p, G = (1 << 32) + 5, 4, 2
+    bsg._lib.release_all()
     torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 22 * n:
@@ -147,4 +148,5 @@ def test_group_global_positions_above_2_32(cuda, bsg):
         grp.close()
         ctx.close()
         del keys
+        bsg._lib.release_all()
         torch.cuda.empty_cache()

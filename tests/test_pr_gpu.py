@@ -219,6 +219,7 @@ def test_c5_full_size_in_process(cuda, bsg, p):
     torch.cuda.synchronize()
     _chunked_properties(torch, keys, out)
     del keys, out
+    bsg._lib.release_all()
     torch.cuda.empty_cache()
 
 
@@ -256,6 +257,7 @@ def test_large_segments_wide_rows(cuda, bsg, radix_log2):
     assert L.bsg_radix_sort_u32(ctx.handle, keys.data_ptr(), exp.data_ptr(), n, radix_log2, 1, st) == 0
     assert same()
     del keys, got, exp
+    bsg._lib.release_all()
     torch.cuda.empty_cache()
 
 
@@ -293,6 +295,7 @@ def test_fused_round_large_blocks(cuda, bsg):
             assert bool(torch.equal(nxt[w], exp[offs[w]:offs[w] + sizes[w]])), (bits, w)
         del nxt
     del keys, exp, blocks
+    bsg._lib.release_all()
     torch.cuda.empty_cache()
 
 
@@ -334,6 +337,7 @@ def test_fused_round_global_positions_above_2_32(cuda, bsg):
     for a in range(0, n, step):
         assert bool(torch.equal(nxt[a:a + step], exp[a:a + step])), a
     del keys, nxt, exp, blocks
+    bsg._lib.release_all()
     torch.cuda.empty_cache()
 
 
@@ -374,6 +378,7 @@ def test_distributed_world1_large_block(cuda, bsg):
         peer = D.PeerBlocks(n)
         check(D.parallel_radix_sort(keys.clone(), n, radix=256, exchange="peer", peer=peer))
         del peer, keys, exp
+        bsg._lib.release_all()
         torch.cuda.empty_cache()
     finally:
         dist.destroy_process_group()

@@ -261,6 +261,7 @@ def test_multi_chunk_and_wide_positions(cuda, bsg, n):
         assert bool((d[1:] >= d[:-1]).all()) and int(d[0]) >= prev
         prev = int(d[-1])
     del inp, out
+    bsg._lib.release_all()
     torch.cuda.empty_cache()
 
 
