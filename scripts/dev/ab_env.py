@@ -26,7 +26,7 @@ ok = bool(torch.equal(out.view(torch.int32).to(torch.int64) & 0xFFFFFFFF, exp)) 
 ts.sort(); print("RESULT", min(ts), ts[len(ts) // 2], os_ms / max(os_cnt, 1), ok)
 '''
 
-repo = os.path.dirname(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+repo = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 res = {}
 for rnd in range(int(os.environ.get("AB_ROUNDS", "3"))):
     for spec in sys.argv[1:]:
