@@ -46,6 +46,9 @@
 #ifndef BSG_COUNT_FAST
 #define BSG_COUNT_FAST 1 // byte-digit counting: LOP3 row offset + IMAD increment (7 instead of 9 per key)
 #endif
+#ifndef BSG_LB_FAST
+#define BSG_LB_FAST 1 // look-back rounds whose words are all published aggregates take a branch-free sum
+#endif
 #ifndef BSG_EARLY_COUNT
 #define BSG_EARLY_COUNT 1 // count-then-rank: the upper half of the warps counts the next tile during the look-back
 #endif
@@ -772,14 +775,32 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             Stat prefix = 0;
             // one round trip: W predecessors from t down; consumes the
             // published ones up to the first inclusive (done) or unpublished
-            auto lb_round = [&](auto wtag, int64_t& t, bool& done) {
+            auto lb_round = [&](auto wtag, int32_t& t, bool& done) {
                 constexpr int W = decltype(wtag)::value;
                 Stat sv[W];
+                const Stat* p = stat + static_cast<uint64_t>(static_cast<uint32_t>(t)) * RADIX + tid;
+                const int32_t avail = t - static_cast<int32_t>(tfirst); // predecessors t .. t-avail exist
 #pragma unroll
-                for (int j = 0; j < W; ++j)
-                    sv[j] = (t - j >= static_cast<int64_t>(tfirst))
-                                ? ld_relaxed_gpu(&stat[static_cast<uint64_t>(t - j) * RADIX + tid])
-                                : SW::INC;
+                for (int j = 0; j < W; ++j) sv[j] = (j <= avail) ? ld_relaxed_gpu(p - j * RADIX) : SW::INC;
+                if constexpr (BSG_LB_FAST) {
+                    // common case: W published aggregates -- consume them all
+                    Stat all = sv[0], any = sv[0], sum = sv[0];
+#pragma unroll
+                    for (int j = 1; j < W; ++j) {
+                        all &= sv[j];
+                        any |= sv[j];
+                        sum += sv[j];
+                    }
+                    if ((all & SW::AGG) && !(any & SW::INC)) {
+                        prefix += sum - static_cast<Stat>(W) * SW::AGG; // each word carries the AGG bit once
+                        if (BSG_LB_STATS) {
+                            ++lbs_rounds;
+                            lbs_used += W;
+                        }
+                        t -= W;
+                        return;
+                    }
+                }
                 int used = 0;
                 bool stop = false;
 #pragma unroll
@@ -802,7 +823,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 t -= used;
             };
             if (tile > tfirst && !(dbg & 1)) {
-                int64_t t = static_cast<int64_t>(tile) - 1;
+                int32_t t = static_cast<int32_t>(tile) - 1;
                 bool done = false;
                 if constexpr (LB_FIRST > LB_WIN) lb_round(std::integral_constant<int, LB_FIRST>{}, t, done);
                 while (!done) lb_round(std::integral_constant<int, LB_WIN>{}, t, done);
