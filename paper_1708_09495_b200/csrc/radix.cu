@@ -50,7 +50,8 @@
 #define BSG_LB_FAST 1 // look-back rounds whose words are all published aggregates take a branch-free sum
 #endif
 #ifndef BSG_EARLY_COUNT
-#define BSG_EARLY_COUNT 1 // count-then-rank: the upper half of the warps counts the next tile during the look-back
+#define BSG_EARLY_COUNT 2 // count-then-rank: the upper half of the warps counts the next tile during the
+                          // look-back (1: their own keys, 2: all keys)
 #endif
 #ifndef BSG_LB_FIRST
 #define BSG_LB_FIRST 0 // wider first look-back round (predecessors), 0 = same as the window
@@ -291,7 +292,7 @@ __device__ __forceinline__ uint32_t peers_ballot(uint32_t d, int32_t neg1) {
 
 // Phase-cycle instrumentation (dbg bit 8): thread 0 of every CTA accumulates
 // clock64 deltas per phase.  Development aid only.
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[16]; // [0..7] thread 0, [8..15] thread 256 (an early-count warp)
 #ifndef BSG_LB_STATS
 #define BSG_LB_STATS 0 // development: look-back round/predecessor/stall counts (g_lb_stats)
 #endif
@@ -474,16 +475,18 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // as one IMAD on the FMA pipe.
     const uint32_t wrow_bytes = static_cast<uint32_t>(warp) * (RADIX * 2);
     const uint32_t ffff = static_cast<uint32_t>(-neg1) * 0xFFFFu; // runtime 0xFFFF keeps the IMAD
-    auto count_digit = [&](uint32_t d) {
+    auto count_digit_row = [&](uint32_t d, uint32_t row_bytes) {
         if constexpr (BITS == 8 && BSG_COUNT_FAST) {
             uint32_t boff, inc;
-            asm("lop3.b32 %0, %1, 0x1FC, %2, 0xEA;" : "=r"(boff) : "r"(d << 1), "r"(wrow_bytes)); // (a & b) | c
+            asm("lop3.b32 %0, %1, 0x1FC, %2, 0xEA;" : "=r"(boff) : "r"(d << 1), "r"(row_bytes)); // (a & b) | c
             asm("mad.lo.u32 %0, %1, %2, 1;" : "=r"(inc) : "r"(d & 1u), "r"(ffff));
             atomicAdd(reinterpret_cast<uint32_t*>(smem + L::wcnt_off + boff), inc);
         } else {
-            atomicAdd(reinterpret_cast<uint32_t*>(s_wcnt + warp * RADIX) + (d >> 1), 1u << ((d & 1u) * 16u));
+            atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(s_wcnt) + row_bytes) + (d >> 1),
+                      1u << ((d & 1u) * 16u));
         }
     };
+    auto count_digit = [&](uint32_t d) { count_digit_row(d, wrow_bytes); };
     uint32_t lbs_rounds = 0, lbs_used = 0, lbs_stops = 0, lbs_tiles = 0;
     const uint32_t dmul = static_cast<uint32_t>(-neg1) << (BITS == 8 ? (24 - shift) : 0);
     uint32_t keys[ITEMS];
@@ -492,6 +495,9 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // tile k+1 (TMA-delivered to the other buffer) and count them into their
     // own (reset) counter rows; in iteration k+1 they skip the count phase.
     constexpr bool EARLY = RANK == 3 && BSG_EARLY_COUNT && BITS == 8 && !WIDE && THREADS == 512 && ITEMS == 24 && !SEG;
+    // EARLY2: the early warps also count their partner lower warps' keys of
+    // the next tile, so no warp counts at the top of the next iteration
+    constexpr bool EARLY2 = EARLY && BSG_EARLY_COUNT >= 2;
     const bool early_warp = EARLY && warp >= WARPS / 2;
     bool have_next = false; // this warp's keys and counts of the current tile are in place
     for (uint32_t k = 0;; ++k) {
@@ -519,13 +525,16 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         const uint32_t body = use_tma ? ((valid - hw) & ~3u) : 0u;
         long long t_ph = (dbg & 8) ? clock64() : 0;
         auto phase = [&](int ph) {
-            if ((dbg & 8) && tid == 0) {
+            if ((dbg & 8) && (tid == 0 || tid == 256)) {
                 const long long now = clock64();
-                atomicAdd(&g_phase_cycles[ph], static_cast<unsigned long long>(now - t_ph));
+                atomicAdd(&g_phase_cycles[ph + (tid == 256 ? 8 : 0)], static_cast<unsigned long long>(now - t_ph));
                 t_ph = now;
             }
         };
         const bool pre = early_warp && have_next; // keys + counts of this tile already in place
+        // EARLY2: the lower warps' counts of this tile were taken by their
+        // partner early warps as well; they only load their keys
+        const bool precounted = EARLY2 && !early_warp && have_next;
         if (!pre) {
             mbar_wait_parity(&s_bar[cur], (bar_parity >> cur) & 1u);
             bar_parity ^= 1u << cur;
@@ -607,6 +616,19 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         // misaligned (non-TMA) bodies take the guarded path
         if (pre) {
             // counted during the previous tile's look-back
+        } else if (precounted) {
+            // counted by the partner early warp: keys only
+            if (full && hw == 0 && body == static_cast<uint32_t>(TILE)) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) keys[i] = buf[wbase + i * 32 + lane];
+            } else {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const uint32_t idx = wbase + i * 32 + lane;
+                    const uint32_t rel = idx - hw;
+                    keys[i] = idx < valid ? (rel < body ? buf[rel] : __ldg(src + tile_start + idx)) : 0u;
+                }
+            }
         } else if (full && hw == 0 && body == static_cast<uint32_t>(TILE)) rank_items(std::true_type{}, std::true_type{});
         else if (full) rank_items(std::true_type{}, std::false_type{});
         else rank_items(std::false_type{}, std::false_type{});
@@ -702,8 +724,13 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             };
             if (full) rank_stage(std::true_type{});
             else rank_stage(std::false_type{});
+            const uint32_t nxt = s_tile[cur ^ 1];
+            if (EARLY2 && !early_warp && nxt < ntiles) {
+                // this warp is done with its counter row: the partner early
+                // warp may reset it and count this warp's keys of the next tile
+                asm volatile("bar.arrive %0, 64;" ::"r"(2 + warp) : "memory");
+            }
             if (early_warp) {
-                const uint32_t nxt = s_tile[cur ^ 1];
                 if (nxt < ntiles) {
                     uint64_t nstart;
                     uint32_t nvalid, nfirst, nseg;
@@ -713,18 +740,28 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                     // own counter row: this tile's ranks are done with it
                     uint32_t* row = reinterpret_cast<uint32_t*>(wc);
                     for (int i = lane; i < RADIX / 2; i += 32) row[i] = 0;
+                    const uint32_t pwarp = warp - WARPS / 2; // partner lower warp
+                    if (EARLY2) {
+                        asm volatile("bar.sync %0, 64;" ::"r"(2 + pwarp) : "memory");
+                        uint32_t* prow = reinterpret_cast<uint32_t*>(s_wcnt + pwarp * RADIX);
+                        for (int i = lane; i < RADIX / 2; i += 32) prow[i] = 0;
+                    }
                     __syncwarp();
                     mbar_wait_parity(&s_bar[cur ^ 1], (bar_parity >> (cur ^ 1)) & 1u);
                     bar_parity ^= 1u << (cur ^ 1);
                     const uint32_t* nbuf = s_in + (cur ^ 1) * TILE;
+                    const uint32_t pbase = pwarp * (32 * ITEMS);
+                    const uint32_t prow_bytes = pwarp * (RADIX * 2);
                     if (nbody == static_cast<uint32_t>(TILE)) {
                         // whole tile delivered by TMA (full, 16-byte aligned): no guards
 #pragma unroll
                         for (int i = 0; i < ITEMS; ++i) keys[i] = nbuf[wbase + i * 32 + lane];
 #pragma unroll
-                        for (int i = 0; i < ITEMS; ++i) {
-                            const uint32_t d = digit_of_key<BITS>(keys[i], shift);
-                            count_digit(d);
+                        for (int i = 0; i < ITEMS; ++i) count_digit(digit_of_key<BITS>(keys[i], shift));
+                        if (EARLY2) {
+#pragma unroll
+                            for (int i = 0; i < ITEMS; ++i)
+                                count_digit_row(digit_of_key<BITS>(nbuf[pbase + i * 32 + lane], shift), prow_bytes);
                         }
                     } else {
 #pragma unroll
@@ -736,15 +773,23 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
 #pragma unroll
                         for (int i = 0; i < ITEMS; ++i) {
                             const uint32_t idx = wbase + i * 32 + lane;
-                            if (idx < nvalid) {
-                                const uint32_t d = digit_of_key<BITS>(keys[i], shift);
-                                count_digit(d);
+                            if (idx < nvalid) count_digit(digit_of_key<BITS>(keys[i], shift));
+                        }
+                        if (EARLY2) {
+#pragma unroll
+                            for (int i = 0; i < ITEMS; ++i) {
+                                const uint32_t idx = pbase + i * 32 + lane;
+                                const uint32_t rel = idx - nhw;
+                                if (idx < nvalid) {
+                                    const uint32_t k2 = rel < nbody ? nbuf[rel] : __ldg(src + nstart + idx);
+                                    count_digit_row(digit_of_key<BITS>(k2, shift), prow_bytes);
+                                }
                             }
                         }
                     }
-                    have_next = true;
                 }
             }
+            have_next = EARLY && nxt < ntiles;
         } else if (dbg & 16) {
             // timing experiment only: skip staging
         } else if (full) { // every item valid: no per-item guards
@@ -835,12 +880,15 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             s_delta[tid] = static_cast<Off>(digit_base[static_cast<uint64_t>(seg) * RADIX + tid] + prefix -
                                             s_excl[tid]);
         }
+        phase(7);
         __syncthreads();
 
         if (BSG_CLAIM_AT == 2) claim_next();
         phase(5);
         // ---- write digit runs (coalesced within each run); reset counters --
-        if (EARLY) {
+        if (EARLY2) {
+            // every counter row of the next tile was reset and filled by the early warps
+        } else if (EARLY) {
             if (!early_warp) // early warps hold the next tile's counts already
                 for (int i = lane; i < RADIX / 2; i += 32) reinterpret_cast<uint32_t*>(wc)[i] = 0;
         } else {
@@ -1600,10 +1648,11 @@ extern "C" int bsg_debug_lb_stats(unsigned long long* out4, int reset) {
     return e == cudaSuccess ? 0 : 3;
 }
 
-extern "C" int bsg_debug_phase_cycles(unsigned long long* out8, int reset) {
-    cudaError_t e = cudaMemcpyFromSymbol(out8, bsg::g_phase_cycles, sizeof(unsigned long long) * 8);
+// (out16: [0..7] thread 0 of every CTA, [8..15] thread 256)
+extern "C" int bsg_debug_phase_cycles(unsigned long long* out16, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out16, bsg::g_phase_cycles, sizeof(unsigned long long) * 16);
     if (e == cudaSuccess && reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[16] = {};
         e = cudaMemcpyToSymbol(bsg::g_phase_cycles, z, sizeof(z));
     }
     return e == cudaSuccess ? 0 : 3;
