@@ -49,6 +49,9 @@
 #ifndef BSG_LB_FAST
 #define BSG_LB_FAST 1 // look-back rounds whose words are all published aggregates take a branch-free sum
 #endif
+#ifndef BSG_EARLY_WIDE
+#define BSG_EARLY_WIDE 1 // the early count also in the segmented (PR) and 64-bit-row passes
+#endif
 #ifndef BSG_EARLY_COUNT
 #define BSG_EARLY_COUNT 2 // count-then-rank: the upper half of the warps counts the next tile during the
                           // look-back (1: their own keys, 2: all keys)
@@ -494,7 +497,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // look-back of tile k, warps [WARPS/2, WARPS) already load their keys of
     // tile k+1 (TMA-delivered to the other buffer) and count them into their
     // own (reset) counter rows; in iteration k+1 they skip the count phase.
-    constexpr bool EARLY = RANK == 3 && BSG_EARLY_COUNT && BITS == 8 && !WIDE && THREADS == 512 && ITEMS == 24 && !SEG;
+    constexpr bool EARLY = RANK == 3 && BSG_EARLY_COUNT && BITS == 8 && THREADS == 512 && ITEMS == 24 &&
+                           (BSG_EARLY_WIDE || (!WIDE && !SEG));
     // EARLY2: the early warps also count their partner lower warps' keys of
     // the next tile, so no warp counts at the top of the next iteration
     constexpr bool EARLY2 = EARLY && BSG_EARLY_COUNT >= 2;
