@@ -497,7 +497,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // look-back of tile k, warps [WARPS/2, WARPS) already load their keys of
     // tile k+1 (TMA-delivered to the other buffer) and count them into their
     // own (reset) counter rows; in iteration k+1 they skip the count phase.
-    constexpr bool EARLY = RANK == 3 && BSG_EARLY_COUNT && BITS == 8 && THREADS == 512 && ITEMS == 24 &&
+    constexpr bool EARLY = RANK == 3 && BSG_EARLY_COUNT && BITS == 8 && THREADS == 512 && ITEMS >= 20 &&
                            (BSG_EARLY_WIDE || (!WIDE && !SEG));
     // EARLY2: the early warps also count their partner lower warps' keys of
     // the next tile, so no warp counts at the top of the next iteration
@@ -1059,6 +1059,14 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
     case 7:
         return launch_onesweep_cfg<BITS, 256, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
+#if BSG_DEV_KNOBS
+    case 8: // development rows: other tile heights at two CTAs per SM
+        return launch_onesweep_cfg<BITS, 512, 22, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+    case 9:
+        return launch_onesweep_cfg<BITS, 512, 20, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
+                                                         stream, use_tma);
+#endif
     default: // 1024 threads x 16 keys: 16384-key tiles, one CTA per SM
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                           stream, use_tma);
