@@ -230,3 +230,17 @@ def test_gloo_block_networks_match_reference_stages(world, networks, orc):
         exp, _ = orc.block_network(network, k, world, stages)
         got = np.concatenate([out[r][ci] for r in range(world)])
         np.testing.assert_array_equal(got, exp, err_msg=f"network {network} stages {stages}")
+
+
+def test_exchange_sizes_checked_before_any_byte_moves():
+    """bsp_error equivalents on the host side of the orchestration
+    (radix.hpp:207-220, 283-286): a rank must send every key of its block
+    exactly once and, in PR, receive exactly its partition's size."""
+    from paper_1708_09495_b200 import _lib, distributed as D
+
+    D._check_exchange([3, 4], [2, 5], 7, 7, 0, 0)  # consistent
+    with pytest.raises(_lib.BspError, match="send counts"):
+        D._check_exchange([3, 3], [2, 5], 7, 7, 1, 2)
+    with pytest.raises(_lib.BspError, match="receive counts"):
+        D._check_exchange([3, 4], [2, 4], 7, 7, 1, 2)
+    D._check_exchange([3, 4], [9, 9], 7, None, 0, 0)  # single exchange: receive size is data-dependent
