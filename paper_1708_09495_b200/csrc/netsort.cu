@@ -871,9 +871,11 @@ int launch_block_network(int network, const uint32_t* in, uint32_t* out, uint64_
         while ((1u << logl) < L) ++logl;
         TimedScope ts(2 /*BSG_K_NETWORK*/, stream);
         const int f = full ? 1 : 0;
-        if (BSG_NET_R == 32 && L >= 32)
-            return launch_reg<32>(logl, in, out, num_arrays, len, p, P, network, run_stages, f, apc, vec_in, vec_out,
-                                  stream);
+        if constexpr (BSG_NET_R == 32) {
+            if (L >= 32)
+                return launch_reg<32>(logl, in, out, num_arrays, len, p, P, network, run_stages, f, apc, vec_in,
+                                      vec_out, stream);
+        }
         return launch_reg<16>(logl, in, out, num_arrays, len, p, P, network, run_stages, f, apc, vec_in, vec_out,
                               stream);
     }
