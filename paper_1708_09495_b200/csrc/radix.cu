@@ -49,6 +49,9 @@
 #ifndef BSG_LB_FAST
 #define BSG_LB_FAST 1 // look-back rounds whose words are all published aggregates take a branch-free sum
 #endif
+#ifndef BSG_HIST_LOADS
+#define BSG_HIST_LOADS 4 // 16-byte loads in flight per thread in the histogram kernel (2 or 4)
+#endif
 #ifndef BSG_EARLY_WIDE
 #define BSG_EARLY_WIDE 1 // the early count also in the segmented (PR) and 64-bit-row passes
 #endif
@@ -105,11 +108,22 @@ __global__ void __launch_bounds__(kHist2Threads)
     for (int i = threadIdx.x; i < COUNTERS * 32; i += kHist2Threads) sh[i] = 0;
     __syncthreads();
     uint32_t* mine = sh + lane;
+    // byte digits: one PRMT per digit and one IMAD for the lane-private
+    // counter's byte offset (d * 128 + lane * 4; digit j's table at j * 32 KiB)
+    const uint32_t sel = 0x4440u | static_cast<uint32_t>(first_shift >> 3);
+    const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
     auto count_key = [&](uint32_t key) {
 #pragma unroll
         for (int j = 0; j < NDIG; ++j) {
-            const uint32_t d = (key >> (first_shift + j * BITS)) & MASK;
-            atomicAdd(mine + (j * RADIX + d) * 32, 1u);
+            if constexpr (BITS == 8) {
+                const uint32_t d = __byte_perm(key, 0u, sel + static_cast<uint32_t>(j));
+                atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(sh) + (d * 128u + lane4) +
+                                                      j * RADIX * 128),
+                          1u);
+            } else {
+                const uint32_t d = (key >> (first_shift + j * BITS)) & MASK;
+                atomicAdd(mine + (j * RADIX + d) * 32, 1u);
+            }
         }
     };
     const uint64_t mis = (reinterpret_cast<uintptr_t>(in) >> 2) & 3;
@@ -119,6 +133,18 @@ __global__ void __launch_bounds__(kHist2Threads)
     const uint64_t nvec = (n - head) / 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kHist2Threads;
     uint64_t v = static_cast<uint64_t>(blockIdx.x) * kHist2Threads + threadIdx.x;
+#if BSG_HIST_LOADS >= 4
+    for (; v + 3 * stride < nvec; v += 4 * stride) { // four independent 16-byte loads in flight
+        const uint4 a = ldg_stream_v4(body + v);
+        const uint4 b = ldg_stream_v4(body + v + stride);
+        const uint4 c = ldg_stream_v4(body + v + 2 * stride);
+        const uint4 e = ldg_stream_v4(body + v + 3 * stride);
+        count_key(a.x); count_key(a.y); count_key(a.z); count_key(a.w);
+        count_key(b.x); count_key(b.y); count_key(b.z); count_key(b.w);
+        count_key(c.x); count_key(c.y); count_key(c.z); count_key(c.w);
+        count_key(e.x); count_key(e.y); count_key(e.z); count_key(e.w);
+    }
+#endif
     for (; v + stride < nvec; v += 2 * stride) { // two independent 16-byte loads in flight
         const uint4 a = ldg_stream_v4(body + v);
         const uint4 b = ldg_stream_v4(body + v + stride);
