@@ -466,6 +466,39 @@ __global__ void __launch_bounds__(kSegCountThreads)
     const uint32_t* blk = keys + off;
     const uint64_t step = static_cast<uint64_t>(gridDim.x) * kSegCountThreads;
     uint64_t i = static_cast<uint64_t>(blockIdx.x) * kSegCountThreads + threadIdx.x;
+    if constexpr (RADIX == 256) {
+        // byte digits: 16-byte loads (four in flight per thread), one PRMT +
+        // one IMAD per key; the block's unaligned head and tail scalar
+        const uint32_t sel = 0x4440u | static_cast<uint32_t>(shift >> 3);
+        const uint32_t lane4 = (threadIdx.x & 31u) * 4u;
+        auto cnt = [&](uint32_t k) {
+            atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(h) + __byte_perm(k, 0u, sel) * 128u +
+                                                  lane4),
+                      1u);
+        };
+        const uint64_t mis = (reinterpret_cast<uintptr_t>(blk) >> 2) & 3u;
+        const uint64_t head = min(len, mis ? 4 - mis : 0);
+        const uint4* body = reinterpret_cast<const uint4*>(blk + head);
+        const uint64_t nvec = (len - head) / 4;
+        uint64_t v = i;
+        for (; v + 3 * step < nvec; v += 4 * step) {
+            const uint4 a = ldg_stream_v4(body + v), b = ldg_stream_v4(body + v + step),
+                        c = ldg_stream_v4(body + v + 2 * step), e = ldg_stream_v4(body + v + 3 * step);
+            cnt(a.x); cnt(a.y); cnt(a.z); cnt(a.w);
+            cnt(b.x); cnt(b.y); cnt(b.z); cnt(b.w);
+            cnt(c.x); cnt(c.y); cnt(c.z); cnt(c.w);
+            cnt(e.x); cnt(e.y); cnt(e.z); cnt(e.w);
+        }
+        for (; v < nvec; v += step) {
+            const uint4 a = ldg_stream_v4(body + v);
+            cnt(a.x); cnt(a.y); cnt(a.z); cnt(a.w);
+        }
+        if (blockIdx.x == 0) {
+            for (uint64_t j = threadIdx.x; j < head; j += kSegCountThreads) cnt(__ldg(blk + j));
+            for (uint64_t j = head + nvec * 4 + threadIdx.x; j < len; j += kSegCountThreads) cnt(__ldg(blk + j));
+        }
+        i = len; // done
+    }
     for (; i + 3 * step < len; i += 4 * step) {
         const uint32_t k0 = __ldg(blk + i), k1 = __ldg(blk + i + step), k2 = __ldg(blk + i + 2 * step),
                        k3 = __ldg(blk + i + 3 * step);
@@ -491,7 +524,7 @@ int launch_pr_seg_count(const uint32_t* keys, uint64_t n, int p, int bits, int s
         return -1;
     if (n == 0) return 0;
     const uint64_t per = n / static_cast<uint64_t>(p) + 1;
-    const uint64_t want = (per + kSegCountThreads * 32 - 1) / (kSegCountThreads * 32);
+    const uint64_t want = (per + kSegCountThreads * 64 - 1) / (kSegCountThreads * 64);
     const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>(want, std::max<uint64_t>(1, kSmCountB200 * 4 / static_cast<uint64_t>(p)))));
     auto* c = reinterpret_cast<unsigned long long*>(counts);
@@ -696,7 +729,14 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     uint64_t* colchunk = dstart + radix;               // [radix / kDigChunk]
     uint32_t* skew = reinterpret_cast<uint32_t*>(colchunk + 64); // round's skew flag
 
-    if (n && (e = cudaMemcpyAsync(A, in, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
+    const uint64_t max_len0 = n / p + (n % p ? 1 : 0);
+    const bool fused0 = bits == 8 || (bits < 8 && max_len0 <= kChunkKeys);
+    // fused rounds read the input directly and the last one writes `out`
+    // directly; only a single round over overlapping in/out goes through A
+    const bool direct = fused0 && rounds >= 1 &&
+                        !(rounds == 1 && static_cast<const void*>(in) < static_cast<const void*>(out + n) &&
+                          static_cast<const void*>(out) < static_cast<const void*>(in + n));
+    if (n && !direct && (e = cudaMemcpyAsync(A, in, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
         return cuda_fail(e, "pr copy in");
     bsg_run_stats st{};
     std::vector<uint64_t> h_send(pp);
@@ -717,10 +757,13 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     uint32_t* nxt = S;
     for (int round = 0; round < rounds && n && fused; ++round) {
         const int shift = round * bits;
+        // round sources and destinations: input -> S -> A -> ... -> out
+        const uint32_t* src = (direct && round == 0) ? in : cur;
+        uint32_t* dst = (direct && round == rounds - 1) ? out : nxt;
         uint64_t* counts = starts; // [p][radix]
         int64_t* base = gd;        // [p][radix]
         // count_digits of every worker (radix.hpp:127-132), one launch
-        if (!add(launch_pr_seg_count(cur, n, p, bits, shift, counts, stream)))
+        if (!add(launch_pr_seg_count(src, n, p, bits, shift, counts, stream)))
             return cuda_fail(cudaGetLastError(), "pr count");
         {
             TimedScope ts(3 /*BSG_K_PR*/, stream);
@@ -735,7 +778,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         }
         // every worker's local stable pass, stored at the global positions
         // (sort_and_scatter + exchange + gather_slices), one segmented launch
-        if (!add(launch_onesweep_seg(cur, nxt, n, p, bits, shift, reinterpret_cast<const uint64_t*>(base),
+        if (!add(launch_onesweep_seg(src, dst, n, p, bits, shift, reinterpret_cast<const uint64_t*>(base),
                                      ctx->status.as<uint32_t>(), stream, skew)))
             return cuda_fail(cudaGetLastError(), "pr fused pass");
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
@@ -842,7 +885,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         st.words_delivered = st.words_sent;
         *stats = st;
     }
-    if (n && (e = cudaMemcpyAsync(out, A, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
+    if (n && !direct && (e = cudaMemcpyAsync(out, A, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
         return cuda_fail(e, "pr copy out");
     ctx->launches += launches;
     return BSG_OK;
