@@ -733,9 +733,13 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     const bool fused0 = bits == 8 || (bits < 8 && max_len0 <= kChunkKeys);
     // fused rounds read the input directly and the last one writes `out`
     // directly; only a single round over overlapping in/out goes through A
-    const bool direct = fused0 && rounds >= 1 &&
-                        !(rounds == 1 && static_cast<const void*>(in) < static_cast<const void*>(out + n) &&
-                          static_cast<const void*>(out) < static_cast<const void*>(in + n));
+    // (r = 2^16: round 0's byte sub-passes read the input, the last round's
+    // scatter writes `out`; in place is safe, the scatter runs after every read)
+    const bool seg16_0 = !fused0 && bits == 16;
+    const bool direct = (fused0 && rounds >= 1 &&
+                         !(rounds == 1 && static_cast<const void*>(in) < static_cast<const void*>(out + n) &&
+                           static_cast<const void*>(out) < static_cast<const void*>(in + n))) ||
+                        (seg16_0 && rounds >= 1);
     if (n && !direct && (e = cudaMemcpyAsync(A, in, n * 4, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
         return cuda_fail(e, "pr copy in");
     bsg_run_stats st{};
@@ -829,15 +833,16 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             int64_t* bA = gd;
             int64_t* bB = gd + static_cast<uint64_t>(p) * 256;
             uint32_t* mid = ctx->stage_b.as<uint32_t>();
-            if (!add(launch_pr_seg_count(A, n, p, 8, shift, cA, stream)) ||
-                !add(launch_pr_seg_count(A, n, p, 8, shift + 8, cB, stream)))
+            const uint32_t* src = (direct && round == 0) ? in : A;
+            if (!add(launch_pr_seg_count(src, n, p, 8, shift, cA, stream)) ||
+                !add(launch_pr_seg_count(src, n, p, 8, shift + 8, cB, stream)))
                 return cuda_fail(cudaGetLastError(), "pr local count");
             if ((e = cudaMemsetAsync(skew, 0, 2 * sizeof(uint32_t), stream)) != cudaSuccess)
                 return cuda_fail(e, "pr local count");
             pr_local_base_kernel<<<p, 256, 0, stream>>>(cA, n, p, bA, skew);
             pr_local_base_kernel<<<p, 256, 0, stream>>>(cB, n, p, bB, skew + 1);
             launches += 2;
-            if (!add(launch_onesweep_seg(A, mid, n, p, 8, shift, reinterpret_cast<const uint64_t*>(bA),
+            if (!add(launch_onesweep_seg(src, mid, n, p, 8, shift, reinterpret_cast<const uint64_t*>(bA),
                                          ctx->status.as<uint32_t>(), stream, skew)) ||
                 !add(launch_onesweep_seg(mid, S, n, p, 8, shift + 8, reinterpret_cast<const uint64_t*>(bB),
                                          ctx->status.as<uint32_t>(), stream, skew + 1)))
@@ -856,7 +861,9 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             const uint64_t want = (max_len + kScatterThreads * kScatterItems - 1) / (kScatterThreads * kScatterItems);
             const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(
                 1, std::min<uint64_t>(want, std::max<uint64_t>(1, kSmCountB200 * 8 / static_cast<uint64_t>(p)))));
-            pr_scatter_kernel<<<dim3(gx, p), kScatterThreads, 0, stream>>>(S, n, p, shift, mask, radix, dstart, gd, A);
+            uint32_t* rebuilt = (direct && round == rounds - 1) ? out : A;
+            pr_scatter_kernel<<<dim3(gx, p), kScatterThreads, 0, stream>>>(S, n, p, shift, mask, radix, dstart, gd,
+                                                                          rebuilt);
             launches += 4;
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");

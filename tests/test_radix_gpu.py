@@ -312,12 +312,12 @@ def test_in_place_calls(cuda, bsg, orc):
         # in place with 1 and 2 rounds (the fused rounds read the input and
         # write the output directly; a single round over in == out goes
         # through the workspace)
-        for rounds in (1, 2):
+        for bits, rounds in ((8, 1), (8, 2), (16, 1), (16, 2)):
             t = torch.from_numpy(keys.view(np.int32)).cuda()
-            assert L.bsg_parallel_radix_sort_u32(ctx.handle, t.data_ptr(), t.data_ptr(), n, 3, 8, rounds, None, 1,
+            assert L.bsg_parallel_radix_sort_u32(ctx.handle, t.data_ptr(), t.data_ptr(), n, 3, bits, rounds, None, 1,
                                                  st) == 0
             torch.cuda.synchronize()
-            exp, _ = orc.parallel_radix(keys, 3, 256, rounds)
+            exp, _ = orc.parallel_radix(keys, 3, 1 << bits, rounds)
             np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32), exp)
     arrs = orc.generate_uniform_keys(64 * 4096, 3).reshape(64, 4096)
     t = torch.from_numpy(arrs.reshape(-1).view(np.int32)).cuda()
