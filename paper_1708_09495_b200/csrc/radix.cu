@@ -363,7 +363,17 @@ struct SegDesc {
     uint32_t p, nbig;     // nbig = n % p
     uint32_t tiles_big;   // ceil((small + 1) / TILE)
     uint32_t tiles_small; // ceil(small / TILE)
+    uint64_t mbig, msmall; // ceil(2^64 / tiles_*): x / d = umul64hi(x, m) for 32-bit x (d > 1)
+    void set_magic() {
+        mbig = tiles_big > 1 ? ~0ull / tiles_big + 1 : 0;
+        msmall = tiles_small > 1 ? ~0ull / tiles_small + 1 : 0;
+    }
 };
+// x / d for 32-bit x without a division sequence (m = ceil(2^64 / d); exact
+// because x * (m * d - 2^64) < 2^64)
+__device__ __forceinline__ uint32_t div_magic(uint32_t x, uint32_t d, uint64_t m) {
+    return d > 1 ? static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(x), m)) : x;
+}
 struct SegTile {
     uint32_t seg, first; // segment and its first tile id
     uint64_t start, end; // key range of the segment
@@ -373,10 +383,10 @@ __device__ __forceinline__ SegTile seg_of_tile(const SegDesc& sd, uint32_t tile)
     SegTile r;
     const uint32_t big_tiles = sd.nbig * sd.tiles_big;
     if (tile < big_tiles) {
-        r.seg = tile / sd.tiles_big;
+        r.seg = div_magic(tile, sd.tiles_big, sd.mbig);
         r.first = r.seg * sd.tiles_big;
     } else {
-        r.seg = sd.nbig + (sd.tiles_small ? (tile - big_tiles) / sd.tiles_small : 0u);
+        r.seg = sd.nbig + (sd.tiles_small ? div_magic(tile - big_tiles, sd.tiles_small, sd.msmall) : 0u);
         r.first = big_tiles + (r.seg - sd.nbig) * sd.tiles_small;
     }
     r.start = static_cast<uint64_t>(r.seg) * sd.small + (r.seg < sd.nbig ? r.seg : sd.nbig);
@@ -1401,6 +1411,7 @@ int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int 
     sd.nbig = static_cast<uint32_t>(n % static_cast<uint64_t>(p));
     sd.tiles_big = static_cast<uint32_t>((sd.small + 1 + L::TILE - 1) / L::TILE);
     sd.tiles_small = static_cast<uint32_t>((sd.small + L::TILE - 1) / L::TILE);
+    sd.set_magic();
     const uint64_t tiles = static_cast<uint64_t>(sd.nbig) * sd.tiles_big +
                            static_cast<uint64_t>(sd.p - sd.nbig) * sd.tiles_small;
     if (tiles == 0) return 0;
@@ -1469,6 +1480,7 @@ int launch_onesweep_seg_peer_cfg(const uint32_t* src, uint64_t n, int p, int shi
     sd.nbig = static_cast<uint32_t>(n % static_cast<uint64_t>(p));
     sd.tiles_big = static_cast<uint32_t>((sd.small + 1 + L::TILE - 1) / L::TILE);
     sd.tiles_small = static_cast<uint32_t>((sd.small + L::TILE - 1) / L::TILE);
+    sd.set_magic();
     const uint64_t tiles = static_cast<uint64_t>(sd.nbig) * sd.tiles_big +
                            static_cast<uint64_t>(sd.p - sd.nbig) * sd.tiles_small;
     if (tiles == 0) return 0;
