@@ -729,14 +729,17 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     uint64_t* colchunk = dstart + radix;               // [radix / kDigChunk]
     uint32_t* skew = reinterpret_cast<uint32_t*>(colchunk + 64); // round's skew flag
 
-    const uint64_t max_len0 = n / p + (n % p ? 1 : 0);
-    const bool fused0 = bits == 8 || (bits < 8 && max_len0 <= kChunkKeys);
+    const uint64_t max_len = n / p + (n % p ? 1 : 0);
+    // r <= 2^8: each worker's whole round is ONE one-sweep pass whose digit
+    // bases are the global positions of its block's first key per digit
+    // (the same fused round as bsg_pr_fused_round, all blocks local)
+    const bool fused = bits == 8 || (bits < 8 && max_len <= kChunkKeys); // 8-bit: 64-bit rows above 2^29
     // fused rounds read the input directly and the last one writes `out`
     // directly; only a single round over overlapping in/out goes through A
     // (r = 2^16: round 0's byte sub-passes read the input, the last round's
     // scatter writes `out`; in place is safe, the scatter runs after every read)
-    const bool seg16_0 = !fused0 && bits == 16;
-    const bool direct = (fused0 && rounds >= 1 &&
+    const bool seg16_0 = !fused && bits == 16;
+    const bool direct = (fused && rounds >= 1 &&
                          !(rounds == 1 && static_cast<const void*>(in) < static_cast<const void*>(out + n) &&
                            static_cast<const void*>(out) < static_cast<const void*>(in + n))) ||
                         (seg16_0 && rounds >= 1);
@@ -750,11 +753,6 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         launches += static_cast<uint64_t>(l);
         return true;
     };
-    const uint64_t max_len = n / p + (n % p ? 1 : 0);
-    // r <= 2^8: each worker's whole round is ONE one-sweep pass whose digit
-    // bases are the global positions of its block's first key per digit
-    // (the same fused round as bsg_pr_fused_round, all blocks local)
-    const bool fused = bits == 8 || (bits < 8 && max_len <= kChunkKeys); // 8-bit: 64-bit rows above 2^29
     if (fused && (e = ctx->status.ensure(onesweep_seg_status_words(n, p) * sizeof(uint32_t))) != cudaSuccess)
         return cuda_fail(e, "pr workspace");
     uint32_t* cur = A;
