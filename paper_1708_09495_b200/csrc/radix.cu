@@ -342,7 +342,8 @@ struct OnesweepSmem {
     static constexpr size_t scan_off = tcnt_off + sizeof(uint32_t) * RADIX;      // 32 u32
     static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 32;         // 2 tile ids
     static constexpr size_t bar_off = misc_off + 16;                              // 2 mbarriers
-    static constexpr size_t bytes = bar_off + 16;
+    static constexpr size_t range_off = bar_off + 16;                             // 2 x 32 B tile ranges (SEG)
+    static constexpr size_t bytes = range_off + 64;
 };
 
 // dbg bits (timing experiments only; output is wrong when set):
@@ -479,12 +480,33 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     const int lane = tid & 31;
     const int warp = tid >> 5;
 
+    // Segmented passes: the tile -> (segment, key range) map is computed once
+    // per tile by the claiming thread and read by the others from shared
+    // memory (s_range[buffer]: start, valid, first tile, segment)
+    uint64_t* s_range = reinterpret_cast<uint64_t*>(smem + L::range_off);
+    auto buffer_range = [&](uint32_t tile, int b, uint64_t& start, uint32_t& valid, uint32_t& first, uint32_t& seg) {
+        if constexpr (SEG) {
+            (void)tile;
+            start = s_range[4 * b];
+            const uint64_t vf = s_range[4 * b + 1];
+            valid = static_cast<uint32_t>(vf);
+            first = static_cast<uint32_t>(vf >> 32);
+            seg = static_cast<uint32_t>(s_range[4 * b + 2]);
+        } else {
+            tile_range(tile, start, valid, first, seg);
+        }
+    };
     // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
     auto issue = [&](uint32_t tile, int b) {
         if (tile >= ntiles) return;
         uint64_t start;
         uint32_t valid, first_unused, seg_unused;
         tile_range(tile, start, valid, first_unused, seg_unused);
+        if constexpr (SEG) {
+            s_range[4 * b] = start;
+            s_range[4 * b + 1] = static_cast<uint64_t>(valid) | (static_cast<uint64_t>(first_unused) << 32);
+            s_range[4 * b + 2] = seg_unused;
+        }
         // TMA moves the tile's 16-byte-aligned body; the <= 3 head and <= 3
         // tail keys are read with plain loads by the ranking threads
         const uint32_t hw = head_words(src + start, valid);
@@ -557,7 +579,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         if (BSG_CLAIM_AT == 0) claim_next();
         uint64_t tile_start;
         uint32_t valid, tfirst, seg;
-        tile_range(tile, tile_start, valid, tfirst, seg);
+        buffer_range(tile, cur, tile_start, valid, tfirst, seg);
         const bool full = valid == TILE;
         uint32_t* buf = s_in + cur * TILE;
         // non-TMA body / unaligned tail straight from global
@@ -774,7 +796,7 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 if (nxt < ntiles) {
                     uint64_t nstart;
                     uint32_t nvalid, nfirst, nseg;
-                    tile_range(nxt, nstart, nvalid, nfirst, nseg);
+                    buffer_range(nxt, cur ^ 1, nstart, nvalid, nfirst, nseg);
                     const uint32_t nhw = head_words(src + nstart, nvalid);
                     const uint32_t nbody = use_tma ? ((nvalid - nhw) & ~3u) : 0u;
                     // own counter row: this tile's ranks are done with it
