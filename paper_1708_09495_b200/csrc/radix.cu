@@ -49,6 +49,9 @@
 #ifndef BSG_LB_FAST
 #define BSG_LB_FAST 1 // look-back rounds whose words are all published aggregates take a branch-free sum
 #endif
+#ifndef BSG_RANGE_CACHE
+#define BSG_RANGE_CACHE 1 // every pass: the claiming thread computes a tile's range once (shared memory)
+#endif
 #ifndef BSG_HIST_LOADS
 #define BSG_HIST_LOADS 4 // 16-byte loads in flight per thread in the histogram kernel (2 or 4)
 #endif
@@ -484,16 +487,24 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     // per tile by the claiming thread and read by the others from shared
     // memory (s_range[buffer]: start, valid, first tile, segment)
     uint64_t* s_range = reinterpret_cast<uint64_t*>(smem + L::range_off);
-    auto buffer_range = [&](uint32_t tile, int b, uint64_t& start, uint32_t& valid, uint32_t& first, uint32_t& seg) {
-        if constexpr (SEG) {
+    constexpr bool RCACHE = SEG || BSG_RANGE_CACHE;
+    auto buffer_range = [&](uint32_t tile, int b, uint64_t& start, uint32_t& valid, uint32_t& first, uint32_t& seg,
+                            uint32_t& hw, uint32_t& body) {
+        if constexpr (RCACHE) {
             (void)tile;
             start = s_range[4 * b];
             const uint64_t vf = s_range[4 * b + 1];
             valid = static_cast<uint32_t>(vf);
             first = static_cast<uint32_t>(vf >> 32);
-            seg = static_cast<uint32_t>(s_range[4 * b + 2]);
+            const uint64_t sh = s_range[4 * b + 2];
+            seg = static_cast<uint32_t>(sh);
+            const uint32_t hb = static_cast<uint32_t>(sh >> 32); // head words (2 bits) | TMA body << 2
+            hw = hb & 3u;
+            body = hb >> 2;
         } else {
             tile_range(tile, start, valid, first, seg);
+            hw = head_words(src + start, valid);
+            body = use_tma ? ((valid - hw) & ~3u) : 0u;
         }
     };
     // Issues the load of `tile` into buffer b (TMA for the 16B-aligned body).
@@ -502,10 +513,12 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         uint64_t start;
         uint32_t valid, first_unused, seg_unused;
         tile_range(tile, start, valid, first_unused, seg_unused);
-        if constexpr (SEG) {
+        if constexpr (RCACHE) {
+            const uint32_t h = head_words(src + start, valid);
+            const uint32_t bd = use_tma ? ((valid - h) & ~3u) : 0u;
             s_range[4 * b] = start;
             s_range[4 * b + 1] = static_cast<uint64_t>(valid) | (static_cast<uint64_t>(first_unused) << 32);
-            s_range[4 * b + 2] = seg_unused;
+            s_range[4 * b + 2] = static_cast<uint64_t>(seg_unused) | (static_cast<uint64_t>(h | (bd << 2)) << 32);
         }
         // TMA moves the tile's 16-byte-aligned body; the <= 3 head and <= 3
         // tail keys are read with plain loads by the ranking threads
@@ -578,13 +591,11 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
         };
         if (BSG_CLAIM_AT == 0) claim_next();
         uint64_t tile_start;
-        uint32_t valid, tfirst, seg;
-        buffer_range(tile, cur, tile_start, valid, tfirst, seg);
+        uint32_t valid, tfirst, seg, hw, body;
+        buffer_range(tile, cur, tile_start, valid, tfirst, seg, hw, body);
         const bool full = valid == TILE;
         uint32_t* buf = s_in + cur * TILE;
         // non-TMA body / unaligned tail straight from global
-        const uint32_t hw = head_words(src + tile_start, valid);
-        const uint32_t body = use_tma ? ((valid - hw) & ~3u) : 0u;
         long long t_ph = (dbg & 8) ? clock64() : 0;
         auto phase = [&](int ph) {
             if ((dbg & 8) && (tid == 0 || tid == 256)) {
@@ -796,9 +807,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                 if (nxt < ntiles) {
                     uint64_t nstart;
                     uint32_t nvalid, nfirst, nseg;
-                    buffer_range(nxt, cur ^ 1, nstart, nvalid, nfirst, nseg);
-                    const uint32_t nhw = head_words(src + nstart, nvalid);
-                    const uint32_t nbody = use_tma ? ((nvalid - nhw) & ~3u) : 0u;
+                    uint32_t nhw, nbody;
+                    buffer_range(nxt, cur ^ 1, nstart, nvalid, nfirst, nseg, nhw, nbody);
                     // own counter row: this tile's ranks are done with it
                     uint32_t* row = reinterpret_cast<uint32_t*>(wc);
                     for (int i = lane; i < RADIX / 2; i += 32) row[i] = 0;
