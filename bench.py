@@ -52,6 +52,17 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _first_pass_roofline(f_ms, f_cnt, alg_bytes, peak):
+    """The first pass of a full sort (K3f: no order inside a digit run), same
+    8 B/key, timed live like the stable pass."""
+    if not f_cnt:
+        return None
+    per = f_ms / f_cnt
+    ach = alg_bytes / (per / 1e3) / 1e9
+    return {"kernel": "first_pass_kernel (pass 0 of a full sort)", "avg_launch_ms": per, "achieved": ach,
+            "frac": ach / peak, "launches_per_sort": f_cnt / 3}
+
+
 def _traffic(kernel: str, n: int):
     """dram__bytes_read+write per launch from the committed ncu capture."""
     try:
@@ -288,6 +299,7 @@ def run_single(args):
         step()
     os_ms, os_cnt = ctx.kernel_time(_lib.K_ONESWEEP)
     h_ms, h_cnt = ctx.kernel_time(_lib.K_HIST)
+    f_ms, f_cnt = ctx.kernel_time(_lib.K_FIRST_PASS)
     ctx.set_timing(False)
     per_launch_s = os_ms / max(os_cnt, 1) / 1e3
     alg_bytes = 8.0 * n  # one read + one write of every key per pass
@@ -371,8 +383,9 @@ def run_single(args):
                      "traffic": traffic, "kernel": "onesweep_kernel (one stable 8-bit pass)",
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": per_launch_s * 1e3,
                      "peak_source": peak_src, "frac_of_8TBps_nominal": achieved / 8000.0,
-                     "traffic_source": tsrc},
-        "kernels_ms_per_sort": {"onesweep": os_ms / 3, "hist": h_ms / 3},
+                     "traffic_source": tsrc,
+                     "first_pass": _first_pass_roofline(f_ms, f_cnt, alg_bytes, peak)},
+        "kernels_ms_per_sort": {"onesweep": os_ms / 3, "first_pass": f_ms / 3, "hist": h_ms / 3},
         "clocks": clk.summary(),
         "verified": ok and ok_e2e,
     }

@@ -991,6 +991,207 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3f: the first pass of a full keys-only sort (pass 0 of bsg_radix_sort_u32).
+// An LSD sort needs pass k to leave the keys ordered by their low 8(k+1) bits.
+// For k > 0 that takes a stable pass (keys with equal digit k keep the order
+// of their lower digits); for the first pass nothing below the digit exists,
+// so keys with equal digit 0 may land in any order inside their digit run and
+// the final sorted array is unchanged (keys equal in every byte are equal).
+// The single count-sort round (bsg_count_sort_round_u32, radix.hpp:44-65),
+// whose output is observable, always takes the stable K3.  Here:
+//   - no ballots: a key's slot inside its tile run is an atomicAdd on a
+//     shared-memory cursor; counters are private to a lane quad (counter
+//     (d, q) at word d*8 + q, q = lane/4: bank 8*(d&3) + q), so only lanes of
+//     one quad can meet in a bank -- about 2 wavefronts per 32 keys instead of
+//     ~3.5 for a warp-shared row, and at most 4 for any skew;
+//   - no look-back: a tile reserves its slice of digit d's output run with one
+//     global atomicAdd per digit (runs are filled in claim order, not tile
+//     order).  Status words are not used.
+// Tiles, TMA double buffering and the coalesced write-out are K3's.
+// ---------------------------------------------------------------------------
+constexpr int kFirstGroups = 8; // counter copies per digit (lane quads)
+
+template <int THREADS, int ITEMS, bool WIDE>
+struct FirstPassSmem {
+    static constexpr int TILE = THREADS * ITEMS;
+    using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
+    static constexpr size_t in_off = 0;                                           // 2 x TILE u32
+    static constexpr size_t cnt_off = in_off + sizeof(uint32_t) * 2 * TILE;       // 256 x 8 u32
+    static constexpr size_t delta_off = cnt_off + sizeof(uint32_t) * 256 * kFirstGroups; // 256 Off
+    static constexpr size_t scan_off = delta_off + sizeof(uint64_t) * 256;       // 8 u32
+    static constexpr size_t misc_off = scan_off + sizeof(uint32_t) * 8;          // 2 tile ids, 2 (head, body)
+    static constexpr size_t bar_off = misc_off + 16;                               // 2 mbarriers
+    static constexpr size_t bytes = bar_off + 16;
+};
+
+template <int THREADS, int ITEMS, bool WIDE>
+__global__ void __launch_bounds__(THREADS, 2)
+    first_pass_kernel(const PassPlan* __restrict__ plan, uint64_t n, const uint64_t* __restrict__ digit_base,
+                      unsigned long long* __restrict__ reserve, uint32_t* __restrict__ tile_counter, int use_tma) {
+    using L = FirstPassSmem<THREADS, ITEMS, WIDE>;
+    using Off = typename L::Off;
+    constexpr int TILE = L::TILE;
+    constexpr int WARPS = THREADS / 32;
+    static_assert(THREADS >= 256, "one thread per digit in the scan");
+    extern __shared__ __align__(128) uint8_t smem[];
+    if (!plan->active[0]) return;
+    const uint32_t* __restrict__ src = plan->src[0];
+    uint32_t* __restrict__ dst = plan->dst[0];
+    uint32_t* s_in = reinterpret_cast<uint32_t*>(smem + L::in_off);
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L::cnt_off);
+    Off* s_delta = reinterpret_cast<Off*>(smem + L::delta_off);
+    uint32_t* s_scan = reinterpret_cast<uint32_t*>(smem + L::scan_off);
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + L::misc_off); // [0..1] tile ids, [2..3] head | body << 2
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+    const uint32_t ntiles = static_cast<uint32_t>((n + TILE - 1) / TILE);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    auto issue = [&](uint32_t tile, int b) {
+        if (tile >= ntiles) return;
+        const uint64_t start = static_cast<uint64_t>(tile) * TILE;
+        const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), n - start));
+        const uint32_t hw = head_words(src + start, valid);
+        const uint32_t body = use_tma ? ((valid - hw) & ~3u) : 0u;
+        s_tile[2 + b] = hw | (body << 2);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_bar[b], body * 4);
+        if (body) tma_bulk_g2s(s_in + b * TILE, src + start + hw, body * 4, &s_bar[b]);
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+        const uint32_t t0 = atomicAdd(tile_counter, 1u);
+        s_tile[0] = t0;
+        issue(t0, 0);
+    }
+    for (int i = tid; i < 256 * kFirstGroups; i += THREADS) s_cnt[i] = 0;
+
+    // counter (d, q) byte offset: d * 32 + q * 4 = ((key << 5) & 0x1FE0) | q4
+    const uint32_t q4 = static_cast<uint32_t>(lane >> 2) * 4u;
+    auto cnt_off = [&](uint32_t key) {
+        uint32_t o;
+        asm("lop3.b32 %0, %1, 0x1FE0, %2, 0xEA;" : "=r"(o) : "r"(key << 5), "r"(q4)); // (a & b) | c
+        return o;
+    };
+    uint8_t* cnt_base = smem + L::cnt_off;
+    uint32_t parity = 0;
+    uint32_t keys[ITEMS];
+    for (uint32_t k = 0;; ++k) {
+        const int cur = k & 1;
+        __syncthreads(); // s_tile[cur] visible; the previous tile's buffer, counters and deltas are free
+        const uint32_t tile = s_tile[cur];
+        if (tile >= ntiles) break;
+        if (tid == 0) {
+            const uint32_t nxt = atomicAdd(tile_counter, 1u);
+            s_tile[cur ^ 1] = nxt;
+            issue(nxt, cur ^ 1);
+        }
+        const uint64_t start = static_cast<uint64_t>(tile) * TILE;
+        const uint32_t valid = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), n - start));
+        const uint32_t hb = s_tile[2 + cur];
+        const uint32_t hw = hb & 3u, body = hb >> 2;
+        uint32_t* buf = s_in + cur * TILE;
+        mbar_wait_parity(&s_bar[cur], (parity >> cur) & 1u);
+        parity ^= 1u << cur;
+        const bool fast = body == static_cast<uint32_t>(TILE); // full tile, all of it delivered by TMA
+        const uint32_t wbase = warp * (32 * ITEMS);
+
+        // ---- load + count (4 bytes per key: counters hold byte offsets) ----
+        if (fast) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) keys[i] = buf[wbase + i * 32 + lane];
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) atomicAdd(reinterpret_cast<uint32_t*>(cnt_base + cnt_off(keys[i])), 4u);
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t idx = wbase + i * 32 + lane;
+                const uint32_t rel = idx - hw; // wraps for head keys
+                keys[i] = idx < valid ? (rel < body ? buf[rel] : __ldg(src + start + idx)) : 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i)
+                if (wbase + i * 32 + lane < valid)
+                    atomicAdd(reinterpret_cast<uint32_t*>(cnt_base + cnt_off(keys[i])), 4u);
+        }
+        __syncthreads();
+
+        // ---- digit d = tid: quad prefixes -> cursors, tile run start, reservation
+        uint32_t total = 0, excl = 0;
+        unsigned long long reserved = 0;
+        if (tid < 256) {
+            uint4* row = reinterpret_cast<uint4*>(s_cnt + tid * kFirstGroups);
+            const uint4 a = row[0], b = row[1];
+            uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint32_t run = 0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const uint32_t v = c[g];
+                c[g] = run;
+                run += v;
+            }
+            total = run; // bytes
+            if (total) reserved = atomicAdd(&reserve[tid], static_cast<unsigned long long>(total >> 2));
+            const uint32_t incl = warp_inclusive_scan(total);
+            if (lane == 31) s_scan[warp] = incl;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            excl = incl - total;
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+                if (w < warp) excl += s_scan[w];
+            row[0] = make_uint4(c[0] + excl, c[1] + excl, c[2] + excl, c[3] + excl);
+            row[1] = make_uint4(c[4] + excl, c[5] + excl, c[6] + excl, c[7] + excl);
+        }
+        __syncthreads();
+
+        // ---- slot per key, staged in digit order in place ------------------
+        uint8_t* bufb = reinterpret_cast<uint8_t*>(buf);
+        if (fast) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t pos = atomicAdd(reinterpret_cast<uint32_t*>(cnt_base + cnt_off(keys[i])), 4u);
+                *reinterpret_cast<uint32_t*>(bufb + pos) = keys[i];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i)
+                if (wbase + i * 32 + lane < valid) {
+                    const uint32_t pos = atomicAdd(reinterpret_cast<uint32_t*>(cnt_base + cnt_off(keys[i])), 4u);
+                    *reinterpret_cast<uint32_t*>(bufb + pos) = keys[i];
+                }
+        }
+        if (tid < 256) {
+            // the tile's run of digit d starts at staged index excl/4 and at
+            // output index digit_base[d] + reserved
+            s_delta[tid] = static_cast<Off>(digit_base[tid] + reserved - (excl >> 2));
+        }
+        __syncthreads();
+        if (tid < 256) {
+            uint4* row = reinterpret_cast<uint4*>(s_cnt + tid * kFirstGroups);
+            row[0] = make_uint4(0, 0, 0, 0);
+            row[1] = make_uint4(0, 0, 0, 0);
+        }
+
+        // ---- write digit runs (coalesced within each run) ------------------
+        if (valid == static_cast<uint32_t>(TILE)) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t i = j * THREADS + tid;
+                const uint32_t key = buf[i];
+                dst[static_cast<Off>(s_delta[key & 0xFFu] + i)] = key;
+            }
+        } else {
+            for (uint32_t i = tid; i < valid; i += THREADS) {
+                const uint32_t key = buf[i];
+                dst[static_cast<Off>(s_delta[key & 0xFFu] + i)] = key;
+            }
+        }
+    }
+    (void)WARPS;
+}
+
 #ifndef BSG_OS_MINB16
 #define BSG_OS_MINB16 2 // CTAs per SM the 512 x 16 row is compiled for
 #endif
@@ -1042,6 +1243,14 @@ inline int onesweep_dbg() {
     static int d = dev_knob("BSG_OS_DBG", 0);
     return d;
 }
+
+// K3f for the first pass of full sorts (bsg_debug_set_first_pass toggles it:
+// tests compare both paths)
+inline int& first_pass_ref() {
+    static int on = dev_knob("BSG_FIRST_PASS", 1);
+    return on;
+}
+inline bool first_pass_enabled() { return first_pass_ref() != 0; }
 
 inline int onesweep_rank_mode() {
     static int r = dev_knob("BSG_OS_RANK", 0);
@@ -1139,6 +1348,32 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                           stream, use_tma);
     }
+}
+
+// First pass of a full sort (K3f): [tile counter (32 words)][256 x u64 run
+// reservations].  Returns 1 (launches) or -1.
+template <int THREADS, int ITEMS, bool WIDE>
+int launch_first_pass_cfg(const PassPlan* plan, uint64_t n, const uint64_t* base_for_pass, uint32_t* status,
+                          cudaStream_t stream, bool use_tma) {
+    using L = FirstPassSmem<THREADS, ITEMS, WIDE>;
+    auto kern = first_pass_kernel<THREADS, ITEMS, WIDE>;
+    static PerDeviceOccupancy occ; // one per instantiation: the smem attribute is per kernel and device
+    const int per_sm = std::max(1, kernel_occupancy(occ, kern, THREADS, L::bytes));
+    const uint32_t tiles = static_cast<uint32_t>((n + L::TILE - 1) / L::TILE);
+    const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(current_sm_count() * per_sm));
+    if (cudaMemsetAsync(status, 0, (32 + 512) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
+    TimedScope ts(4 /*BSG_K_FIRST_PASS*/, stream);
+    kern<<<grid, THREADS, L::bytes, stream>>>(plan, n, base_for_pass, reinterpret_cast<unsigned long long*>(status + 32),
+                                               status, use_tma ? 1 : 0);
+    return 1;
+}
+
+int launch_first_pass(const PassPlan* plan, uint64_t n, const uint64_t* base_for_pass, uint32_t* status,
+                      cudaStream_t stream, bool use_tma) {
+    if (n > kChunkKeys) return launch_first_pass_cfg<512, 24, true>(plan, n, base_for_pass, status, stream, use_tma);
+    if (n <= (uint64_t{1} << 25))
+        return launch_first_pass_cfg<512, 16, false>(plan, n, base_for_pass, status, stream, use_tma);
+    return launch_first_pass_cfg<512, 24, false>(plan, n, base_for_pass, status, stream, use_tma);
 }
 
 template <int BITS>
@@ -1603,7 +1838,15 @@ int launch_byte_passes(const uint32_t* in, uint32_t* out, uint64_t n, int first_
                                                      ws.plan, in, out, ws.tmp, 1);
     ++launches;
     const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
+    // a full sort's first pass needs no order inside a digit run (K3f)
+    const bool first_free = passes == 4 && first_byte == 0 && first_pass_enabled();
     for (int p = 0; p < passes && n; ++p) {
+        if (p == 0 && first_free) {
+            const int l = launch_first_pass(ws.plan, n, ws.base, ws.status, stream, tma);
+            if (l < 0) return -1;
+            launches += l;
+            continue;
+        }
         const int l = launch_onesweep_pass<8>(ws.plan, p, n, 8 * (first_byte + p), ws.base + p * RADIX, passes,
                                               ws.status, stream, tma);
         if (l < 0) return -1;
@@ -1708,6 +1951,14 @@ int launch_digit_counts(const uint32_t* in, uint64_t n, int bits, int shift, uin
 extern "C" int bsg_debug_set_onesweep_cfg(int cfg) {
     const int prev = bsg::onesweep_cfg_ref();
     bsg::onesweep_cfg_ref() = cfg;
+    return prev;
+}
+
+// Test aid: enables/disables K3f for the first pass of full sorts (on < 0:
+// query only); returns the previous setting.
+extern "C" int bsg_debug_set_first_pass(int on) {
+    const int prev = bsg::first_pass_ref();
+    if (on >= 0) bsg::first_pass_ref() = on;
     return prev;
 }
 

@@ -409,3 +409,44 @@ def test_pageable_host_staging(cuda, bsg, orc):
         np.testing.assert_array_equal(out, orc.count_sort_round(view, 2, 256))
     keys = orc.generate_uniform_keys((1 << 25) + 7, 3)
     np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+
+
+@pytest.mark.parametrize("first", [0, 1])
+def test_first_pass_both_paths(cuda, bsg, orc, first):
+    """Pass 0 of a full sort runs K3f (no order inside a digit run, per-tile
+    run reservations by global atomics) or the stable K3: both must give the
+    oracle's sorted array.  Ragged sizes for both tile rows (8192 and 12288
+    keys), misaligned device pointers (head keys outside the TMA body), skewed
+    and two-valued low bytes (counter contention), and a narrow input whose
+    pass 0 is an identity pass."""
+    torch = cuda
+    L = bsg._lib.lib()
+    prev_small = L.bsg_debug_set_small_sort(0)
+    prev = L.bsg_debug_set_first_pass(first)
+    try:
+        for n in (1, 5, 8191, 8193, 12289, 100003, (1 << 21) + 1, (1 << 25) + 12345):
+            keys = orc.generate_uniform_keys(n, 77 * n + first)
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+        n = 3 * 12288 + 1001
+        base = orc.generate_uniform_keys(n, 4242)
+        inputs = [
+            (base & 0xFFFFFF01).astype(np.uint32),             # two values of digit 0
+            ((base >> 8) << 8 | (base % 3 == 0)).astype(np.uint32),  # digit 0 mostly 0
+            (base & 0xFFFFFF00).astype(np.uint32),             # pass 0 is an identity pass
+            np.minimum(np.random.default_rng(9).zipf(1.1, n), 0xFFFFFFFF).astype(np.uint32),  # Zipf ranks
+        ]
+        for keys in inputs:
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 65536), np.sort(keys))
+        ctx = bsg._lib.context(0)
+        st = torch.cuda.current_stream().cuda_stream
+        for offset in (1, 2, 3):
+            keys = orc.generate_uniform_keys(n + offset, 500 + offset)
+            t = torch.from_numpy(keys.view(np.int32)).cuda()
+            out = torch.empty(n + offset, dtype=torch.int32, device="cuda")[offset:]
+            assert L.bsg_radix_sort_u32(ctx.handle, t[offset:].data_ptr(), out.data_ptr(), n, 8, 1, st) == 0
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys[offset:]))
+    finally:
+        L.bsg_debug_set_first_pass(prev)
+        L.bsg_debug_set_small_sort(prev_small)
