@@ -63,6 +63,14 @@ def _first_pass_roofline(f_ms, f_cnt, alg_bytes, peak):
             "frac": ach / peak, "launches_per_sort": f_cnt / 3}
 
 
+def _variant_roofline(ms, cnt, alg_bytes, peak):
+    if not cnt:
+        return None
+    per = ms / cnt
+    ach = alg_bytes / (per / 1e3) / 1e9
+    return {"avg_launch_ms": per, "achieved": ach, "frac": ach / peak, "launches_per_sort": cnt / 3}
+
+
 def _traffic(kernel: str, n: int):
     """dram__bytes_read+write per launch from the committed ncu capture."""
     try:
@@ -300,7 +308,13 @@ def run_single(args):
     os_ms, os_cnt = ctx.kernel_time(_lib.K_ONESWEEP)
     h_ms, h_cnt = ctx.kernel_time(_lib.K_HIST)
     f_ms, f_cnt = ctx.kernel_time(_lib.K_FIRST_PASS)
+    r_ms, r_cnt = ctx.kernel_time(_lib.K_RELAXED_PASS)
     ctx.set_timing(False)
+    # onesweep_kernel runs passes 1-3: strictly stable (K3) or, where the runs
+    # of equal low bits are long, value-stable (K3r) -- one kernel template,
+    # averaged over all its launches; both variants reported beside it
+    strict_ms, strict_cnt = os_ms, os_cnt
+    os_ms, os_cnt = os_ms + r_ms, os_cnt + r_cnt
     per_launch_s = os_ms / max(os_cnt, 1) / 1e3
     alg_bytes = 8.0 * n  # one read + one write of every key per pass
     achieved = alg_bytes / per_launch_s / 1e9
@@ -315,7 +329,9 @@ def run_single(args):
         _lib.check(L.bsg_radix_sort_u32(ctx.handle, h_in.data_ptr(), h_out.data_ptr(), n, 8, _lib.MEM_HOST, sh))
 
     e2e_step()
-    ke = max(1, min(args.steps, 5))
+    # steps per lane: the pipeline's fill and drain (one H2D and one D2H
+    # without a copy in the other direction) are inside the timed region
+    ke = max(1, min(args.steps, args.e2e_steps))
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(ke):
@@ -380,12 +396,17 @@ def run_single(args):
                 "serial_value": n / (e2e_serial_ms / 1e3), "serial_ms_per_step": e2e_serial_ms},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "onesweep_kernel (one stable 8-bit pass)",
+                     "traffic": traffic, "kernel": "onesweep_kernel (one stable 8-bit pass; passes 1-3 of the sort)",
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": per_launch_s * 1e3,
                      "peak_source": peak_src, "frac_of_8TBps_nominal": achieved / 8000.0,
                      "traffic_source": tsrc,
+                     "launches_per_sort": os_cnt / 3,
+                     "variants": {
+                         "strictly_stable_K3": _variant_roofline(strict_ms, strict_cnt, alg_bytes, peak),
+                         "value_stable_K3r": _variant_roofline(r_ms, r_cnt, alg_bytes, peak)},
                      "first_pass": _first_pass_roofline(f_ms, f_cnt, alg_bytes, peak)},
-        "kernels_ms_per_sort": {"onesweep": os_ms / 3, "first_pass": f_ms / 3, "hist": h_ms / 3},
+        "kernels_ms_per_sort": {"onesweep": os_ms / 3, "onesweep_strict": strict_ms / 3,
+                                "onesweep_value_stable": r_ms / 3, "first_pass": f_ms / 3, "hist": h_ms / 3},
         "clocks": clk.summary(),
         "verified": ok and ok_e2e,
     }
@@ -652,6 +673,8 @@ def main():
                     help="skip the C1/C3/C4/PR rows measured after the config-2 line")
     ap.add_argument("--e2e-inflight", type=int, default=4,
                     help="sorts in flight in the e2e measurement (host threads, one context/stream each)")
+    ap.add_argument("--e2e-steps", type=int, default=20,
+                    help="e2e steps per lane (capped by --steps); total e2e steps = lanes x this")
     ap.add_argument("--pr-variant", choices=["A", "B", "P"], default="P",
                     help="multi-GPU algorithm: A = per-round PR4 (4 NCCL exchanges), B = single exchange, "
                          "P = per-round PR4 with the exchange + rebuild as one peer-store kernel over NVLink")

@@ -96,7 +96,8 @@ enum bsg_kernel_class {
     BSG_K_NETWORK = 2,  /* batched BTN/OET block network (netsort.cu) */
     BSG_K_PR = 3,       /* parallel-radix plan/rebuild kernels (pr.cu) */
     BSG_K_FIRST_PASS = 4, /* first pass of a full sort, no order inside a digit run (radix.cu K3f) */
-    BSG_K_CLASSES = 5
+    BSG_K_RELAXED_PASS = 5, /* pass k > 0 of a full sort, value-stable ranking (radix.cu K3r) */
+    BSG_K_CLASSES = 6
 };
 int bsg_ctx_set_timing(bsg_ctx* ctx, int enable);
 /* Synchronises the recorded events and returns the summed duration (ms) and

@@ -434,7 +434,7 @@ constexpr int default_lb_window() {
 }
 
 template <int BITS, int THREADS, int ITEMS, bool WIDE, int RANK, typename Sink = PlainSink,
-          int LBW = default_lb_window<THREADS>(), bool SEG = false>
+          int LBW = default_lb_window<THREADS>(), bool SEG = false, bool RELAX = false>
 __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const uint32_t* __restrict__ src,
                                                Sink dst, uint64_t chunk_n, int shift,
                                                const uint64_t* __restrict__ digit_base, uint32_t* __restrict__ status,
@@ -767,8 +767,8 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
             auto rank_stage = [&](auto full_tag) {
                 constexpr bool FULL = decltype(full_tag)::value;
                 constexpr int PB = ITEMS % 4 == 0 ? 4 : ITEMS;
-#pragma unroll
-                for (int i0 = 0; i0 < ITEMS; i0 += PB) {
+                // PB items ranked by the ballot multisplit (input order kept)
+                auto ballot_batch = [&](int i0) {
                     uint32_t peers[PB], dgt[PB];
 #pragma unroll
                     for (int ii = 0; ii < PB; ++ii) {
@@ -793,7 +793,53 @@ __device__ __forceinline__ void onesweep_tiles(uint8_t* __restrict__ smem, const
                         __syncwarp();
                         if (ok) buf[r] = keys[i];
                     }
+                };
+                if constexpr (RELAX && FULL && BITS == 8) {
+                    // Value-stable ranking (passes k > 0 of a full keys-only
+                    // sort): the input is ordered by the low `shift` bits, and
+                    // keys equal in those bits AND in the digit may leave the
+                    // pass in any order (later passes and the final array
+                    // cannot tell them apart).  A run of items whose first and
+                    // last key agree in the low bits holds one low-bits value,
+                    // so its keys take their slots by one shared-memory atomic
+                    // each on the warp's offset row -- no ballots.  Items are
+                    // still ranked in item order, warps and tiles by the scan
+                    // and the look-back as in the stable pass.
+                    const uint32_t lowmask = (1u << shift) - 1u;
+                    auto atomic_item = [&](int i) {
+                        const uint32_t key = keys[i];
+                        const uint32_t d = digit_of_key<BITS>(key, shift);
+                        uint32_t boff, inc, sel;
+                        asm("lop3.b32 %0, %1, 0x1FC, %2, 0xEA;" : "=r"(boff) : "r"(d << 1), "r"(wrow_bytes));
+                        asm("mad.lo.u32 %0, %1, %2, 1;" : "=r"(inc) : "r"(d & 1u), "r"(ffff));
+                        const uint32_t old = atomicAdd(reinterpret_cast<uint32_t*>(smem + L::wcnt_off + boff), inc);
+                        asm("mad.lo.u32 %0, %1, 0x22, 0x4410;" : "=r"(sel) : "r"(d & 1u)); // half d & 1 of the word
+                        buf[__byte_perm(old, 0u, sel)] = key;
+                    };
+                    const uint32_t kf = __shfl_sync(0xffffffffu, keys[0], 0);
+                    const uint32_t kl = __shfl_sync(0xffffffffu, keys[ITEMS - 1], 31);
+                    if (((kf ^ kl) & lowmask) == 0u) {
+                        // the warp's whole chunk holds one low-bits value
+#pragma unroll
+                        for (int i = 0; i < ITEMS; ++i) atomic_item(i);
+                        return;
+                    }
+#pragma unroll
+                    for (int i0 = 0; i0 < ITEMS; i0 += PB) {
+                        const uint32_t a = __shfl_sync(0xffffffffu, keys[i0], 0);
+                        const uint32_t b = __shfl_sync(0xffffffffu, keys[i0 + PB - 1], 31);
+                        if (((a ^ b) & lowmask) == 0u) {
+#pragma unroll
+                            for (int ii = 0; ii < PB; ++ii) atomic_item(i0 + ii);
+                            __syncwarp(); // the next batch ranks after these slots are taken
+                        } else {
+                            ballot_batch(i0);
+                        }
+                    }
+                    return;
                 }
+#pragma unroll
+                for (int i0 = 0; i0 < ITEMS; i0 += PB) ballot_batch(i0);
             };
             if (full) rank_stage(std::true_type{});
             else rank_stage(std::false_type{});
@@ -1211,7 +1257,9 @@ __global__ void __launch_bounds__(THREADS, (onesweep_min_blocks<THREADS, ITEMS>(
     extern __shared__ __align__(128) uint8_t smem[];
     if (!plan->active[pass]) return;
     uint32_t parity = 0;
-    if constexpr (RANK == 3) {
+    // RANK 4 = count-then-rank (3) with value-stable ranking (see rank_stage)
+    constexpr int R = RANK == 4 ? 3 : RANK;
+    if constexpr (R == 3) {
         // skewed digit distribution (a digit holds > n/16 keys): the counting
         // reductions would serialise on that digit's counter; rank first
         // (warp-aggregated by the ballot multisplit) instead.  (Two kernels
@@ -1224,9 +1272,9 @@ __global__ void __launch_bounds__(THREADS, (onesweep_min_blocks<THREADS, ITEMS>(
             return;
         }
     }
-    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, RANK>(smem, plan->src[pass] + chunk_off, PlainSink{plan->dst[pass]}, chunk_n,
-                                                     shift, digit_base, status, tile_counter, use_tma, dbg, neg1,
-                                                     true, parity);
+    onesweep_tiles<BITS, THREADS, ITEMS, WIDE, R, PlainSink, default_lb_window<THREADS>(), false, RANK == 4>(
+        smem, plan->src[pass] + chunk_off, PlainSink{plan->dst[pass]}, chunk_n, shift, digit_base, status,
+        tile_counter, use_tma, dbg, neg1, true, parity);
 }
 
 constexpr int kMinTile = 4096;
@@ -1252,6 +1300,19 @@ inline int& first_pass_ref() {
 }
 inline bool first_pass_enabled() { return first_pass_ref() != 0; }
 
+// Value-stable ranking in passes k > 0 of full sorts (bsg_debug_set_relaxed_passes
+// toggles it: tests compare both paths).  A pass qualifies when the runs of equal
+// low bits it meets are long for uniformly distributed low bits: n >> shift keys
+// per run, at least kRelaxMinRun (a warp item is 32 keys).
+inline int& relaxed_passes_ref() {
+    static int on = dev_knob("BSG_RELAXED", 1);
+    return on;
+}
+constexpr uint64_t kRelaxMinRun = 512;
+inline bool relaxed_pass(uint64_t n, int shift) {
+    return relaxed_passes_ref() != 0 && shift > 0 && shift < 32 && (n >> shift) >= kRelaxMinRun;
+}
+
 inline int onesweep_rank_mode() {
     static int r = dev_knob("BSG_OS_RANK", 0);
     return r;
@@ -1272,15 +1333,15 @@ int launch_onesweep_cfg_r(const PassPlan* plan, int pass, uint64_t n, int shift,
     const uint64_t stat_words = static_cast<uint64_t>(tiles) * RADIX * (WIDE ? 2 : 1);
     (void)passes_stride; // digit bases: chunk row 0 of [chunk][pass][radix] = global starts
     if (cudaMemsetAsync(status, 0, (32 + stat_words) * sizeof(uint32_t), stream) != cudaSuccess) return -1;
-    TimedScope ts(0 /*BSG_K_ONESWEEP*/, stream);
+    TimedScope ts(RANK == 4 ? 5 /*BSG_K_RELAXED_PASS*/ : 0 /*BSG_K_ONESWEEP*/, stream);
     kern<<<grid, THREADS, L::bytes, stream>>>(plan, pass, 0, n, shift, base_for_pass, status + 32, status,
                                                use_tma ? 1 : 0, onesweep_dbg(), -1);
     return 1;
 }
 
-template <int BITS, int THREADS, int ITEMS, bool WIDE>
+template <int BITS, int THREADS, int ITEMS, bool WIDE, bool CAN_RELAX = false>
 int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
-                        int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+                        int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma, bool relaxed = false) {
     // RANK 3 = per-warp count by shared-memory reductions, then ballot-multisplit
     // ranks against the final offsets with the scatter (default, BSG_OS_RANK=0);
     // 0 = rank first, stage after the scan (BSG_OS_RANK=2, +3.4% per sort);
@@ -1296,18 +1357,26 @@ int launch_onesweep_cfg(const PassPlan* plan, int pass, uint64_t n, int shift, c
         default:
             break;
         }
+        // RANK 4: value-stable ranking for passes k > 0 of a full sort
+        if constexpr (CAN_RELAX) {
+            if (relaxed)
+                return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 4>(plan, pass, n, shift, base_for_pass,
+                                                                            passes_stride, status, stream, use_tma);
+        }
     }
+    (void)relaxed;
     return launch_onesweep_cfg_r<BITS, THREADS, ITEMS, WIDE, 3>(plan, pass, n, shift, base_for_pass, passes_stride,
                                                                 status, stream, use_tma);
 }
 
 template <int BITS>
 int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, const uint64_t* base_for_pass,
-                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma) {
+                         int passes_stride, uint32_t* status, cudaStream_t stream, bool use_tma,
+                         bool relaxed = false) {
     const bool wide = n > kChunkKeys;
     if (wide) // n > 2^29: 64-bit status words and positions, the large-n rows
-        return launch_onesweep_cfg<BITS, 512, 24, true>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                        stream, use_tma);
+        return launch_onesweep_cfg<BITS, 512, 24, true, BITS == 8>(plan, pass, n, shift, base_for_pass,
+                                                                   passes_stride, status, stream, use_tma, relaxed);
     if constexpr (BITS != 8)
         return launch_onesweep_cfg<BITS, 1024, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
@@ -1322,8 +1391,8 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
         return launch_onesweep_cfg<BITS, 256, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
     case 1:
-        return launch_onesweep_cfg<BITS, 512, 16, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                         stream, use_tma);
+        return launch_onesweep_cfg<BITS, 512, 16, false, BITS == 8>(plan, pass, n, shift, base_for_pass,
+                                                                    passes_stride, status, stream, use_tma, relaxed);
     case 4:
         return launch_onesweep_cfg<BITS, 1024, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                           stream, use_tma);
@@ -1331,8 +1400,8 @@ int launch_onesweep_pass(const PassPlan* plan, int pass, uint64_t n, int shift, 
         return launch_onesweep_cfg<BITS, 1024, 20, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                           stream, use_tma);
     case 6:
-        return launch_onesweep_cfg<BITS, 512, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
-                                                         stream, use_tma);
+        return launch_onesweep_cfg<BITS, 512, 24, false, BITS == 8>(plan, pass, n, shift, base_for_pass,
+                                                                    passes_stride, status, stream, use_tma, relaxed);
     case 7:
         return launch_onesweep_cfg<BITS, 256, 24, false>(plan, pass, n, shift, base_for_pass, passes_stride, status,
                                                          stream, use_tma);
@@ -1847,8 +1916,11 @@ int launch_byte_passes(const uint32_t* in, uint32_t* out, uint64_t n, int first_
             launches += l;
             continue;
         }
+        // passes k > 0 of a full sort read keys ordered by their low 8k bits
+        // and need keep only that order (value-stable ranking)
+        const bool relaxed = passes == 4 && first_byte == 0 && p > 0 && relaxed_pass(n, 8 * p);
         const int l = launch_onesweep_pass<8>(ws.plan, p, n, 8 * (first_byte + p), ws.base + p * RADIX, passes,
-                                              ws.status, stream, tma);
+                                              ws.status, stream, tma, relaxed);
         if (l < 0) return -1;
         launches += l;
     }
@@ -1959,6 +2031,14 @@ extern "C" int bsg_debug_set_onesweep_cfg(int cfg) {
 extern "C" int bsg_debug_set_first_pass(int on) {
     const int prev = bsg::first_pass_ref();
     if (on >= 0) bsg::first_pass_ref() = on;
+    return prev;
+}
+
+// Test aid: enables/disables value-stable ranking in passes k > 0 of full
+// sorts (on < 0: query only); returns the previous setting.
+extern "C" int bsg_debug_set_relaxed_passes(int on) {
+    const int prev = bsg::relaxed_passes_ref();
+    if (on >= 0) bsg::relaxed_passes_ref() = on;
     return prev;
 }
 

@@ -450,3 +450,39 @@ def test_first_pass_both_paths(cuda, bsg, orc, first):
     finally:
         L.bsg_debug_set_first_pass(prev)
         L.bsg_debug_set_small_sort(prev_small)
+
+
+@pytest.mark.parametrize("relaxed", [0, 1])
+def test_relaxed_passes_both_paths(cuda, bsg, orc, relaxed):
+    """Passes k > 0 of a full sort rank value-stably (keys equal in the low 8k
+    bits and in the digit take their slots by shared-memory atomics; runs of
+    items with different low bits fall back to the ballot multisplit) or
+    strictly stably: both must give the oracle's sorted array.  Sizes pick
+    both tile rows and make pass 1 only (2^22: runs of 2^14 keys), passes 1-2
+    (2^26: runs of 2^18 and 2^10 keys, so most warps of pass 2 meet a run
+    boundary) qualify; inputs with few or skewed low-bits values, long runs
+    of fully equal keys and run boundaries inside warp items."""
+    L = bsg._lib.lib()
+    prev_small = L.bsg_debug_set_small_sort(0)
+    prev = L.bsg_debug_set_relaxed_passes(relaxed)
+    try:
+        for n in ((1 << 17) + 3, (1 << 22) + 1, (1 << 25) + 12345, (1 << 26) + 77):
+            keys = orc.generate_uniform_keys(n, 31 * n + relaxed)
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+        n = (1 << 23) + 4099
+        base = orc.generate_uniform_keys(n, 990)
+        rng = np.random.default_rng(5)
+        inputs = [
+            (base & 0xFFFF0003).astype(np.uint32),                  # 4 low-byte values, byte 1 constant
+            (base & 0xFF00FFFF).astype(np.uint32),                  # byte 2 constant (identity pass in between)
+            ((base & 0xFFFFFF00) | (base % 7 == 0)).astype(np.uint32),  # low byte 0 for 6/7 of the keys
+            rng.choice(base[:1000], n).astype(np.uint32),           # 1000 distinct keys, long equal runs
+            ((base & 0xFFFF0000) | (np.arange(n) % 37)).astype(np.uint32),  # low-bits runs of n/37 keys
+            np.minimum(rng.zipf(1.1, n), 0xFFFFFFFF).astype(np.uint32),
+        ]
+        for keys in inputs:
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+            np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 65536), np.sort(keys))
+    finally:
+        L.bsg_debug_set_relaxed_passes(prev)
+        L.bsg_debug_set_small_sort(prev_small)
