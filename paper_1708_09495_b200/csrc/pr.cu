@@ -781,7 +781,7 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
         // every worker's local stable pass, stored at the global positions
         // (sort_and_scatter + exchange + gather_slices), one segmented launch
         if (!add(launch_onesweep_seg(src, dst, n, p, bits, shift, reinterpret_cast<const uint64_t*>(base),
-                                     ctx->status.as<uint32_t>(), stream, skew)))
+                                     ctx->status.as<uint32_t>(), stream, skew, rounds * bits == 32)))
             return cuda_fail(cudaGetLastError(), "pr fused pass");
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
         if (stats) {

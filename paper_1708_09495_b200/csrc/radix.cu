@@ -1715,7 +1715,10 @@ int launch_onesweep_peer(const uint32_t* block, uint64_t len, int bits, int shif
 // ---------------------------------------------------------------------------
 // WIDE: 64-bit status words and positions (segments above 2^29 keys or
 // arrays above 2^32 keys, e.g. BASELINE config 5's n = 2^33 with p <= 8).
-template <int BITS, int THREADS, int ITEMS, bool WIDE>
+// RELAX: value-stable ranking (rank_stage) -- the rounds of a full in-process
+// PR run, whose worker blocks are ordered by the low `shift` bits (round 0:
+// shift = 0, every key qualifies).
+template <int BITS, int THREADS, int ITEMS, bool WIDE, bool RELAX>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     onesweep_seg_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, const SegDesc sd, int shift,
                         const uint64_t* __restrict__ base_table, uint32_t* __restrict__ status,
@@ -1724,20 +1727,20 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 512 ? 2 : 1))
     uint32_t parity = 0;
     // count then rank unless the caller flags a heavy digit (or gives no flag)
     if (BITS == 8 && skew && !*skew)
-        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PlainSink, default_lb_window<THREADS>(), true>(
+        onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 3, PlainSink, default_lb_window<THREADS>(), true, RELAX>(
             smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
     else
         onesweep_tiles<BITS, THREADS, ITEMS, WIDE, 0, PlainSink, default_lb_window<THREADS>(), true>(
             smem, src, PlainSink{dst}, 0, shift, base_table, status, tile_counter, 1, 0, neg1, true, parity, sd);
 }
 
-template <int BITS, int THREADS, int ITEMS, bool WIDE = false>
+template <int BITS, int THREADS, int ITEMS, bool WIDE = false, bool RELAX = false>
 int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int shift,
                             const uint64_t* base_table, uint32_t* status, cudaStream_t stream,
                             const uint32_t* skew) {
     using L = OnesweepSmem<BITS, THREADS, ITEMS, WIDE>;
     constexpr int RADIX = 1 << BITS;
-    auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS, WIDE>;
+    auto kern = onesweep_seg_kernel<BITS, THREADS, ITEMS, WIDE, RELAX>;
     static PerDeviceOccupancy occ;
     const int per_sm = std::max(1, kernel_occupancy(occ, kern, THREADS, L::bytes));
     const int sms = current_sm_count();
@@ -1760,12 +1763,25 @@ int launch_onesweep_seg_cfg(const uint32_t* src, uint32_t* dst, uint64_t n, int 
 }
 
 int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
-                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream, const uint32_t* skew) {
+                        const uint64_t* base_table, uint32_t* status, cudaStream_t stream, const uint32_t* skew,
+                        bool full_run) {
     if (n == 0) return 0;
+    // rounds of a full run may rank value-stably (round 0: nothing below the digit)
+    const bool relaxed = full_run && bits == 8 && relaxed_passes_ref() != 0 && (shift == 0 || relaxed_pass(n, shift));
     if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys || n > 0xFFFFFFFFull) {
         // 64-bit status words and positions
         if (bits != 8) return -1;
+        if (relaxed)
+            return launch_onesweep_seg_cfg<8, 512, 24, true, true>(src, dst, n, p, shift, base_table, status, stream,
+                                                                   skew);
         return launch_onesweep_seg_cfg<8, 512, 24, true>(src, dst, n, p, shift, base_table, status, stream, skew);
+    }
+    if (relaxed) {
+        if (n > (uint64_t{1} << 23))
+            return launch_onesweep_seg_cfg<8, 512, 24, false, true>(src, dst, n, p, shift, base_table, status, stream,
+                                                                    skew);
+        return launch_onesweep_seg_cfg<8, 512, 16, false, true>(src, dst, n, p, shift, base_table, status, stream,
+                                                                skew);
     }
     switch (bits) {
     case 1: return launch_onesweep_seg_cfg<1, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);

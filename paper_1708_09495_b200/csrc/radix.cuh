@@ -76,9 +76,11 @@ struct PeerTable {
 // launches (0 or 1) or -1.
 // skew: device flag (0 = no digit holds > 1/16 of a block: count-then-rank
 // path); nullptr = always rank first.
+// full_run: the pass is round shift / bits of a full PR run from round 0 whose
+// intermediate states are not returned (value-stable ranking allowed).
 int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, int bits, int shift,
                         const uint64_t* base_table, uint32_t* status, cudaStream_t stream,
-                        const uint32_t* skew = nullptr);
+                        const uint32_t* skew = nullptr, bool full_run = false);
 uint64_t onesweep_seg_status_words(uint64_t n, int p);
 
 // launch_onesweep_seg whose write-out stores key position g into

@@ -454,3 +454,39 @@ def test_protocol_errors_raise_bsp_error(cuda, bsg):
         D._check_exchange([1, 2], [3, 4], 4, 7, 0, 0)
     with pytest.raises(bsg._lib.BspError):
         D._check_exchange([1, 2], [3, 3], 3, 7, 0, 0)
+
+
+@pytest.mark.parametrize("relaxed", [0, 1])
+def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
+    """The rounds of a FULL in-process PR4 run (no rounds limit: intermediate
+    states are not returned) may rank value-stably; a rounds-limited run always
+    ranks strictly.  Both settings must give the oracle's output and RunStats,
+    for both tile rows (n <= 2^23: 8192-key tiles, above: 12288), ragged
+    blocks, duplicate-heavy and skewed keys; rounds-limited states stay
+    bit-exact whatever the setting."""
+    L = bsg._lib.lib()
+    prev = L.bsg_debug_set_relaxed_passes(relaxed)
+    try:
+        for n, ps in (((1 << 17) + 5, (1, 3, 8)), ((1 << 22) + 5, (3, 8)), ((1 << 24) + 3, (2, 5))):
+            keys = orc.generate_uniform_keys(n, 17 * n + relaxed)
+            exp = np.sort(keys)
+            for p in ps:
+                res = pr(bsg, keys, p, 256)
+                np.testing.assert_array_equal(res.output, exp)
+                if n <= (1 << 22) + 5:
+                    _, est = orc.parallel_radix(keys, p, 256)
+                    assert res.stats == est
+        n = (1 << 21) + 77
+        base = orc.generate_uniform_keys(n, 71)
+        rng = np.random.default_rng(3)
+        for keys in ((base & 0xFFFF0007).astype(np.uint32), rng.choice(base[:500], n).astype(np.uint32),
+                     np.minimum(rng.zipf(1.1, n), 0xFFFFFFFF).astype(np.uint32)):
+            for p in (2, 7):
+                np.testing.assert_array_equal(pr(bsg, keys, p, 256).output, np.sort(keys))
+        keys = orc.generate_uniform_keys((1 << 20) + 9, 5)
+        state = keys
+        for r in range(1, 4):
+            state = orc.count_sort_round(state, r - 1, 256)
+            np.testing.assert_array_equal(pr(bsg, keys, 4, 256, rounds=r).output, state)
+    finally:
+        L.bsg_debug_set_relaxed_passes(prev)
