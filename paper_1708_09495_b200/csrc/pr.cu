@@ -840,10 +840,14 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             pr_local_base_kernel<<<p, 256, 0, stream>>>(cA, n, p, bA, skew);
             pr_local_base_kernel<<<p, 256, 0, stream>>>(cB, n, p, bB, skew + 1);
             launches += 2;
+            // full runs: both sub-passes may rank value-stably (a block enters
+            // the round ordered by its low `shift` bits, the second sub-pass by
+            // its low shift + 8 bits)
+            const bool full_run = rounds * bits == 32;
             if (!add(launch_onesweep_seg(src, mid, n, p, 8, shift, reinterpret_cast<const uint64_t*>(bA),
-                                         ctx->status.as<uint32_t>(), stream, skew)) ||
+                                         ctx->status.as<uint32_t>(), stream, skew, full_run)) ||
                 !add(launch_onesweep_seg(mid, S, n, p, 8, shift + 8, reinterpret_cast<const uint64_t*>(bB),
-                                         ctx->status.as<uint32_t>(), stream, skew + 1)))
+                                         ctx->status.as<uint32_t>(), stream, skew + 1, full_run)))
                 return cuda_fail(cudaGetLastError(), "pr local pass");
         }
         {

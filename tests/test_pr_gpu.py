@@ -458,7 +458,7 @@ def test_protocol_errors_raise_bsp_error(cuda, bsg):
 
 @pytest.mark.parametrize("relaxed", [0, 1])
 def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
-    """The rounds of a FULL in-process PR4 run (no rounds limit: intermediate
+    """The rounds of a FULL in-process PR4/PR2 run (no rounds limit: intermediate
     states are not returned) may rank value-stably; a rounds-limited run always
     ranks strictly.  Both settings must give the oracle's output and RunStats,
     for both tile rows (n <= 2^23: 8192-key tiles, above: 12288), ragged
@@ -471,11 +471,12 @@ def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
             keys = orc.generate_uniform_keys(n, 17 * n + relaxed)
             exp = np.sort(keys)
             for p in ps:
-                res = pr(bsg, keys, p, 256)
-                np.testing.assert_array_equal(res.output, exp)
-                if n <= (1 << 22) + 5:
-                    _, est = orc.parallel_radix(keys, p, 256)
-                    assert res.stats == est
+                for radix in (256, 65536):
+                    res = pr(bsg, keys, p, radix)
+                    np.testing.assert_array_equal(res.output, exp)
+                    if n <= (1 << 22) + 5:
+                        _, est = orc.parallel_radix(keys, p, radix)
+                        assert res.stats == est
         n = (1 << 21) + 77
         base = orc.generate_uniform_keys(n, 71)
         rng = np.random.default_rng(3)
@@ -483,10 +484,12 @@ def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
                      np.minimum(rng.zipf(1.1, n), 0xFFFFFFFF).astype(np.uint32)):
             for p in (2, 7):
                 np.testing.assert_array_equal(pr(bsg, keys, p, 256).output, np.sort(keys))
+                np.testing.assert_array_equal(pr(bsg, keys, p, 65536).output, np.sort(keys))
         keys = orc.generate_uniform_keys((1 << 20) + 9, 5)
         state = keys
         for r in range(1, 4):
             state = orc.count_sort_round(state, r - 1, 256)
             np.testing.assert_array_equal(pr(bsg, keys, 4, 256, rounds=r).output, state)
+        np.testing.assert_array_equal(pr(bsg, keys, 3, 65536, rounds=1).output, orc.count_sort_round(keys, 0, 65536))
     finally:
         L.bsg_debug_set_relaxed_passes(prev)
