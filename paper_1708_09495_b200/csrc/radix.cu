@@ -1309,8 +1309,13 @@ inline int& relaxed_passes_ref() {
     return on;
 }
 constexpr uint64_t kRelaxMinRun = 512;
+// below 2^24 keys the sort is latency-bound and the ranking is not what it
+// waits for (measured 2^22-2^23: +0.4 / +1.9% with the relaxation, 2^24: -0.5%,
+// 2^25-2^28: -3.2 .. -4.5%)
+constexpr uint64_t kRelaxMinKeys = uint64_t{1} << 24;
 inline bool relaxed_pass(uint64_t n, int shift) {
-    return relaxed_passes_ref() != 0 && shift > 0 && shift < 32 && (n >> shift) >= kRelaxMinRun;
+    return relaxed_passes_ref() != 0 && n >= kRelaxMinKeys && shift > 0 && shift < 32 &&
+           (n >> shift) >= kRelaxMinRun;
 }
 
 inline int onesweep_rank_mode() {
@@ -1767,7 +1772,8 @@ int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, i
                         bool full_run) {
     if (n == 0) return 0;
     // rounds of a full run may rank value-stably (round 0: nothing below the digit)
-    const bool relaxed = full_run && bits == 8 && relaxed_passes_ref() != 0 && (shift == 0 || relaxed_pass(n, shift));
+    const bool relaxed = full_run && bits == 8 && relaxed_passes_ref() != 0 && n >= kRelaxMinKeys &&
+                         (shift == 0 || relaxed_pass(n, shift));
     if (n / static_cast<uint64_t>(p) + 1 > kChunkKeys || n > 0xFFFFFFFFull) {
         // 64-bit status words and positions
         if (bits != 8) return -1;
@@ -1776,13 +1782,9 @@ int launch_onesweep_seg(const uint32_t* src, uint32_t* dst, uint64_t n, int p, i
                                                                    skew);
         return launch_onesweep_seg_cfg<8, 512, 24, true>(src, dst, n, p, shift, base_table, status, stream, skew);
     }
-    if (relaxed) {
-        if (n > (uint64_t{1} << 23))
-            return launch_onesweep_seg_cfg<8, 512, 24, false, true>(src, dst, n, p, shift, base_table, status, stream,
-                                                                    skew);
-        return launch_onesweep_seg_cfg<8, 512, 16, false, true>(src, dst, n, p, shift, base_table, status, stream,
+    if (relaxed) // n >= 2^24: the 12288-key tile row
+        return launch_onesweep_seg_cfg<8, 512, 24, false, true>(src, dst, n, p, shift, base_table, status, stream,
                                                                 skew);
-    }
     switch (bits) {
     case 1: return launch_onesweep_seg_cfg<1, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);
     case 2: return launch_onesweep_seg_cfg<2, 512, 16>(src, dst, n, p, shift, base_table, status, stream, skew);

@@ -461,9 +461,9 @@ def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
     """The rounds of a FULL in-process PR4/PR2 run (no rounds limit: intermediate
     states are not returned) may rank value-stably; a rounds-limited run always
     ranks strictly.  Both settings must give the oracle's output and RunStats,
-    for both tile rows (n <= 2^23: 8192-key tiles, above: 12288), ragged
-    blocks, duplicate-heavy and skewed keys; rounds-limited states stay
-    bit-exact whatever the setting."""
+    below and above the 2^24 keys the relaxation starts at, ragged blocks,
+    duplicate-heavy and skewed keys; rounds-limited states stay bit-exact
+    whatever the setting."""
     L = bsg._lib.lib()
     prev = L.bsg_debug_set_relaxed_passes(relaxed)
     try:
@@ -477,7 +477,7 @@ def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
                     if n <= (1 << 22) + 5:
                         _, est = orc.parallel_radix(keys, p, radix)
                         assert res.stats == est
-        n = (1 << 21) + 77
+        n = (1 << 24) + 77
         base = orc.generate_uniform_keys(n, 71)
         rng = np.random.default_rng(3)
         for keys in ((base & 0xFFFF0007).astype(np.uint32), rng.choice(base[:500], n).astype(np.uint32),

@@ -457,11 +457,12 @@ def test_relaxed_passes_both_paths(cuda, bsg, orc, relaxed):
     """Passes k > 0 of a full sort rank value-stably (keys equal in the low 8k
     bits and in the digit take their slots by shared-memory atomics; runs of
     items with different low bits fall back to the ballot multisplit) or
-    strictly stably: both must give the oracle's sorted array.  Sizes pick
-    both tile rows and make pass 1 only (2^22: runs of 2^14 keys), passes 1-2
-    (2^26: runs of 2^18 and 2^10 keys, so most warps of pass 2 meet a run
-    boundary) qualify; inputs with few or skewed low-bits values, long runs
-    of fully equal keys and run boundaries inside warp items."""
+    strictly stably: both must give the oracle's sorted array.  The relaxation
+    applies from 2^24 keys: sizes below it (strict either way), both tile rows
+    above it (2^25: 8192-key tiles, pass 1 only; 2^26: 12288-key tiles, passes
+    1-2 with runs of 2^18 and 2^10 keys, so most warps of pass 2 meet a run
+    boundary); inputs with few or skewed low-bits values, long runs of fully
+    equal keys and run boundaries inside warp items."""
     L = bsg._lib.lib()
     prev_small = L.bsg_debug_set_small_sort(0)
     prev = L.bsg_debug_set_relaxed_passes(relaxed)
@@ -469,7 +470,7 @@ def test_relaxed_passes_both_paths(cuda, bsg, orc, relaxed):
         for n in ((1 << 17) + 3, (1 << 22) + 1, (1 << 25) + 12345, (1 << 26) + 77):
             keys = orc.generate_uniform_keys(n, 31 * n + relaxed)
             np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
-        n = (1 << 23) + 4099
+        n = (1 << 24) + 4099
         base = orc.generate_uniform_keys(n, 990)
         rng = np.random.default_rng(5)
         inputs = [
