@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
 #include "context.cuh"
 #include "netsort.cuh"
 #include "pr.cuh"
@@ -49,11 +50,20 @@ int bsg_ctx::radix_ws(uint64_t n, RadixWorkspace* ws) {
 
 namespace {
 
+// Serialises the context's calls, selects its device, binds its kernel timer
+// and brackets the call in an NVTX range named after the entry point (a no-op
+// unless a tool such as nsys or ncu --nvtx is attached).
 struct CallGuard {
     std::lock_guard<std::mutex> lock;
     DeviceGuard dev;
-    explicit CallGuard(bsg_ctx* c) : lock(c->mu), dev(c->device) { tl_timer = &c->timer; }
-    ~CallGuard() { tl_timer = nullptr; }
+    CallGuard(bsg_ctx* c, const char* entry) : lock(c->mu), dev(c->device) {
+        tl_timer = &c->timer;
+        nvtxRangePushA(entry);
+    }
+    ~CallGuard() {
+        nvtxRangePop();
+        tl_timer = nullptr;
+    }
 };
 
 int check_ctx(bsg_ctx* ctx) {
@@ -181,7 +191,7 @@ int bsg_ctx_release(bsg_ctx* ctx) {
     if (int rc = check_ctx(ctx)) return rc;
     for (bsg_ctx* m : ctx->members)
         if (int rc = bsg_ctx_release(m)) return rc;
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     if (ctx->used && ctx->last_use) {
         const cudaError_t e = cudaEventSynchronize(ctx->last_use);
         if (e != cudaSuccess) return cuda_fail(e, "ctx release");
@@ -209,7 +219,7 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
         ctx->member_streams.clear();
     }
     {
-        CallGuard g(ctx);
+        CallGuard g(ctx, __func__);
         for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
                           &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
                           &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws})
@@ -281,7 +291,7 @@ int bsg_ctx_group_device(const bsg_ctx* ctx, int member) {
 
 int bsg_ctx_set_timing(bsg_ctx* ctx, int enable) {
     if (int rc = check_ctx(ctx)) return rc;
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     ctx->timer.reset();
     ctx->timer.enabled = enable != 0;
     return BSG_OK;
@@ -290,7 +300,7 @@ int bsg_ctx_set_timing(bsg_ctx* ctx, int enable) {
 int bsg_ctx_get_timing(bsg_ctx* ctx, int kernel_class, double* total_ms, uint64_t* launches) {
     if (int rc = check_ctx(ctx)) return rc;
     if (kernel_class < 0 || kernel_class >= BSG_K_CLASSES) return fail(BSG_EINVAL, "unknown kernel class");
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     double ms = 0;
     uint64_t cnt = 0;
     for (auto& r : ctx->timer.recs) {
@@ -309,7 +319,7 @@ int bsg_ctx_get_timing(bsg_ctx* ctx, int kernel_class, double* total_ms, uint64_
 
 int bsg_ctx_reserve(bsg_ctx* ctx, uint64_t n) {
     if (int rc = check_ctx(ctx)) return rc;
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     RadixWorkspace ws;
     return ctx->radix_ws(n, &ws);
 }
@@ -319,7 +329,7 @@ int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = radix_bits_or_fail(radix_log2)) return rc;
     if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);
     return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
@@ -345,7 +355,7 @@ int bsg_count_sort_round_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
     if (round < 0 || round >= rounds)
         return fail(BSG_EINVAL, "round " + std::to_string(round) + " outside [0, " + std::to_string(rounds) + ")");
     if (n && (!in || !out)) return fail(BSG_EINVAL, "null key pointer");
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);
     return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
@@ -371,7 +381,7 @@ int bsg_merge_split_u32(bsg_ctx* ctx, const uint32_t* a, uint64_t na, const uint
     if (int rc = check_ctx(ctx)) return rc;
     if ((na && (!a || !low)) || (nb && (!b || !high))) return fail(BSG_EINVAL, "null key pointer");
     if (na + nb >= (uint64_t{1} << 31)) return fail(BSG_EINVAL, "merge_split: |a|+|b| must be < 2^31");
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);
     if (mem_kind == BSG_MEM_DEVICE) {
@@ -441,7 +451,7 @@ int bsg_block_network_batched_u32(bsg_ctx* ctx, int network, const uint32_t* in,
         st.words_delivered = st.words_sent;
         *stats = st;
     }
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);
     const uint64_t n_in = num_arrays * len, n_out = num_arrays * out_per;
@@ -512,7 +522,7 @@ int bsg_parallel_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out,
     const int rounds = (rounds_limit >= 0 && rounds_limit < all_rounds) ? rounds_limit : all_rounds;
     if (ctx->members.size() > 1) return parallel_radix_sort_group(ctx, in, out, n, p, radix_log2, rounds, stats, mem_kind,
                                                                   static_cast<cudaStream_t>(stream));
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);
     return with_device_io(ctx, in, out, n, n, mem_kind, st, [&](const uint32_t* d_in, uint32_t* d_out, cudaStream_t s) -> int {
@@ -556,7 +566,7 @@ int bsg_pr_count_digits(bsg_ctx* ctx, const uint32_t* block, uint64_t len, int r
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = radix_bits_or_fail(radix_log2)) return rc;
     if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     StreamOrder order(ctx, static_cast<cudaStream_t>(stream));
     const int l = launch_pr_count(ctx, block, len, round, radix_log2, counts, static_cast<cudaStream_t>(stream));
     if (l < 0) return cuda_fail(cudaGetLastError(), "count_digits launch");
@@ -570,7 +580,7 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
     if (int rc = radix_bits_or_fail(radix_log2)) return rc;
     if (p < 1 || me < 0 || me >= p) return fail(BSG_EINVAL, "pr_plan: worker index out of range");
     (void)round;
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     StreamOrder order(ctx, static_cast<cudaStream_t>(stream));
     // scratch for launch_pr_plan: split[p], coltot[r], dstart[r], colchunk[r/1024], rowchunk[p][r/1024]
     const uint64_t chunks = ((uint64_t{1} << radix_log2) + 1023) / 1024;
@@ -590,7 +600,7 @@ int bsg_pr_plan(bsg_ctx* ctx, const uint64_t* counts, uint64_t n, int p, int me,
 
 int bsg_ctx_enable_peer_access(bsg_ctx* ctx, int* enabled) {
     if (int rc = check_ctx(ctx)) return rc;
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     int count = 0, ok = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -621,7 +631,7 @@ int bsg_pr_rebuild(bsg_ctx* ctx, const uint32_t* recv, uint64_t recv_len, const 
     if (int rc = radix_bits_or_fail(radix_log2)) return rc;
     if (round < 0 || round >= 32 / radix_log2) return fail(BSG_EINVAL, "round out of range");
     if (p < 1 || !recv_counts || (recv_len && (!recv || !block || !rebuild_delta))) return fail(BSG_EINVAL, "null pointer");
-    CallGuard g(ctx);
+    CallGuard g(ctx, __func__);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder order(ctx, st);
     uint32_t* flag = nullptr;

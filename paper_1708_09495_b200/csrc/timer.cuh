@@ -6,6 +6,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 namespace bsg {
 
@@ -50,13 +51,20 @@ struct TimedScope {
     int cls;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
+    static const char* class_name(int c) {
+        static const char* const names[] = {"K3 one-sweep pass", "K1 histogram", "block network", "PR plan/rebuild",
+                                            "K3f first pass", "K3r value-stable pass"};
+        return c >= 0 && c < 6 ? names[c] : "kernel";
+    }
     TimedScope(int cls_, cudaStream_t s_) : t(tl_timer), cls(cls_), s(s_) {
+        nvtxRangePushA(class_name(cls_)); // the launches of one kernel class (host-side range)
         if (t && t->enabled) {
             a = t->get();
             cudaEventRecord(a, s);
         }
     }
     ~TimedScope() {
+        nvtxRangePop();
         if (a) {
             cudaEvent_t b = t->get();
             cudaEventRecord(b, s);
