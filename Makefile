@@ -5,7 +5,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr
 PKG := paper_1708_09495_b200
 SRC := $(PKG)/csrc
-CU := $(SRC)/api.cu $(SRC)/radix.cu $(SRC)/netsort.cu $(SRC)/pr.cu $(SRC)/mtgen.cu $(SRC)/staging.cu
+CU := $(SRC)/api.cu $(SRC)/radix.cu $(SRC)/netsort.cu $(SRC)/pr.cu $(SRC)/mtgen.cu $(SRC)/staging.cu $(SRC)/msd.cu
 CPP := $(SRC)/host_util.cpp
 HDR := $(wildcard $(SRC)/*.cuh) include/bsg.h
 OBJDIR := build/obj

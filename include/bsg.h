@@ -97,7 +97,10 @@ enum bsg_kernel_class {
     BSG_K_PR = 3,       /* parallel-radix plan/rebuild kernels (pr.cu) */
     BSG_K_FIRST_PASS = 4, /* first pass of a full sort, no order inside a digit run (radix.cu K3f) */
     BSG_K_RELAXED_PASS = 5, /* pass k > 0 of a full sort, value-stable ranking (radix.cu K3r) */
-    BSG_K_CLASSES = 6
+    BSG_K_MSD_HIST = 6,      /* hybrid route: 16-bit histogram + plan (msd.cu H1/H2) */
+    BSG_K_MSD_PARTITION = 7, /* hybrid route: the two unordered byte partitions (msd.cu MA/MB) */
+    BSG_K_MSD_LOCAL = 8,     /* hybrid route: local sort of the top-16-bit buckets (msd.cu MC) */
+    BSG_K_CLASSES = 9
 };
 int bsg_ctx_set_timing(bsg_ctx* ctx, int enable);
 /* Synchronises the recorded events and returns the summed duration (ms) and

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("BSG_LIB", os.path.join(_HERE, "libbsg.so"))
 BSG_OK, BSG_EINVAL, BSG_EPROTO, BSG_ECUDA, BSG_ENOMEM, BSG_ENCCL = range(6)
 MEM_HOST, MEM_DEVICE = 0, 1
 NET_BTN, NET_OET = 0, 1
-K_ONESWEEP, K_HIST, K_NETWORK, K_PR, K_FIRST_PASS, K_RELAXED_PASS = range(6)
+K_ONESWEEP, K_HIST, K_NETWORK, K_PR, K_FIRST_PASS, K_RELAXED_PASS, K_MSD_HIST, K_MSD_PARTITION, K_MSD_LOCAL = range(9)
 
 
 class LibraryNotBuilt(RuntimeError):

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
+#include "msd.cuh"
 #include "context.cuh"
 #include "netsort.cuh"
 #include "pr.cuh"
@@ -198,7 +199,7 @@ int bsg_ctx_release(bsg_ctx* ctx) {
     }
     for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
                       &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
-                      &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws, &ctx->grp_cur,
+                      &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws, &ctx->msd_ws, &ctx->grp_cur,
                       &ctx->grp_nxt, &ctx->grp_recv})
         b->release();
     return BSG_OK;
@@ -222,7 +223,7 @@ int bsg_ctx_destroy(bsg_ctx* ctx) {
         CallGuard g(ctx, __func__);
         for (DevBuf* b : {&ctx->tmp, &ctx->status, &ctx->hist, &ctx->base, &ctx->plan, &ctx->stage_in, &ctx->stage_out,
                           &ctx->stage_b, &ctx->pr_counts, &ctx->pr_sorted, &ctx->pr_recv, &ctx->pr_block, &ctx->pr_misc,
-                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws})
+                          &ctx->pr_delta, &ctx->net_sched, &ctx->cnt32, &ctx->proto, &ctx->mt_ws, &ctx->msd_ws})
             b->release();
         if (ctx->last_use) cudaEventDestroy(ctx->last_use);
         release_stage(ctx);
@@ -340,7 +341,18 @@ int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t
         // lg r <= 8.  r = 2^16 runs each 16-bit round as two stable 8-bit
         // sub-passes (low byte then high byte of the digit), which is
         // bit-identical to count_sort_round(., round, 65536).
-        const int l = launch_radix_sort8(d_in, d_out, n, ws, s, true);
+        // Large inputs first try the hybrid route (msd.cu); the LSD sort
+        // below then runs only if that route's device-side plan declined or
+        // its local sort gave up (gate word), re-sorting the untouched input.
+        const uint32_t* gate = nullptr;
+        if (msd_sort_applies(d_in, d_out, n)) {
+            cudaError_t e = ctx->msd_ws.ensure(msd_workspace_bytes());
+            if (e != cudaSuccess) return cuda_fail(e, "workspace msd");
+            const int lm = launch_msd_sort(d_in, d_out, ws.tmp, n, ctx->msd_ws.ptr, s, &gate);
+            if (lm < 0) return cuda_fail(cudaGetLastError(), "hybrid sort launch");
+            ctx->launches += static_cast<uint64_t>(lm);
+        }
+        const int l = launch_radix_sort8(d_in, d_out, n, ws, s, true, gate);
         if (l < 0) return cuda_fail(cudaGetLastError(), "radix sort launch");
         ctx->launches += static_cast<uint64_t>(l);
         return BSG_OK;

@@ -57,6 +57,7 @@ struct bsg_ctx {
     bsg::DevBuf net_sched, cnt32;
     bsg::DevBuf proto; // protocol-check flag word (bsp_error equivalent, pr.cu)
     bsg::DevBuf mt_ws; // device generator: segment start windows + jump polynomials
+    bsg::DevBuf msd_ws; // hybrid route: plan, 16-bit histogram, reservations (msd.cu)
     // Cross-stream ordering of the shared workspace: every call records
     // `last_use` on its stream; a call on a different stream first waits on
     // it, so device-mode calls issued on two streams never run on the same

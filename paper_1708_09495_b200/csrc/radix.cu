@@ -102,7 +102,9 @@ constexpr int kHist2Threads = 1024;
 
 template <int BITS, int NDIG>
 __global__ void __launch_bounds__(kHist2Threads)
-    hist_kernel(const uint32_t* __restrict__ in, uint64_t n, int first_shift, uint32_t* __restrict__ hist) {
+    hist_kernel(const uint32_t* __restrict__ in, uint64_t n, int first_shift, uint32_t* __restrict__ hist,
+                const uint32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return; // another route already produced the result (msd.cu)
     constexpr int RADIX = 1 << BITS;
     constexpr uint32_t MASK = RADIX - 1;
     constexpr int COUNTERS = NDIG * RADIX;
@@ -172,7 +174,8 @@ __global__ void __launch_bounds__(kHist2Threads)
 }
 
 template <int BITS, int NDIG>
-void launch_hist(const uint32_t* in, uint64_t n, int first_shift, uint32_t* hist, cudaStream_t stream) {
+void launch_hist(const uint32_t* in, uint64_t n, int first_shift, uint32_t* hist, cudaStream_t stream,
+                 const uint32_t* gate = nullptr) {
     constexpr size_t smem = sizeof(uint32_t) * NDIG * (1 << BITS) * 32;
     static PerDeviceOccupancy occ;
     auto kern = hist_kernel<BITS, NDIG>;
@@ -180,7 +183,7 @@ void launch_hist(const uint32_t* in, uint64_t n, int first_shift, uint32_t* hist
     const int sms = current_sm_count();
     const uint64_t want = (n / 4 + kHist2Threads - 1) / kHist2Threads;
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, sms * per_sm)));
-    kern<<<grid, kHist2Threads, smem, stream>>>(in, n, first_shift, hist);
+    kern<<<grid, kHist2Threads, smem, stream>>>(in, n, first_shift, hist, gate);
 }
 
 // ---------------------------------------------------------------------------
@@ -189,12 +192,31 @@ void launch_hist(const uint32_t* in, uint64_t n, int first_shift, uint32_t* hist
 __global__ void __launch_bounds__(kScanThreads)
     scan_plan_kernel(const uint32_t* __restrict__ hist, int chunks, int passes, int radix,
                      uint64_t n, uint64_t* __restrict__ base, PassPlan* __restrict__ plan,
-                     const uint32_t* in, uint32_t* out, uint32_t* tmp, int allow_skip) {
+                     const uint32_t* in, uint32_t* out, uint32_t* tmp, int allow_skip,
+                     const uint32_t* __restrict__ gate = nullptr) {
     __shared__ uint64_t s_warp[kScanThreads / 32];
     __shared__ int s_active[kMaxPasses];
     __shared__ int s_skew[kMaxPasses];
     const int d = threadIdx.x;
     const int lane = d & 31, warp = d >> 5;
+    if (gate && *gate == 0) {
+        // another route already produced the result in `out` (msd.cu): no
+        // pass runs and nothing is copied
+        if (d == 0) {
+            PassPlan pl;
+            for (int p = 0; p < kMaxPasses; ++p) {
+                pl.src[p] = nullptr;
+                pl.dst[p] = nullptr;
+                pl.active[p] = 0;
+                pl.skew[p] = 0;
+            }
+            pl.executed = 0;
+            pl.need_copy = 0;
+            pl.final_buf = out;
+            *plan = pl;
+        }
+        return;
+    }
     for (int p = 0; p < passes; ++p) {
         uint64_t total = 0;
         if (d < radix)
@@ -1886,8 +1908,8 @@ uint64_t onesweep_status_words(uint64_t n) {
 
 
 int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws,
-                       cudaStream_t stream, bool allow_tma) {
-    return launch_byte_passes(in, out, n, 0, 4, ws, stream, allow_tma);
+                       cudaStream_t stream, bool allow_tma, const uint32_t* gate) {
+    return launch_byte_passes(in, out, n, 0, 4, ws, stream, allow_tma, gate);
 }
 
 // `passes` stable 8-bit passes over bytes first_byte .. first_byte+passes-1:
@@ -1897,13 +1919,13 @@ int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const Radi
 // the r = 2^16 sort as 2 rounds x 2 byte sub-passes); passes = 2: one
 // r = 2^16 count-sort round (radix.hpp:44-65 at r = 65536) at 20 B/key.
 int launch_byte_passes(const uint32_t* in, uint32_t* out, uint64_t n, int first_byte, int passes,
-                       const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma) {
+                       const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma, const uint32_t* gate) {
     constexpr int RADIX = 256;
     const uint64_t chunks = n ? (n + kChunkKeys - 1) / kChunkKeys : 1;
     int launches = 0;
     if (passes == 4 && first_byte == 0) {
         const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
-        const int l = launch_small_sort(in, out, n, ws, stream, tma);
+        const int l = gate ? 0 : launch_small_sort(in, out, n, ws, stream, tma);
         if (l != 0) return l;
     }
     if (passes < 1 || passes > 4 || first_byte + passes > 4) return -1;
@@ -1914,15 +1936,15 @@ int launch_byte_passes(const uint32_t* in, uint32_t* out, uint64_t n, int first_
         TimedScope ts(1 /*BSG_K_HIST*/, stream);
         uint32_t* h = ws.hist + c * passes * RADIX;
         switch (passes) {
-        case 1: launch_hist<8, 1>(in + off, len, 8 * first_byte, h, stream); break;
-        case 2: launch_hist<8, 2>(in + off, len, 8 * first_byte, h, stream); break;
-        case 3: launch_hist<8, 3>(in + off, len, 8 * first_byte, h, stream); break;
-        default: launch_hist<8, 4>(in + off, len, 8 * first_byte, h, stream); break;
+        case 1: launch_hist<8, 1>(in + off, len, 8 * first_byte, h, stream, gate); break;
+        case 2: launch_hist<8, 2>(in + off, len, 8 * first_byte, h, stream, gate); break;
+        case 3: launch_hist<8, 3>(in + off, len, 8 * first_byte, h, stream, gate); break;
+        default: launch_hist<8, 4>(in + off, len, 8 * first_byte, h, stream, gate); break;
         }
         ++launches;
     }
     scan_plan_kernel<<<1, kScanThreads, 0, stream>>>(ws.hist, static_cast<int>(chunks), passes, RADIX, n, ws.base,
-                                                     ws.plan, in, out, ws.tmp, 1);
+                                                     ws.plan, in, out, ws.tmp, 1, gate);
     ++launches;
     const bool tma = allow_tma; // tiles TMA their 16-byte-aligned bodies at any alignment
     // a full sort's first pass needs no order inside a digit run (K3f)

@@ -40,14 +40,16 @@ uint64_t onesweep_status_words(uint64_t n);
 
 // Full LSD sort of n keys with 8-bit passes over bits [0, 8*passes).
 // Returns the number of kernel launches enqueued, or -1 on launch error.
+// gate: optional device word; when it reads 0 at run time the whole sort is
+// skipped on the device (another route already wrote `out`, msd.cu).
 int launch_radix_sort8(const uint32_t* in, uint32_t* out, uint64_t n, const RadixWorkspace& ws,
-                       cudaStream_t stream, bool allow_tma);
+                       cudaStream_t stream, bool allow_tma, const uint32_t* gate = nullptr);
 
 // `passes` stable byte passes starting at byte `first_byte` with one
 // histogram read and one plan (passes = 2, first_byte = 2*round: one r = 2^16
 // count-sort round).  Returns launches or -1.
 int launch_byte_passes(const uint32_t* in, uint32_t* out, uint64_t n, int first_byte, int passes,
-                       const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma);
+                       const RadixWorkspace& ws, cudaStream_t stream, bool allow_tma, const uint32_t* gate = nullptr);
 
 // One stable count-sort pass over the `bits`-wide digit at bit `shift`
 // (bits in {1,2,4,8}).  Returns launches enqueued or -1.

@@ -53,8 +53,9 @@ struct TimedScope {
     cudaEvent_t a = nullptr;
     static const char* class_name(int c) {
         static const char* const names[] = {"K3 one-sweep pass", "K1 histogram", "block network", "PR plan/rebuild",
-                                            "K3f first pass", "K3r value-stable pass"};
-        return c >= 0 && c < 6 ? names[c] : "kernel";
+                                            "K3f first pass", "K3r value-stable pass", "hybrid: histogram + plan",
+                                            "hybrid: byte partitions", "hybrid: local sort"};
+        return c >= 0 && c < 9 ? names[c] : "kernel";
     }
     TimedScope(int cls_, cudaStream_t s_) : t(tl_timer), cls(cls_), s(s_) {
         nvtxRangePushA(class_name(cls_)); // the launches of one kernel class (host-side range)

@@ -8,7 +8,7 @@ out=build/var/$name; mkdir -p $out
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr -DBSG_DEV_KNOBS=1 $*"
 S=${SRCDIR:-paper_1708_09495_b200/csrc}
 objs=""
-for f in api radix netsort pr mtgen staging; do
+for f in api radix netsort pr mtgen staging msd; do
   $NV -c $S/$f.cu -o $out/$f.o & objs="$objs $out/$f.o"
 done
 $NV -x cu -c $S/host_util.cpp -o $out/host_util.o & objs="$objs $out/host_util.o"

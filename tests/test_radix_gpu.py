@@ -487,3 +487,106 @@ def test_relaxed_passes_both_paths(cuda, bsg, orc, relaxed):
     finally:
         L.bsg_debug_set_relaxed_passes(prev)
         L.bsg_debug_set_small_sort(prev_small)
+
+
+def test_hybrid_route_and_its_fallbacks(cuda, bsg, orc):
+    """Full sorts of large evenly spread inputs may take the hybrid route
+    (msd.cu: two unordered byte partitions of the top 16 bits, then a local
+    sort of every top-16-bit bucket); whatever it cannot take falls back to
+    the LSD sort on the device.  Forced on for every size here: uniform keys
+    (the route itself, ragged sizes, misaligned pointers), a bucket above the
+    local sort's capacity (the plan declines), more than 15 equal keys in one
+    bucket (the local sort gives up and the LSD sort re-sorts the untouched
+    input), duplicate-heavy and skewed keys, and in-place calls (never routed).
+    Every result must equal the oracle's sorted array."""
+    torch = cuda
+    L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    prev = L.bsg_debug_set_msd(2)
+
+    def dev_sort(keys, offset=0, inplace=False):
+        t = torch.from_numpy(np.concatenate([np.zeros(offset, np.uint32), keys]).view(np.int32)).cuda()
+        src = t[offset:]
+        out = src if inplace else torch.empty(keys.size + offset, dtype=torch.int32, device="cuda")[offset:]
+        assert L.bsg_radix_sort_u32(ctx.handle, src.data_ptr(), out.data_ptr(), keys.size, 8, 1, st) == 0
+        torch.cuda.synchronize()
+        if not inplace:
+            np.testing.assert_array_equal(src.cpu().numpy().view(np.uint32), keys)  # the input is never written
+        return out.cpu().numpy().view(np.uint32)
+
+    try:
+        for n in (1, 2, 5, 8191, 100003, (1 << 20) + 1, (1 << 24) + 7, (1 << 26) + 12345):
+            keys = orc.generate_uniform_keys(n, 11 * n + 3)
+            np.testing.assert_array_equal(dev_sort(keys), np.sort(keys))
+        n = 300007
+        base = orc.generate_uniform_keys(n, 99)
+        rng = np.random.default_rng(12)
+        cases = {
+            "one top-16 value (bucket above capacity)": ((base & 0xFFFF) | 0x12340000).astype(np.uint32),
+            "20 equal keys among uniform ones": np.concatenate([base, np.full(20, base[7], np.uint32)]),
+            "every key 16 times": np.repeat(base[: n // 16], 16),
+            "every key 17 times": np.repeat(base[: n // 17], 17),
+            "1000 distinct keys": rng.choice(base[:1000], n).astype(np.uint32),
+            "zipf": np.minimum(rng.zipf(1.1, n), 0xFFFFFFFF).astype(np.uint32),
+            "all equal": np.full(n, 0xDEADBEEF, np.uint32),
+            "low 16 bits constant": (base & 0xFFFF0000).astype(np.uint32),
+            "sorted": np.sort(base),
+            "reverse sorted": np.sort(base)[::-1].copy(),
+        }
+        for name, keys in cases.items():
+            np.testing.assert_array_equal(dev_sort(keys), np.sort(keys), err_msg=name)
+        keys = orc.generate_uniform_keys((1 << 22) + 5, 8)
+        for offset in (1, 2, 3):
+            np.testing.assert_array_equal(dev_sort(keys, offset=offset), np.sort(keys))
+        np.testing.assert_array_equal(dev_sort(keys, inplace=True), np.sort(keys))
+        # host-memory entry (staged through the context's device buffers)
+        np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 256), np.sort(keys))
+        np.testing.assert_array_equal(bsg.radix.serial_radix_sort(keys, 65536), np.sort(keys))
+    finally:
+        L.bsg_debug_set_msd(prev)
+
+
+def test_hybrid_route_in_its_size_window(cuda, bsg):
+    """Left to itself the library takes the hybrid route (msd.cu) for full
+    sorts of a little more than 2^28 keys: 1.125 x 2^28 uniform keys run
+    through it (its kernels are launched and the LSD passes stay idle) and the
+    result equals an independent device sort; the same keys with one top-16
+    value heavier than a bucket may be are declined by its plan on the device
+    and sorted by the LSD passes."""
+    torch = cuda
+    from paper_1708_09495_b200 import _lib
+    L = _lib.lib()
+    ctx = _lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.bsg_debug_set_msd(-1) == 0  # auto
+    n = (1 << 28) + (1 << 25) + 12345
+    t = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.check(L.bsg_generate_uniform_device_u32(ctx.handle, t.data_ptr(), n, bsg.derive_seed(7, 1), st))
+    out = torch.empty_like(t)
+
+    def run_and_times():
+        ctx.set_timing(False)
+        ctx.set_timing(True)
+        _lib.check(L.bsg_radix_sort_u32(ctx.handle, t.data_ptr(), out.data_ptr(), n, 8, 1, st))
+        torch.cuda.synchronize()
+        r = {k: ctx.kernel_time(getattr(_lib, k)) for k in ("K_MSD_LOCAL", "K_ONESWEEP", "K_RELAXED_PASS", "K_FIRST_PASS")}
+        ctx.set_timing(False)
+        return r
+
+    def expect():
+        return torch.sort(t.view(torch.uint32).to(torch.int64))[0].to(torch.uint32).view(torch.int32)
+
+    kt = run_and_times()
+    assert torch.equal(out, expect())
+    assert kt["K_MSD_LOCAL"][1] == 1 and kt["K_MSD_LOCAL"][0] > 0.5, kt  # the local sort did the work ...
+    lsd_ms = kt["K_ONESWEEP"][0] + kt["K_RELAXED_PASS"][0] + kt["K_FIRST_PASS"][0]
+    assert lsd_ms < 0.2, kt  # ... and the LSD passes exited at once
+    t[: 10000] = (t[: 10000] & 0xFFFF) | 0x7FFF0000  # bucket 0x7FFF: 4608 + 10000 keys > capacity
+    out.zero_()
+    kt = run_and_times()
+    assert torch.equal(out, expect())
+    lsd_ms = kt["K_ONESWEEP"][0] + kt["K_RELAXED_PASS"][0] + kt["K_FIRST_PASS"][0]
+    assert kt["K_MSD_LOCAL"][0] < 0.2 and lsd_ms > 1.0, kt  # declined: the LSD passes sorted
+    del t, out
+    torch.cuda.empty_cache()
