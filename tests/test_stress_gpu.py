@@ -116,3 +116,51 @@ def test_register_networks_repeated(cuda, bsg):
                                                                ln, p, -1, None, 1, st))
                 got = out.view(torch.int32).to(torch.int64).view(num, ln) & 0xFFFFFFFF
                 assert torch.equal(got, ref), (ln, p, net)
+
+
+def test_full_sort_routes_agree_on_random_inputs(cuda, bsg):
+    """Every route a full sort may take -- strictly stable passes, K3f for pass
+    0, value-stable passes, the hybrid MSD route (forced) -- over random sizes
+    and key shapes that move the runs of equal low bits around (uniform, few
+    distinct keys, few distinct low/high halves, long constant runs, sorted,
+    byte-wise low entropy): all results equal torch.sort of the same keys."""
+    torch = cuda
+    L = bsg._lib.lib()
+    rng = np.random.default_rng(77)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    prev = (L.bsg_debug_set_small_sort(0), L.bsg_debug_set_first_pass(-1), L.bsg_debug_set_relaxed_passes(-1),
+            L.bsg_debug_set_msd(-1))
+
+    def make(kind, n):
+        u = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+        if kind == 0:
+            return u
+        if kind == 1:  # few distinct keys
+            return u[torch.randint(0, max(1, min(n, 37)), (n,), device="cuda", generator=g)]
+        if kind == 2:  # few distinct low halves
+            return (u & -65536) | (u & 0x0003)
+        if kind == 3:  # few distinct high halves, random low bits
+            return (u & 0xFFFF) | ((u >> 30) << 16)
+        if kind == 4:  # long constant runs
+            return torch.repeat_interleave(u[: max(1, n // 1000)], 1000)[:n].contiguous() if n >= 1000 else u
+        if kind == 5:  # already sorted
+            return torch.sort(u)[0]
+        return u & 0x03030303  # byte-wise low entropy
+
+    try:
+        sizes = [int(x) for x in rng.integers(1, 1 << 25, 10)] + [(1 << 24) + 1, (1 << 25) + 4097]
+        for i, n in enumerate(sizes):
+            t = make(i % 7, n)
+            n = t.numel()
+            ref = _dev_sort_ref(torch, t)
+            for first, relaxed, msd in ((0, 0, 1), (1, 0, 1), (1, 1, 1), (1, 1, 2)):
+                L.bsg_debug_set_first_pass(first)
+                L.bsg_debug_set_relaxed_passes(relaxed)
+                L.bsg_debug_set_msd(msd)
+                assert _eq(torch, _sort(bsg, torch, t), ref), (n, i % 7, first, relaxed, msd)
+            del t, ref
+    finally:
+        L.bsg_debug_set_small_sort(prev[0])
+        L.bsg_debug_set_first_pass(prev[1])
+        L.bsg_debug_set_relaxed_passes(prev[2])
+        L.bsg_debug_set_msd(prev[3])
