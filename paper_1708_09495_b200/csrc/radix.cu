@@ -3,23 +3,33 @@
 // Restates the count-sort round of radix.hpp:44-65 (histogram, exclusive
 // scan, stable forward scatter) and serial_radix_sort (radix.hpp:69-90) as
 // three kernels:
-//   K1 hist_kernel      -- one read of the keys, per-CTA shared-memory
-//                          histograms of every digit with per-thread run-length
-//                          aggregation (skewed inputs hit far fewer atomics),
-//                          flushed to per-chunk global bins.
+//   K1 hist_kernel      -- one read of the keys (16-byte loads), per-CTA
+//                          shared-memory histograms of every digit with a
+//                          private copy of every counter per lane (no bank
+//                          conflicts for uniform and all-equal keys alike),
+//                          reduced into per-chunk global bins.
 //   K2 scan_plan_kernel -- exclusive digit scans -> per-chunk output bases, and
 //                          a device-resident PassPlan that skips identity
 //                          passes (one digit value holds all n keys) and picks
 //                          the ping-pong buffers so the result lands in `out`
 //                          with no host round trip.
-//   K3 onesweep_kernel  -- one stable pass: TMA bulk load of an 8192-key tile
-//                          into shared memory, warp-striped match-any ranking
-//                          (original order inside a warp = item-major,
-//                          lane-minor, so ranks are stable), per-warp digit
-//                          counts -> early publication of the tile aggregate,
-//                          decoupled look-back across tiles per digit, then the
-//                          tile is staged in digit order in shared memory and
-//                          written out in digit runs (coalesced).
+//   K3 onesweep_kernel  -- one stable pass over persistent CTAs: TMA bulk
+//                          load of a 12288-key tile into shared memory (double
+//                          buffered), per-warp digit counts, early publication
+//                          of the tile aggregate, decoupled look-back across
+//                          tiles per digit, warp-striped stable ranking by a
+//                          bit-serial ballot multisplit straight into the
+//                          staged tile (original order inside a warp =
+//                          item-major, lane-minor), digit runs written out
+//                          coalesced.
+// Inside a FULL keys-only sort, whose intermediate states nobody sees:
+//   K3f first_pass_kernel -- pass 0: no order inside a digit run (shared-memory
+//                          cursors per lane quad, global run reservations, no
+//                          ballots, no look-back);
+//   K3r onesweep_kernel<...,4> -- passes over long runs of equal low bits:
+//                          value-stable ranking by one shared-memory atomic
+//                          per key, ballots only where a warp item straddles
+//                          a run boundary (rank_stage).
 // All counts/positions are 64-bit at the chunk level (a chunk is <= 2^29
 // keys so the 30-bit look-back payload never overflows).
 #include <algorithm>
