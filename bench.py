@@ -361,25 +361,33 @@ def run_single(args):
     torch.cuda.synchronize()
     nl = len(lanes)
     kp = nl * ke
-    start = torch.cuda.Event(enable_timing=True)
-    ends = [torch.cuda.Event(enable_timing=True) for _ in lanes]
-    start.record(stream)
-    for _, st_, _, _ in lanes[1:]:
-        st_.wait_event(start)
 
-    def worker(i):
-        c, st, hi, ho = lanes[i]
-        for _ in range(kp // nl):
-            lane_step(c, st, hi, ho)
-        ends[i].record(st)
+    def e2e_run():
+        start = torch.cuda.Event(enable_timing=True)
+        ends = [torch.cuda.Event(enable_timing=True) for _ in lanes]
+        start.record(stream)
+        for _, st_, _, _ in lanes[1:]:
+            st_.wait_event(start)
 
-    ths = [threading.Thread(target=worker, args=(i,)) for i in range(nl)]
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
-    torch.cuda.synchronize()
-    e2e_ms = max(start.elapsed_time(e) for e in ends) / kp
+        def worker(i):
+            c, st, hi, ho = lanes[i]
+            for _ in range(kp // nl):
+                lane_step(c, st, hi, ho)
+            ends[i].record(st)
+
+        ths = [threading.Thread(target=worker, args=(i,)) for i in range(nl)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        torch.cuda.synchronize()
+        return max(start.elapsed_time(e) for e in ends) / kp
+
+    # The hosts are shared VMs whose PCIe duplex rate moves from second to
+    # second: the whole timed e2e run (fill and drain included)
+    # is repeated and the MEDIAN run is reported, every run listed beside it.
+    e2e_runs = [e2e_run() for _ in range(max(1, args.e2e_repeats))]
+    e2e_ms = sorted(e2e_runs)[len(e2e_runs) // 2]
     ref_s = d_out.cpu().numpy().view(np.uint32)[:: max(1, n // 4096)]
     for _, _, _, ho in lanes[1:]:
         ok_e2e = ok_e2e and bool(np.array_equal(ho.numpy().view(np.uint32)[:: max(1, n // 4096)], ref_s))
@@ -390,7 +398,9 @@ def run_single(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic (reference generator, seeded)", "config": _config(1),
         "e2e": {"value": n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
-                "ms_per_step": e2e_ms, "in_flight": args.e2e_inflight,
+                "ms_per_step": e2e_ms, "in_flight": args.e2e_inflight, "steps": kp,
+                "runs_ms_per_step": e2e_runs, "reported": "median of the runs",
+
                 "path": "bsg_radix_sort_u32(BSG_MEM_HOST) from pinned host memory; host threads, each with "
                         "its own context/stream, so one step's D2H overlaps another step's H2D",
                 "serial_value": n / (e2e_serial_ms / 1e3), "serial_ms_per_step": e2e_serial_ms},
@@ -673,6 +683,8 @@ def main():
                     help="skip the C1/C3/C4/PR rows measured after the config-2 line")
     ap.add_argument("--e2e-inflight", type=int, default=4,
                     help="sorts in flight in the e2e measurement (host threads, one context/stream each)")
+    ap.add_argument("--e2e-repeats", type=int, default=3,
+                    help="repetitions of the whole timed e2e run; the median is reported")
     ap.add_argument("--e2e-steps", type=int, default=20,
                     help="e2e steps per lane (capped by --steps); total e2e steps = lanes x this")
     ap.add_argument("--pr-variant", choices=["A", "B", "P"], default="P",
