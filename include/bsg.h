@@ -139,8 +139,9 @@ int bsg_partition_owner_of(uint64_t n, int p, uint64_t pos);
  * final array is returned, as in the reference; the passes in between keep
  * the order by key VALUE that the next pass needs (K3f/K3r), not
  * positions among equal keys.  A round whose result is returned
- * (bsg_count_sort_round_u32, a rounds-limited bsg_parallel_radix_sort_u32) is
- * strictly stable. */
+ * (bsg_count_sort_round_u32, a rounds-limited bsg_parallel_radix_sort_u32, or
+ * one that returns RunStats, whose count matrices depend on it) is strictly
+ * stable. */
 int bsg_radix_sort_u32(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n,
                        int radix_log2, int mem_kind, void* stream);
 

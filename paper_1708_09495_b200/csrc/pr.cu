@@ -779,9 +779,15 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             launches += 3;
         }
         // every worker's local stable pass, stored at the global positions
-        // (sort_and_scatter + exchange + gather_slices), one segmented launch
+        // (sort_and_scatter + exchange + gather_slices), one segmented launch.
+        // A full run whose RunStats are not asked for returns only the sorted
+        // array, so its rounds may rank value-stably (radix.cu rank_stage).
+        // With RunStats every round is strictly stable: which of two keys
+        // equal in the low bits and the digit lands left of a block boundary
+        // decides the next round's count matrix, and the message counts must
+        // be the reference's.
         if (!add(launch_onesweep_seg(src, dst, n, p, bits, shift, reinterpret_cast<const uint64_t*>(base),
-                                     ctx->status.as<uint32_t>(), stream, skew, rounds * bits == 32)))
+                                     ctx->status.as<uint32_t>(), stream, skew, rounds * bits == 32 && !stats)))
             return cuda_fail(cudaGetLastError(), "pr fused pass");
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "pr round");
         if (stats) {
@@ -843,7 +849,8 @@ int run_parallel_radix_local(bsg_ctx* ctx, const uint32_t* in, uint32_t* out, ui
             // full runs: both sub-passes may rank value-stably (a block enters
             // the round ordered by its low `shift` bits, the second sub-pass by
             // its low shift + 8 bits)
-            const bool full_run = rounds * bits == 32;
+            // (without RunStats only: see the r <= 2^8 rounds above)
+            const bool full_run = rounds * bits == 32 && !stats;
             if (!add(launch_onesweep_seg(src, mid, n, p, 8, shift, reinterpret_cast<const uint64_t*>(bA),
                                          ctx->status.as<uint32_t>(), stream, skew, full_run)) ||
                 !add(launch_onesweep_seg(mid, S, n, p, 8, shift + 8, reinterpret_cast<const uint64_t*>(bB),

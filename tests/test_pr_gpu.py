@@ -458,33 +458,50 @@ def test_protocol_errors_raise_bsp_error(cuda, bsg):
 
 @pytest.mark.parametrize("relaxed", [0, 1])
 def test_full_run_value_stable_rounds(cuda, bsg, orc, relaxed):
-    """The rounds of a FULL in-process PR4/PR2 run (no rounds limit: intermediate
-    states are not returned) may rank value-stably; a rounds-limited run always
-    ranks strictly.  Both settings must give the oracle's output and RunStats,
-    below and above the 2^24 keys the relaxation starts at, ragged blocks,
-    duplicate-heavy and skewed keys; rounds-limited states stay bit-exact
-    whatever the setting."""
+    """The rounds of a FULL in-process PR4/PR2 run whose RunStats are not asked
+    for (C ABI, stats = NULL: only the sorted array is returned) may rank
+    value-stably from 2^24 keys on; a run that returns RunStats or is
+    rounds-limited always ranks strictly, so its count matrices -- and message
+    counts -- are the reference's.  Both settings must give the oracle's
+    output, below and above 2^24 keys, for ragged blocks, duplicate-heavy and
+    skewed keys; RunStats and rounds-limited states stay bit-exact whatever
+    the setting."""
+    torch = cuda
     L = bsg._lib.lib()
+    ctx = bsg._lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
     prev = L.bsg_debug_set_relaxed_passes(relaxed)
+
+    def sort_no_stats(keys, p, bits):
+        t = torch.from_numpy(keys.view(np.int32)).cuda()
+        out = torch.empty_like(t)
+        assert L.bsg_parallel_radix_sort_u32(ctx.handle, t.data_ptr(), out.data_ptr(), keys.size, p, bits, -1, None,
+                                             1, st) == 0, bsg._lib.last_error()
+        torch.cuda.synchronize()
+        return out.cpu().numpy().view(np.uint32)
+
     try:
-        for n, ps in (((1 << 17) + 5, (1, 3, 8)), ((1 << 22) + 5, (3, 8)), ((1 << 24) + 3, (2, 5))):
+        for n, ps in (((1 << 17) + 5, (1, 3, 8)), ((1 << 22) + 5, (3, 8)), ((1 << 24) + 3, (2, 5)),
+                      ((1 << 25) + 1001, (8,))):
             keys = orc.generate_uniform_keys(n, 17 * n + relaxed)
             exp = np.sort(keys)
             for p in ps:
-                for radix in (256, 65536):
-                    res = pr(bsg, keys, p, radix)
-                    np.testing.assert_array_equal(res.output, exp)
-                    if n <= (1 << 22) + 5:
-                        _, est = orc.parallel_radix(keys, p, radix)
+                for bits in (8, 16):
+                    np.testing.assert_array_equal(sort_no_stats(keys, p, bits), exp)
+                    if n <= (1 << 24) + 3:
+                        res = pr(bsg, keys, p, 1 << bits)  # with RunStats: strictly stable rounds
+                        np.testing.assert_array_equal(res.output, exp)
+                        _, est = orc.parallel_radix(keys, p, 1 << bits)
                         assert res.stats == est
         n = (1 << 24) + 77
         base = orc.generate_uniform_keys(n, 71)
         rng = np.random.default_rng(3)
         for keys in ((base & 0xFFFF0007).astype(np.uint32), rng.choice(base[:500], n).astype(np.uint32),
                      np.minimum(rng.zipf(1.1, n), 0xFFFFFFFF).astype(np.uint32)):
+            exp = np.sort(keys)
             for p in (2, 7):
-                np.testing.assert_array_equal(pr(bsg, keys, p, 256).output, np.sort(keys))
-                np.testing.assert_array_equal(pr(bsg, keys, p, 65536).output, np.sort(keys))
+                np.testing.assert_array_equal(sort_no_stats(keys, p, 8), exp)
+                np.testing.assert_array_equal(sort_no_stats(keys, p, 16), exp)
         keys = orc.generate_uniform_keys((1 << 20) + 9, 5)
         state = keys
         for r in range(1, 4):
